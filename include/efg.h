@@ -1,0 +1,118 @@
+/*
+ * efg.h -- C ABI of the B200-native Expected Force engine (libefg.so).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types except an opaque
+ * `void*` stream.  Status codes: 0 ok, 1 invalid argument (-> ValueError),
+ * 2 CUDA error, 3 NCCL error, 4 out of memory.  efg_last_error() returns the
+ * calling thread's last message.  Caller owns every input and output buffer
+ * (outputs pre-allocated, e.g. np.empty); the library owns device memory
+ * through the opaque context.  Calls on one context are serialised by an
+ * internal mutex.
+ *
+ * Each entry point cites the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/efgraph/).
+ */
+#ifndef EFG_H
+#define EFG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EFG_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define EFG_API __attribute__((visibility("default")))
+#else
+#define EFG_API
+#endif
+
+typedef struct efg_ctx efg_ctx;
+
+/* mode: expected_force.py:114-120 (`ef(g, mode=...)`) */
+enum { EFG_MODE_CLUSTER_CENTRIC = 0, EFG_MODE_VERTEX_CENTRIC = 1 };
+
+/* engine: which device algorithm evaluates the per-seed cluster sums.
+ *  FACTORIZED -- degree-histogram factorisation + triangle corrections (default)
+ *  DIRECT     -- per-seed enumeration of every star and chain (original formulation)
+ *  ALG1       -- Algorithm-1 middle-triplet scatter, cross-check */
+enum { EFG_ENGINE_AUTO = 0, EFG_ENGINE_FACTORIZED = 1, EFG_ENGINE_DIRECT = 2, EFG_ENGINE_ALG1 = 3 };
+
+typedef struct efg_stats {
+    double ms_device;            /* device time of the whole call (CUDA events) */
+    double ms_prepare;           /* degrees, neighbour degrees, F table, orientation */
+    double ms_enumerate;         /* cluster sums (the hot kernels) */
+    double ms_h2d;               /* host->device copies (host-buffer entry points) */
+    double ms_d2h;               /* device->host copies */
+    int64_t clusters_processed;  /* reference semantics: sum C(d,2), x3 in vertex mode */
+    int64_t cluster_visits;      /* clusters represented: 3 * sum C(d,2) */
+    int64_t terms;               /* pair terms evaluated by the engine */
+    int64_t bytes_alg;           /* 16*sumC + 64*m + 33*n */
+    int64_t launches;            /* kernels launched by the library in this call */
+    int64_t h2d_bytes, d2h_bytes;
+    int32_t engine;
+    int32_t dmax;
+} efg_stats;
+
+EFG_API int efg_abi_version(void);
+EFG_API const char *efg_last_error(void);
+
+/* Context on CUDA device `device` with a library-owned non-blocking stream. */
+EFG_API int efg_create(int device, efg_ctx **out);
+EFG_API int efg_destroy(efg_ctx *ctx);
+/* Use a caller-provided cudaStream_t (NULL restores the library's own). */
+EFG_API int efg_set_stream(efg_ctx *ctx, void *stream);
+EFG_API int efg_synchronize(efg_ctx *ctx);
+
+/* K1: replaces graph.py:147-190 `build_graph(edges)`.  `edges` is k host
+ * (u, v) int64 pairs.  The CSR stays resident in the context; sizes out. */
+EFG_API int efg_build_graph(efg_ctx *ctx, const int64_t *edges, int64_t k, int64_t *n_out, int64_t *m_out);
+/* Copy the resident CSR out: offsets[n+1], neighbors[2m], orig_ids[n]
+ * (the Graph fields of graph.py:34-57). */
+EFG_API int efg_fetch_graph(efg_ctx *ctx, int64_t *offsets, int32_t *neighbors, int64_t *orig_ids);
+/* Device pointers of the resident CSR (valid until the next build). */
+EFG_API int efg_graph_device(efg_ctx *ctx, const int64_t **d_offsets, const int32_t **d_neighbors,
+                     int64_t *n_out, int64_t *m_out);
+
+/* Replaces expected_force.py:114-120 `ef`, :138-174 `ef_cluster_centric` and
+ * :345-418 `ef_vertex_centric` for a host CSR (offsets[n+1], neighbors[2m]).
+ * Outputs (host, length n): ef f64, cluster_total i64, flags u8;
+ * *clusters_processed per the reference mode semantics.  T_out (exact
+ * int64 sum w*d) and W_out (f64 sum w*d*ln d) are optional (NULL). */
+EFG_API int efg_expected_force(efg_ctx *ctx, const int64_t *offsets, const int32_t *neighbors, int64_t n,
+                       int32_t mode, int32_t engine, double *ef, int64_t *cluster_total,
+                       uint8_t *flags, int64_t *clusters_processed, int64_t *T_out, double *W_out,
+                       efg_stats *stats);
+
+/* Device-resident variant: every pointer is device memory; computes seeds
+ * [seed_lo, seed_hi) of the graph and writes outputs at index seed - seed_lo.
+ * Asynchronous on the context stream when stats == NULL. */
+EFG_API int efg_expected_force_device(efg_ctx *ctx, const int64_t *d_offsets, const int32_t *d_neighbors,
+                              int64_t n, int64_t seed_lo, int64_t seed_hi, int32_t engine,
+                              double *d_ef, int64_t *d_cluster_total, uint8_t *d_flags,
+                              int64_t *d_T, double *d_W, efg_stats *stats);
+
+/* K2: balanced contiguous seed shards for `parts` devices by the engine's
+ * per-seed work prefix (bounds_out[parts+1], host).  Independent of which
+ * device runs which shard, so results are identical for any device count. */
+EFG_API int efg_shard_bounds(efg_ctx *ctx, const int64_t *d_offsets, const int32_t *d_neighbors, int64_t n,
+                     int32_t engine, int32_t parts, int64_t *bounds_out);
+
+/* K5: key-node ranking -- the k largest EF values, ties to the smaller id,
+ * i.e. np.lexsort((ids, -ef))[:k] (cf. analysis.py:101, :240).  ids_out is
+ * host int64[k].  The _device form reads a device ef array. */
+EFG_API int efg_topk(efg_ctx *ctx, const double *ef, int64_t n, int64_t k, int64_t *ids_out);
+EFG_API int efg_topk_device(efg_ctx *ctx, const double *d_ef, int64_t n, int64_t k, int64_t *ids_out);
+
+/* Pinned (page-locked) host memory for zero-staging copies; the Python layer
+ * allocates Graph arrays and EF outputs here. */
+EFG_API int efg_host_alloc(int64_t bytes, void **out);
+EFG_API int efg_host_free(void *p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* EFG_H */

@@ -1,0 +1,360 @@
+// C ABI of libefg.so (include/efg.h): status codes, thread-local last error,
+// per-context serialisation, host<->device staging and timing.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "efg_internal.cuh"
+
+namespace efg {
+thread_local int64_t g_launches = 0;
+
+Context::~Context() {
+  for (auto& kv : bufs) kv.second.release();
+  csr.b_off.release();
+  csr.b_nbr.release();
+  csr.b_orig.release();
+  for (auto& e : ev)
+    if (e) cudaEventDestroy(e);
+  if (own_stream && stream) cudaStreamDestroy(stream);
+}
+}  // namespace efg
+
+using efg::Context;
+
+struct efg_ctx {
+  Context c;
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+template <class F>
+int guarded(efg_ctx* ctx, F&& body) {
+  if (!ctx) return fail(efg::EFG_INVALID, "null efg context");
+  std::lock_guard<std::mutex> lock(ctx->c.mu);
+  try {
+    cudaError_t e = cudaSetDevice(ctx->c.device);
+    if (e != cudaSuccess) return fail(efg::EFG_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    body(ctx->c);
+    g_last_error.clear();
+    return efg::EFG_OK;
+  } catch (const efg::Error& err) {
+    return fail(err.code, err.what());
+  } catch (const std::bad_alloc&) {
+    return fail(efg::EFG_OOM, "host out of memory");
+  } catch (const std::exception& err) {
+    return fail(efg::EFG_CUDA, err.what());
+  }
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  EFG_CUDA_CHECK(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
+int resolve_engine(int mode, int engine) {
+  if (engine == EFG_ENGINE_AUTO)
+    return mode == EFG_MODE_VERTEX_CENTRIC ? EFG_ENGINE_DIRECT : EFG_ENGINE_FACTORIZED;
+  return engine;
+}
+
+// Run one EF pass over device CSR `g` for seeds r; outputs device, index = seed - r.lo.
+void run_engine(Context& c, const efg::CSRView& g, efg::SeedRange r, int engine, double* ef, int64_t* tot,
+                uint8_t* fl, int64_t* T, double* W, efg_stats* st) {
+  EFG_REQUIRE(engine == EFG_ENGINE_FACTORIZED || engine == EFG_ENGINE_DIRECT,
+              "unknown engine " + std::to_string(engine));
+  efg::Prepared P;
+  cudaEvent_t* ev = c.ev;
+  if (st) EFG_CUDA_CHECK(cudaEventRecord(ev[2], c.stream));
+  efg::prepare(c, g, engine == EFG_ENGINE_FACTORIZED, P);
+  if (st) EFG_CUDA_CHECK(cudaEventRecord(ev[3], c.stream));
+  if (engine == EFG_ENGINE_FACTORIZED)
+    efg::ef_factorized(c, P, r, ef, tot, fl, T, W, st);
+  else
+    efg::ef_direct(c, P, r, ef, tot, fl, T, W, st);
+  if (st) {
+    EFG_CUDA_CHECK(cudaEventRecord(ev[4], c.stream));
+    EFG_CUDA_CHECK(cudaEventSynchronize(ev[4]));
+    st->ms_prepare = elapsed(ev[2], ev[3]);
+    st->ms_enumerate = elapsed(ev[3], ev[4]);
+    st->dmax = P.dmax;
+    st->cluster_visits = 3 * P.sum_c2;
+    st->clusters_processed = P.sum_c2;
+    st->bytes_alg = 16 * P.sum_c2 + 32 * g.m2 + 33 * g.n;
+    st->engine = engine;
+  }
+}
+
+template <class T>
+T* stage(Context& c, const char* name, const T* host, int64_t count) {
+  T* d = c.buf(name).as<T>(count > 0 ? count : 1);
+  if (count > 0) EFG_CUDA_CHECK(cudaMemcpyAsync(d, host, count * sizeof(T), cudaMemcpyHostToDevice, c.stream));
+  return d;
+}
+
+}  // namespace
+
+extern "C" {
+
+int efg_abi_version(void) { return EFG_ABI_VERSION; }
+
+const char* efg_last_error(void) { return g_last_error.c_str(); }
+
+int efg_create(int device, efg_ctx** out) {
+  if (!out) return fail(efg::EFG_INVALID, "null output pointer");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess) return fail(efg::EFG_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  if (device < 0 || device >= ndev) return fail(efg::EFG_INVALID, "device index out of range");
+  efg_ctx* ctx = new (std::nothrow) efg_ctx;
+  if (!ctx) return fail(efg::EFG_OOM, "host out of memory");
+  ctx->c.device = device;
+  int rc = guarded(ctx, [&](Context& c) {
+    EFG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+    c.own_stream = true;
+    for (auto& x : c.ev) EFG_CUDA_CHECK(cudaEventCreate(&x));
+    EFG_CUDA_CHECK(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
+  });
+  if (rc) {
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return 0;
+}
+
+int efg_destroy(efg_ctx* ctx) {
+  if (!ctx) return 0;
+  cudaSetDevice(ctx->c.device);
+  if (ctx->c.stream) cudaStreamSynchronize(ctx->c.stream);
+  delete ctx;
+  return 0;
+}
+
+int efg_set_stream(efg_ctx* ctx, void* stream) {
+  return guarded(ctx, [&](Context& c) {
+    if (c.own_stream && c.stream) {
+      EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      EFG_CUDA_CHECK(cudaStreamDestroy(c.stream));
+    }
+    if (stream) {
+      c.stream = static_cast<cudaStream_t>(stream);
+      c.own_stream = false;
+    } else {
+      EFG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking));
+      c.own_stream = true;
+    }
+  });
+}
+
+int efg_synchronize(efg_ctx* ctx) {
+  return guarded(ctx, [&](Context& c) { EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream)); });
+}
+
+int efg_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return fail(efg::EFG_INVALID, "bad host_alloc arguments");
+  cudaError_t e = cudaHostAlloc(out, bytes > 0 ? (size_t)bytes : 1, cudaHostAllocPortable);
+  if (e != cudaSuccess) return fail(efg::EFG_OOM, std::string("cudaHostAlloc: ") + cudaGetErrorString(e));
+  return 0;
+}
+
+int efg_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+  return 0;
+}
+
+int efg_build_graph(efg_ctx* ctx, const int64_t* edges, int64_t k, int64_t* n_out, int64_t* m_out) {
+  if (k < 0 || (k > 0 && !edges)) return fail(efg::EFG_INVALID, "bad edge array");
+  return guarded(ctx, [&](Context& c) {
+    const int64_t* d_edges = stage(c, "edges_in", edges, 2 * k);
+    efg::build_csr_device(c, d_edges, k, c.csr);
+    EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    if (n_out) *n_out = c.csr.n;
+    if (m_out) *m_out = c.csr.m;
+  });
+}
+
+int efg_fetch_graph(efg_ctx* ctx, int64_t* offsets, int32_t* neighbors, int64_t* orig_ids) {
+  return guarded(ctx, [&](Context& c) {
+    const int64_t n = c.csr.n, m = c.csr.m;
+    if (offsets) {
+      if (n == 0) {
+        offsets[0] = 0;
+      } else {
+        EFG_CUDA_CHECK(cudaMemcpyAsync(offsets, c.csr.offsets, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+      }
+    }
+    if (neighbors && m) EFG_CUDA_CHECK(cudaMemcpyAsync(neighbors, c.csr.nbr, 2 * m * sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+    if (orig_ids && n) EFG_CUDA_CHECK(cudaMemcpyAsync(orig_ids, c.csr.orig_ids, n * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int efg_graph_device(efg_ctx* ctx, const int64_t** d_offsets, const int32_t** d_neighbors, int64_t* n_out,
+                     int64_t* m_out) {
+  return guarded(ctx, [&](Context& c) {
+    if (d_offsets) *d_offsets = c.csr.offsets;
+    if (d_neighbors) *d_neighbors = c.csr.nbr;
+    if (n_out) *n_out = c.csr.n;
+    if (m_out) *m_out = c.csr.m;
+  });
+}
+
+int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neighbors, int64_t n, int32_t mode,
+                       int32_t engine, double* ef, int64_t* cluster_total, uint8_t* flags,
+                       int64_t* clusters_processed, int64_t* T_out, double* W_out, efg_stats* stats) {
+  if (n < 0 || !offsets) return fail(efg::EFG_INVALID, "bad offsets");
+  if (mode != EFG_MODE_CLUSTER_CENTRIC && mode != EFG_MODE_VERTEX_CENTRIC)
+    return fail(efg::EFG_INVALID, "unknown mode " + std::to_string(mode) + "; expected cluster_centric or vertex_centric");
+  if (n > 0 && (!ef || !cluster_total || !flags)) return fail(efg::EFG_INVALID, "null output array");
+  return guarded(ctx, [&](Context& c) {
+    efg::g_launches = 0;
+    efg_stats local{};
+    efg_stats* st = stats ? stats : &local;
+    std::memset(st, 0, sizeof *st);
+    const int eng = resolve_engine(mode, engine);
+    if (n == 0) {
+      if (clusters_processed) *clusters_processed = 0;
+      st->engine = eng;
+      return;
+    }
+    const int64_t m2 = offsets[n] - offsets[0];
+    EFG_REQUIRE(offsets[0] == 0 && m2 >= 0 && m2 % 2 == 0, "offsets must start at 0 and cover 2m entries");
+    EFG_REQUIRE(n < (int64_t(1) << 31), "graph too large: n exceeds int32 id space");
+    cudaEvent_t* ev = c.ev;
+    EFG_CUDA_CHECK(cudaEventRecord(ev[0], c.stream));
+    efg::CSRView g;
+    g.n = n;
+    g.m2 = m2;
+    g.offsets = stage(c, "h_offsets", offsets, n + 1);
+    g.nbr = stage(c, "h_nbr", neighbors, m2);
+    EFG_CUDA_CHECK(cudaEventRecord(ev[1], c.stream));
+    double* d_ef = c.buf("o_ef").as<double>(n);
+    int64_t* d_tot = c.buf("o_tot").as<int64_t>(n);
+    uint8_t* d_fl = c.buf("o_fl").as<uint8_t>(n);
+    int64_t* d_T = T_out ? c.buf("o_T").as<int64_t>(n) : nullptr;
+    double* d_W = W_out ? c.buf("o_W").as<double>(n) : nullptr;
+    run_engine(c, g, efg::SeedRange{0, n}, eng, d_ef, d_tot, d_fl, d_T, d_W, st);
+    EFG_CUDA_CHECK(cudaEventRecord(ev[5], c.stream));
+    EFG_CUDA_CHECK(cudaMemcpyAsync(ef, d_ef, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaMemcpyAsync(cluster_total, d_tot, n * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaMemcpyAsync(flags, d_fl, n, cudaMemcpyDeviceToHost, c.stream));
+    if (T_out) EFG_CUDA_CHECK(cudaMemcpyAsync(T_out, d_T, n * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    if (W_out) EFG_CUDA_CHECK(cudaMemcpyAsync(W_out, d_W, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaEventRecord(ev[6], c.stream));
+    EFG_CUDA_CHECK(cudaEventSynchronize(ev[6]));
+    st->ms_h2d = elapsed(ev[0], ev[1]);
+    st->ms_d2h = elapsed(ev[5], ev[6]);
+    st->ms_device = elapsed(ev[0], ev[6]);
+    st->h2d_bytes = (n + 1) * 8 + m2 * 4;
+    st->d2h_bytes = n * 17 + (T_out ? n * 8 : 0) + (W_out ? n * 8 : 0);
+    if (mode == EFG_MODE_VERTEX_CENTRIC) st->clusters_processed = st->cluster_visits;
+    if (clusters_processed) *clusters_processed = st->clusters_processed;
+    st->launches = efg::g_launches;
+  });
+}
+
+int efg_expected_force_device(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n,
+                              int64_t seed_lo, int64_t seed_hi, int32_t engine, double* d_ef,
+                              int64_t* d_cluster_total, uint8_t* d_flags, int64_t* d_T, double* d_W,
+                              efg_stats* stats) {
+  if (n < 0 || seed_lo < 0 || seed_hi < seed_lo || seed_hi > n)
+    return fail(efg::EFG_INVALID, "bad seed range");
+  return guarded(ctx, [&](Context& c) {
+    efg::g_launches = 0;
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    const int eng = resolve_engine(EFG_MODE_CLUSTER_CENTRIC, engine);
+    if (n == 0 || seed_hi == seed_lo) return;
+    int64_t off_n = 0;
+    EFG_CUDA_CHECK(cudaMemcpyAsync(&off_n, d_offsets + n, sizeof off_n, cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    efg::CSRView g;
+    g.n = n;
+    g.m2 = off_n;
+    g.offsets = d_offsets;
+    g.nbr = d_neighbors;
+    if (stats) EFG_CUDA_CHECK(cudaEventRecord(c.ev[0], c.stream));
+    run_engine(c, g, efg::SeedRange{seed_lo, seed_hi}, eng, d_ef, d_cluster_total, d_flags, d_T, d_W, stats);
+    if (stats) {
+      EFG_CUDA_CHECK(cudaEventRecord(c.ev[6], c.stream));
+      EFG_CUDA_CHECK(cudaEventSynchronize(c.ev[6]));
+      stats->ms_device = elapsed(c.ev[0], c.ev[6]);
+      stats->launches = efg::g_launches;
+    }
+  });
+}
+
+int efg_shard_bounds(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n, int32_t engine,
+                     int32_t parts, int64_t* bounds_out) {
+  if (parts < 1 || !bounds_out || n < 0) return fail(efg::EFG_INVALID, "bad shard arguments");
+  return guarded(ctx, [&](Context& c) {
+    const int eng = resolve_engine(EFG_MODE_CLUSTER_CENTRIC, engine);
+    bounds_out[0] = 0;
+    for (int p = 1; p <= parts; ++p) bounds_out[p] = n;
+    if (n == 0) return;
+    int64_t off_n = 0;
+    EFG_CUDA_CHECK(cudaMemcpyAsync(&off_n, d_offsets + n, sizeof off_n, cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    efg::CSRView g{n, off_n, d_offsets, d_neighbors};
+    efg::Prepared P;
+    efg::prepare(c, g, eng == EFG_ENGINE_FACTORIZED, P);
+    int64_t* work = c.buf("k2_work").as<int64_t>(n);
+    if (eng == EFG_ENGINE_FACTORIZED)
+      efg::factorized_work(c, P, work);
+    else
+      efg::direct_work(c, P, work);
+    std::vector<int64_t> h(n);
+    EFG_CUDA_CHECK(cudaMemcpyAsync(h.data(), work, n * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    // inclusive prefix; cut at p * total / parts (first seed whose prefix reaches the target)
+    long double total = 0;
+    for (int64_t v = 0; v < n; ++v) total += h[v];
+    long double acc = 0;
+    int p = 1;
+    for (int64_t v = 0; v < n && p < parts; ++v) {
+      acc += h[v];
+      while (p < parts && acc >= total * p / parts) bounds_out[p++] = v + 1;
+    }
+    for (; p < parts; ++p) bounds_out[p] = n;
+    for (p = 1; p <= parts; ++p) bounds_out[p] = std::max(bounds_out[p], bounds_out[p - 1]);
+  });
+}
+
+int efg_topk_device(efg_ctx* ctx, const double* d_ef, int64_t n, int64_t k, int64_t* ids_out) {
+  if (n < 0 || k < 0 || (k > 0 && !ids_out)) return fail(efg::EFG_INVALID, "bad topk arguments");
+  return guarded(ctx, [&](Context& c) {
+    const int64_t kk = std::min(k, n);
+    if (kk == 0) return;
+    int64_t* d_ids = c.buf("t_out").as<int64_t>(kk);
+    efg::topk_device(c, d_ef, n, kk, d_ids);
+    EFG_CUDA_CHECK(cudaMemcpyAsync(ids_out, d_ids, kk * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int efg_topk(efg_ctx* ctx, const double* ef, int64_t n, int64_t k, int64_t* ids_out) {
+  if (n < 0 || k < 0 || (n > 0 && !ef) || (k > 0 && !ids_out)) return fail(efg::EFG_INVALID, "bad topk arguments");
+  return guarded(ctx, [&](Context& c) {
+    const int64_t kk = std::min(k, n);
+    if (kk == 0) return;
+    const double* d_ef = stage(c, "t_in", ef, n);
+    int64_t* d_ids = c.buf("t_out").as<int64_t>(kk);
+    efg::topk_device(c, d_ef, n, kk, d_ids);
+    EFG_CUDA_CHECK(cudaMemcpyAsync(ids_out, d_ids, kk * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// Shared helpers for the efg sm_100a kernels (no torch types anywhere).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace efg {
+
+// Status codes of the C ABI (include/efg.h).
+enum Status : int {
+  EFG_OK = 0,
+  EFG_INVALID = 1,   // -> ValueError
+  EFG_CUDA = 2,      // -> OSError subclass (device error)
+  EFG_NCCL = 3,
+  EFG_OOM = 4,
+};
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define EFG_CUDA_CHECK(expr)                                                        \
+  do {                                                                              \
+    cudaError_t _e = (expr);                                                        \
+    if (_e != cudaSuccess) {                                                        \
+      throw ::efg::Error(_e == cudaErrorMemoryAllocation ? ::efg::EFG_OOM            \
+                                                         : ::efg::EFG_CUDA,          \
+                         std::string(#expr) + ": " + cudaGetErrorString(_e) +        \
+                             " (" __FILE__ ":" + std::to_string(__LINE__) + ")");    \
+    }                                                                               \
+  } while (0)
+
+#define EFG_REQUIRE(cond, msg)                                                      \
+  do {                                                                              \
+    if (!(cond)) throw ::efg::Error(::efg::EFG_INVALID, (msg));                      \
+  } while (0)
+
+constexpr int kWarp = 32;
+constexpr int kNumSMs = 148;   // B200; queried at runtime as well
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Grow-only device scratch buffer owned by a context.
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void* get(size_t need) {
+    if (need == 0) need = 16;
+    if (need > bytes) {
+      if (p) EFG_CUDA_CHECK(cudaFree(p));
+      p = nullptr;
+      bytes = 0;
+      size_t want = need + need / 8;
+      EFG_CUDA_CHECK(cudaMalloc(&p, want));
+      bytes = want;
+    }
+    return p;
+  }
+  template <class T>
+  T* as(size_t count) { return static_cast<T*>(get(count * sizeof(T))); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+};
+
+// Launch-count bookkeeping (stats.launches); every kernel launch in the
+// library goes through EFG_LAUNCH so the count is exact.
+extern thread_local int64_t g_launches;
+#define EFG_LAUNCH(kernel, grid, block, smem, stream, ...)                         \
+  do {                                                                              \
+    if ((grid) > 0) {                                                               \
+      kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                   \
+      EFG_CUDA_CHECK(cudaGetLastError());                                           \
+      ++::efg::g_launches;                                                          \
+    }                                                                               \
+  } while (0)
+
+}  // namespace efg

@@ -1,0 +1,87 @@
+// Internal (C++) interfaces between the efg translation units.
+#pragma once
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "common.cuh"
+#include "../../include/efg.h"
+
+namespace efg {
+
+// Device-resident CSR (Graph arrays of efgraph/graph.py:34-57).
+struct DeviceCSR {
+  int64_t n = 0, m = 0;
+  int64_t* offsets = nullptr;   // [n+1]
+  int32_t* nbr = nullptr;       // [2m], strictly ascending per row
+  int64_t* orig_ids = nullptr;  // [n]
+  DevBuf b_off, b_nbr, b_orig;
+  void alloc(int64_t n_, int64_t m_) {
+    offsets = b_off.as<int64_t>(n_ + 1);
+    nbr = b_nbr.as<int32_t>(2 * m_ > 0 ? 2 * m_ : 1);
+    orig_ids = b_orig.as<int64_t>(n_ > 0 ? n_ : 1);
+  }
+};
+
+struct Context {
+  int device = 0;
+  int num_sms = kNumSMs;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::map<std::string, DevBuf> bufs;
+  std::mutex mu;
+  cudaEvent_t ev[16] = {};
+  DeviceCSR csr;  // resident graph of efg_build_graph / efg_rmat_build
+  DevBuf& buf(const std::string& name) { return bufs[name]; }
+  ~Context();
+};
+
+// Read-only view of a CSR that some caller owns (device pointers).
+struct CSRView {
+  int64_t n = 0, m2 = 0;                 // m2 = 2m adjacency entries
+  const int64_t* offsets = nullptr;
+  const int32_t* nbr = nullptr;
+};
+
+// Per-call derived arrays (all device pointers into context scratch).
+struct Prepared {
+  CSRView g;
+  int32_t dmax = 0;
+  int64_t sum_c2 = 0;           // sum_v C(dv, 2) = cluster_count (graph.py:249-255)
+  int32_t* deg = nullptr;       // [n]
+  int32_t* nd = nullptr;        // [2m]  degree of each adjacency entry
+  int64_t* s1 = nullptr;        // [n]   sum of neighbour degrees
+  double* ftab = nullptr;       // [3*dmax+8]  F[d] = d ln d (0 for d = 0)
+  int64_t ftab_len = 0;
+  // degree-ordered orientation: j in Adj+(i) iff (d_j, j) > (d_i, i)
+  int32_t* dplus = nullptr;     // [n]
+  int64_t* offp = nullptr;      // [n+1]
+  int2* adjp = nullptr;         // [m]  (j, d_j), ascending j
+};
+
+struct SeedRange {
+  int64_t lo = 0, hi = 0;
+};
+
+// csr_build.cu
+void build_csr_device(Context& ctx, const int64_t* d_edges, int64_t k, DeviceCSR& out);
+
+// prep.cu
+void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P);
+
+// ef_factor.cu -- factorised cluster-centric engine
+void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* total, uint8_t* flags,
+                   int64_t* T_out, double* W_out, efg_stats* st);
+
+// ef_direct.cu -- direct per-seed enumeration (original formulation)
+void ef_direct(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* total, uint8_t* flags,
+               int64_t* T_out, double* W_out, efg_stats* st);
+
+// K2 -- per-seed work estimates (int64 [n]) used for balanced sharding
+void factorized_work(Context& ctx, Prepared& P, int64_t* d_work);
+void direct_work(Context& ctx, Prepared& P, int64_t* d_work);
+
+// topk.cu -- K5
+void topk_device(Context& ctx, const double* d_ef, int64_t n, int64_t k, int64_t* d_ids_out);
+
+}  // namespace efg

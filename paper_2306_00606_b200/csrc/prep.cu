@@ -1,0 +1,139 @@
+// Per-call preparation of the arrays every EF engine reads.
+//
+// Reference counterparts: g.degrees() (graph.py:63-65), the key span / degree
+// bound (expected_force.py:177-180: cluster degree < 3*dmax), and the
+// internal-edge test structure (_und_edge_codes + _edge_mask,
+// expected_force.py:183-197), which is replaced here by a degree-ordered
+// orientation of the CSR: each undirected edge appears once, in the list of
+// its lower-ranked endpoint, so every triangle is discovered exactly once per
+// member seed.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "efg_internal.cuh"
+
+namespace efg {
+
+namespace {
+
+__global__ void k_deg(const int64_t* __restrict__ offsets, int64_t n, int32_t* __restrict__ deg) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v < n) deg[v] = (int32_t)(offsets[v + 1] - offsets[v]);
+}
+
+// F[d] = d * ln d, the per-cluster term of W (expected_force.py:318-321 uses
+// (c*d)*ln d per histogram row; per cluster c = 1).
+__global__ void k_ftab(double* __restrict__ F, int64_t len) {
+  int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (d < len) F[d] = d > 0 ? (double)d * log((double)d) : 0.0;
+}
+
+__global__ void k_nd(const int32_t* __restrict__ nbr, int64_t m2, const int32_t* __restrict__ deg,
+                     int32_t* __restrict__ nd) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < m2) nd[e] = __ldg(deg + nbr[e]);
+}
+
+__device__ __forceinline__ bool ranks_above(int32_t dj, int32_t j, int32_t di, int32_t i) {
+  return dj > di || (dj == di && j > i);
+}
+
+// Warp per row: s1[v] = sum of neighbour degrees; dplus[v] = |Adj+(v)|.
+__global__ void k_row_sums(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
+                           const int32_t* __restrict__ nd, int64_t n, int64_t* __restrict__ s1,
+                           int64_t* __restrict__ dplus) {
+  const int lane = threadIdx.x & 31;
+  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (v >= n) return;
+  int64_t b = offsets[v], e = offsets[v + 1];
+  int32_t dv = (int32_t)(e - b);
+  int64_t s = 0;
+  int cnt = 0;
+  for (int64_t p = b + lane; p < e; p += 32) {
+    int32_t dj = nd[p];
+    s += dj;
+    cnt += ranks_above(dj, nbr[p], dv, (int32_t)v);
+  }
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if (lane == 0) {
+    s1[v] = s;
+    dplus[v] = cnt;
+  }
+}
+
+// Warp per row: ordered compaction of Adj+(v) as packed (j, d_j).
+__global__ void k_fill_adjp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
+                            const int32_t* __restrict__ nd, int64_t n, const int64_t* __restrict__ offp,
+                            int2* __restrict__ adjp) {
+  const int lane = threadIdx.x & 31;
+  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (v >= n) return;
+  int64_t b = offsets[v], e = offsets[v + 1];
+  int32_t dv = (int32_t)(e - b);
+  int64_t out = offp[v];
+  for (int64_t p0 = b; p0 < e; p0 += 32) {
+    int64_t p = p0 + lane;
+    int32_t j = 0, dj = 0;
+    bool take = false;
+    if (p < e) {
+      j = nbr[p];
+      dj = nd[p];
+      take = ranks_above(dj, j, dv, (int32_t)v);
+    }
+    unsigned mask = __ballot_sync(0xffffffffu, take);
+    if (take) adjp[out + __popc(mask & ((1u << lane) - 1))] = make_int2(j, dj);
+    out += __popc(mask);
+  }
+}
+
+struct Choose2 {
+  __host__ __device__ int64_t operator()(const int32_t& d) const { return (int64_t)d * (d - 1) / 2; }
+};
+
+}  // namespace
+
+void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P) {
+  cudaStream_t s = ctx.stream;
+  const int B = 256;
+  P.g = g;
+  const int64_t n = g.n, m2 = g.m2;
+  P.deg = ctx.buf("deg").as<int32_t>(n);
+  P.nd = ctx.buf("nd").as<int32_t>(m2);
+  P.s1 = ctx.buf("s1").as<int64_t>(n);
+  EFG_LAUNCH(k_deg, ceil_div(n, B), B, 0, s, g.offsets, n, P.deg);
+  // dmax -> F table length (cluster degree <= 3*dmax - 4)
+  int32_t* dmax_d = ctx.buf("dmax").as<int32_t>(1);
+  size_t tmp = 0;
+  EFG_CUDA_CHECK(cub::DeviceReduce::Max(nullptr, tmp, P.deg, dmax_d, n, s));
+  EFG_CUDA_CHECK(cub::DeviceReduce::Max(ctx.buf("cub").get(tmp), tmp, P.deg, dmax_d, n, s));
+  int32_t dmax = 0;
+  EFG_CUDA_CHECK(cudaMemcpyAsync(&dmax, dmax_d, sizeof dmax, cudaMemcpyDeviceToHost, s));
+  EFG_CUDA_CHECK(cudaStreamSynchronize(s));
+  P.dmax = dmax;
+  {
+    cub::TransformInputIterator<int64_t, Choose2, const int32_t*> c2(P.deg, Choose2{});
+    int64_t* sum_d = ctx.buf("sumc2").as<int64_t>(1);
+    EFG_CUDA_CHECK(cub::DeviceReduce::Sum(nullptr, tmp, c2, sum_d, n, s));
+    EFG_CUDA_CHECK(cub::DeviceReduce::Sum(ctx.buf("cub").get(tmp), tmp, c2, sum_d, n, s));
+    EFG_CUDA_CHECK(cudaMemcpyAsync(&P.sum_c2, sum_d, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  }
+  P.ftab_len = 3 * (int64_t)(dmax > 1 ? dmax : 1) + 8;
+  P.ftab = ctx.buf("ftab").as<double>(P.ftab_len);
+  EFG_LAUNCH(k_ftab, ceil_div(P.ftab_len, B), B, 0, s, P.ftab, P.ftab_len);
+  EFG_LAUNCH(k_nd, ceil_div(m2, B), B, 0, s, g.nbr, m2, P.deg, P.nd);
+  int64_t* dplus64 = ctx.buf("dplus64").as<int64_t>(n + 1);
+  EFG_LAUNCH(k_row_sums, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.s1, dplus64);
+  if (!need_orientation) return;
+  P.offp = ctx.buf("offp").as<int64_t>(n + 1);
+  EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, dplus64, P.offp, n + 1, s));
+  EFG_CUDA_CHECK(cudaMemsetAsync(dplus64 + n, 0, sizeof(int64_t), s));
+  EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dplus64, P.offp, n + 1, s));
+  P.adjp = ctx.buf("adjp").as<int2>(m2 / 2 > 0 ? m2 / 2 : 1);
+  EFG_LAUNCH(k_fill_adjp, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.offp, P.adjp);
+  P.dplus = nullptr;  // |Adj+(v)| = offp[v+1] - offp[v]
+}
+
+}  // namespace efg

@@ -1,0 +1,95 @@
+"""Pin the CPU oracle (oracle/) against the reference's own golden vectors.
+
+The fixtures in tests/golden/ were produced by running the reference package
+itself (scripts/make_golden.py).  If the oracle agrees with them, it can check
+the GPU path at sizes the reference cannot run.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from conftest import ef_close
+from oracle import brute
+from oracle import ef as O
+from oracle import graph as G
+
+
+def test_oracle_matches_reference_on_every_golden_case(golden):
+    checked = 0
+    for name, case in golden.items():
+        if case.n == 0:
+            continue
+        off, nb = case.get("offsets"), case.get("neighbors")
+        ef, tot, fl, T, W = O.ef_seeds(off, nb, threads=4)
+        assert np.array_equal(tot, case.get("cluster_total")), name
+        assert np.array_equal(fl, case.get("flags")), name
+        assert ef_close(ef, case.get("ef"), rtol=1e-12, atol=1e-14), name
+        # T is exact; EF = ln T - W/T reproduces the oracle's own ef
+        live = T > 0
+        assert np.all(ef[~live] == 0.0)
+        assert ef_close(np.log(T[live].astype(np.float64)) - W[live] / T[live], ef[live], rtol=1e-13, atol=1e-14), name
+        assert O.cluster_count(off) == case.meta["cluster_count"]
+        checked += 1
+    assert checked >= 250
+
+
+def test_oracle_is_bitwise_on_almost_all_cases(golden):
+    # same operation order as _scores_from_histograms; only libm log vs numpy log may differ
+    same = total = 0
+    for case in golden.values():
+        if case.n == 0:
+            continue
+        ef = O.ef_seeds(case.get("offsets"), case.get("neighbors"), threads=2)[0]
+        same += int(np.array_equal(ef, case.get("ef")))
+        total += 1
+    assert same >= 0.95 * total
+
+
+def test_graph_restatement_matches_reference_build(golden):
+    for name, case in golden.items():
+        edges = case.get("edges")
+        if edges is None:
+            continue
+        n, m, off, nb, orig = G.build_csr(edges)
+        assert (n, m) == (case.n, case.m), name
+        assert np.array_equal(off, case.get("offsets")), name
+        assert np.array_equal(nb, case.get("neighbors")), name
+        assert np.array_equal(orig, case.get("orig_ids")), name
+
+
+def test_brute_force_restatement_matches_reference_brute(golden):
+    for name, case in golden.items():
+        want = case.get("ef_brute")
+        if want is None or case.n > 60:
+            continue
+        bf = brute.expected_force(brute.adjacency(case.get("edges")))
+        got = np.array([bf[int(o)] for o in case.get("orig_ids")])
+        assert np.allclose(got, want, rtol=0, atol=1e-12), name
+        assert brute.cluster_count(brute.adjacency(case.get("edges"))) == case.meta["naive_cluster_count"]
+
+
+def test_known_answers(golden):
+    # closed forms asserted by the reference (test_expected_force.py:69-92, test_acceptance.py:59-72)
+    s3 = golden["star3"]
+    ef = O.ef_seeds(s3.get("offsets"), s3.get("neighbors"))[0]
+    assert ef[0] == pytest.approx(math.log(6), abs=1e-12)
+    assert np.allclose(ef[1:], math.log(2), atol=1e-12)
+    p4 = golden["path4"]
+    ef, tot, fl, T, W = O.ef_seeds(p4.get("offsets"), p4.get("neighbors"))
+    assert ef[0] == 0.0 and ef[3] == 0.0 and tot[0] == 1
+    assert ef[1] == pytest.approx(math.log(3), abs=1e-12)
+    k3 = golden["triangle"]
+    ef, tot, fl, _, _ = O.ef_seeds(k3.get("offsets"), k3.get("neighbors"))
+    assert np.all(ef == 0.0) and set(fl.tolist()) == {2}
+    e = golden["edge"]
+    assert O.ef_seeds(e.get("offsets"), e.get("neighbors"))[2].tolist() == [1, 1]
+
+
+def test_seed_subset_equals_full_run(golden):
+    case = golden["rmat_12_8_3"]
+    off, nb = case.get("offsets"), case.get("neighbors")
+    seeds = np.random.default_rng(0).choice(case.n, 300, replace=False)
+    ef, tot, fl, T, W = O.ef_seeds(off, nb, seeds=seeds, threads=3)
+    assert np.array_equal(ef, case.get("ef")[seeds]) or ef_close(ef, case.get("ef")[seeds], 1e-14, 0)
+    assert np.array_equal(tot, case.get("cluster_total")[seeds])

@@ -106,6 +106,13 @@ EFG_API int efg_shard_bounds(efg_ctx *ctx, const int64_t *d_offsets, const int32
 EFG_API int efg_topk(efg_ctx *ctx, const double *ef, int64_t n, int64_t k, int64_t *ids_out);
 EFG_API int efg_topk_device(efg_ctx *ctx, const double *d_ef, int64_t n, int64_t k, int64_t *ids_out);
 
+/* Live per-kernel device timing: when enabled, every kernel launch (and each
+ * CUB call) records a CUDA event pair on the launching stream; the report is
+ * JSON {"kernel": [total_ms, launches], ...} accumulated since the last reset. */
+EFG_API int efg_profile_enable(efg_ctx *ctx, int32_t on);
+EFG_API int efg_profile_reset(efg_ctx *ctx);
+EFG_API int efg_profile_report(efg_ctx *ctx, char *buf, int64_t cap);
+
 /* Pinned (page-locked) host memory for zero-staging copies; the Python layer
  * allocates Graph arrays and EF outputs here. */
 EFG_API int efg_host_alloc(int64_t bytes, void **out);

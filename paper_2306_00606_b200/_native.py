@@ -31,7 +31,8 @@ EXPORTED = (
     "efg_abi_version", "efg_last_error", "efg_create", "efg_destroy", "efg_set_stream",
     "efg_synchronize", "efg_build_graph", "efg_fetch_graph", "efg_graph_device",
     "efg_expected_force", "efg_expected_force_device", "efg_shard_bounds", "efg_topk",
-    "efg_topk_device", "efg_host_alloc", "efg_host_free",
+    "efg_topk_device", "efg_host_alloc", "efg_host_free", "efg_profile_enable", "efg_profile_reset",
+    "efg_profile_report",
 )
 
 
@@ -102,6 +103,9 @@ def lib():
             "efg_topk_device": ([p, p, i64, i64, p], ctypes.c_int),
             "efg_host_alloc": ([i64, P(p)], ctypes.c_int),
             "efg_host_free": ([p], ctypes.c_int),
+            "efg_profile_enable": ([p, i32], ctypes.c_int),
+            "efg_profile_reset": ([p], ctypes.c_int),
+            "efg_profile_report": ([p, ctypes.c_char_p, i64], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)
@@ -138,6 +142,19 @@ class Context:
 
     def close(self):
         self._fin()
+
+    def profile(self, on: bool = True) -> None:
+        check(lib().efg_profile_enable(self.handle, int(on)))
+
+    def profile_reset(self) -> None:
+        check(lib().efg_profile_reset(self.handle))
+
+    def profile_report(self) -> dict:
+        import json
+
+        buf = ctypes.create_string_buffer(1 << 16)
+        check(lib().efg_profile_report(self.handle, buf, len(buf)))
+        return {k: {"ms": v[0], "launches": int(v[1])} for k, v in json.loads(buf.value.decode()).items()}
 
 
 _contexts: dict[int, Context] = {}

@@ -12,6 +12,41 @@
 
 namespace efg {
 thread_local int64_t g_launches = 0;
+thread_local int64_t g_lib_calls = 0;
+thread_local Profiler* g_prof = nullptr;
+
+cudaEvent_t Profiler::take() {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    EFG_CUDA_CHECK(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  return pool[used++];
+}
+
+void Profiler::resolve() {
+  for (auto& r : pending) {
+    float ms = 0.f;
+    EFG_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+    auto& t = totals[r.name];
+    t.first += ms;
+    t.second += 1;
+  }
+  pending.clear();
+  used = 0;
+}
+
+Profiler::~Profiler() {
+  for (auto e : pool) cudaEventDestroy(e);
+}
+
+void prof_begin(Profiler* p, const char* name, cudaStream_t s) {
+  Profiler::Rec r{name, p->take(), p->take()};
+  EFG_CUDA_CHECK(cudaEventRecord(r.a, s));
+  p->pending.push_back(r);
+}
+
+void prof_end(Profiler* p, cudaStream_t s) { EFG_CUDA_CHECK(cudaEventRecord(p->pending.back().b, s)); }
 
 Context::~Context() {
   for (auto& kv : bufs) kv.second.release();
@@ -45,10 +80,19 @@ int guarded(efg_ctx* ctx, F&& body) {
   try {
     cudaError_t e = cudaSetDevice(ctx->c.device);
     if (e != cudaSuccess) return fail(efg::EFG_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+    efg::g_prof = ctx->c.prof.on ? &ctx->c.prof : nullptr;
     body(ctx->c);
+    if (efg::g_prof && !ctx->c.prof.pending.empty()) {
+      EFG_CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+      ctx->c.prof.resolve();
+    }
+    efg::g_prof = nullptr;
     g_last_error.clear();
     return efg::EFG_OK;
   } catch (const efg::Error& err) {
+    efg::g_prof = nullptr;
+    ctx->c.prof.pending.clear();
+    ctx->c.prof.used = 0;
     return fail(err.code, err.what());
   } catch (const std::bad_alloc&) {
     return fail(efg::EFG_OOM, "host out of memory");
@@ -329,6 +373,30 @@ int efg_shard_bounds(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_ne
     }
     for (; p < parts; ++p) bounds_out[p] = n;
     for (p = 1; p <= parts; ++p) bounds_out[p] = std::max(bounds_out[p], bounds_out[p - 1]);
+  });
+}
+
+int efg_profile_enable(efg_ctx* ctx, int32_t on) {
+  return guarded(ctx, [&](Context& c) { c.prof.on = on != 0; });
+}
+
+int efg_profile_reset(efg_ctx* ctx) {
+  return guarded(ctx, [&](Context& c) { c.prof.totals.clear(); });
+}
+
+int efg_profile_report(efg_ctx* ctx, char* buf, int64_t cap) {
+  if (!buf || cap < 3) return fail(efg::EFG_INVALID, "bad report buffer");
+  return guarded(ctx, [&](Context& c) {
+    std::string js = "{";
+    bool first = true;
+    for (auto& kv : c.prof.totals) {
+      if (!first) js += ",";
+      first = false;
+      js += "\"" + kv.first + "\":[" + std::to_string(kv.second.first) + "," + std::to_string(kv.second.second) + "]";
+    }
+    js += "}";
+    EFG_REQUIRE((int64_t)js.size() < cap, "report buffer too small");
+    std::memcpy(buf, js.c_str(), js.size() + 1);
   });
 }
 

@@ -68,16 +68,35 @@ struct DevBuf {
   }
 };
 
-// Launch-count bookkeeping (stats.launches); every kernel launch in the
-// library goes through EFG_LAUNCH so the count is exact.
+// Launch bookkeeping.  Every kernel launch in the library goes through
+// EFG_LAUNCH (count is exact: stats.launches); library calls that launch
+// their own kernels (CUB) go through EFG_REGION.  When the context's profiler
+// is on, both record a CUDA event pair on the launching stream so per-kernel
+// device times are measured live (efg_profile_report).
+struct Profiler;
 extern thread_local int64_t g_launches;
+extern thread_local int64_t g_lib_calls;
+extern thread_local Profiler* g_prof;
+void prof_begin(Profiler*, const char* name, cudaStream_t s);
+void prof_end(Profiler*, cudaStream_t s);
+
 #define EFG_LAUNCH(kernel, grid, block, smem, stream, ...)                         \
   do {                                                                              \
     if ((grid) > 0) {                                                               \
+      if (::efg::g_prof) ::efg::prof_begin(::efg::g_prof, #kernel, (stream));       \
       kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                   \
       EFG_CUDA_CHECK(cudaGetLastError());                                           \
+      if (::efg::g_prof) ::efg::prof_end(::efg::g_prof, (stream));                  \
       ++::efg::g_launches;                                                          \
     }                                                                               \
+  } while (0)
+
+#define EFG_REGION(name, stream, ...)                                              \
+  do {                                                                              \
+    if (::efg::g_prof) ::efg::prof_begin(::efg::g_prof, (name), (stream));          \
+    __VA_ARGS__;                                                                    \
+    if (::efg::g_prof) ::efg::prof_end(::efg::g_prof, (stream));                    \
+    ++::efg::g_lib_calls;                                                           \
   } while (0)
 
 }  // namespace efg

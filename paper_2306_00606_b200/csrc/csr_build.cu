@@ -100,7 +100,7 @@ void build_csr_device(Context& ctx, const int64_t* d_edges, int64_t k, DeviceCSR
   // compact away self-loop endpoints
   size_t tmp = 0;
   EFG_CUDA_CHECK(cub::DeviceSelect::Flagged(nullptr, tmp, d_edges, flag2, ends_sorted, dnum, 2 * k, s));
-  EFG_CUDA_CHECK(cub::DeviceSelect::Flagged(ctx.buf("cub").get(tmp), tmp, d_edges, flag2, ends_sorted, dnum, 2 * k, s));
+  EFG_REGION("cub::DeviceSelect::Flagged", s, EFG_CUDA_CHECK(cub::DeviceSelect::Flagged(ctx.buf("cub").get(tmp), tmp, d_edges, flag2, ends_sorted, dnum, 2 * k, s)));
   int64_t nend = 0;
   EFG_CUDA_CHECK(cudaMemcpyAsync(&nend, dnum, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   EFG_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -108,9 +108,9 @@ void build_csr_device(Context& ctx, const int64_t* d_edges, int64_t k, DeviceCSR
   // id range -> number of radix bits (ids may be any int64, like the
   // reference's np.unique; sort them as unsigned offsets from the minimum)
   EFG_CUDA_CHECK(cub::DeviceReduce::Min(nullptr, tmp, ends_sorted, dnum + 1, nend, s));
-  EFG_CUDA_CHECK(cub::DeviceReduce::Min(ctx.buf("cub").get(tmp), tmp, ends_sorted, dnum + 1, nend, s));
+  EFG_REGION("cub::DeviceReduce::Min", s, EFG_CUDA_CHECK(cub::DeviceReduce::Min(ctx.buf("cub").get(tmp), tmp, ends_sorted, dnum + 1, nend, s)));
   EFG_CUDA_CHECK(cub::DeviceReduce::Max(nullptr, tmp, ends_sorted, dnum + 2, nend, s));
-  EFG_CUDA_CHECK(cub::DeviceReduce::Max(ctx.buf("cub").get(tmp), tmp, ends_sorted, dnum + 2, nend, s));
+  EFG_REGION("cub::DeviceReduce::Max", s, EFG_CUDA_CHECK(cub::DeviceReduce::Max(ctx.buf("cub").get(tmp), tmp, ends_sorted, dnum + 2, nend, s)));
   int64_t mm[2] = {0, 0};
   EFG_CUDA_CHECK(cudaMemcpyAsync(mm, dnum + 1, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   EFG_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -120,10 +120,10 @@ void build_csr_device(Context& ctx, const int64_t* d_edges, int64_t k, DeviceCSR
   uint64_t* ukeys = reinterpret_cast<uint64_t*>(ends_sorted);
   uint64_t* ukeys_alt = reinterpret_cast<uint64_t*>(ends);
   EFG_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, ukeys, ukeys_alt, nend, 0, idbits, s));
-  EFG_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(ctx.buf("cub").get(tmp), tmp, ukeys, ukeys_alt, nend, 0, idbits, s));
+  EFG_REGION("cub::DeviceRadixSort::SortKeys", s, EFG_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(ctx.buf("cub").get(tmp), tmp, ukeys, ukeys_alt, nend, 0, idbits, s)));
   int64_t* orig = ctx.buf("k1_orig").as<int64_t>(nend);
   EFG_CUDA_CHECK(cub::DeviceSelect::Unique(nullptr, tmp, ukeys_alt, reinterpret_cast<uint64_t*>(orig), dnum, nend, s));
-  EFG_CUDA_CHECK(cub::DeviceSelect::Unique(ctx.buf("cub").get(tmp), tmp, ukeys_alt, reinterpret_cast<uint64_t*>(orig), dnum, nend, s));
+  EFG_REGION("cub::DeviceSelect::Unique", s, EFG_CUDA_CHECK(cub::DeviceSelect::Unique(ctx.buf("cub").get(tmp), tmp, ukeys_alt, reinterpret_cast<uint64_t*>(orig), dnum, nend, s)));
   int64_t n = 0;
   EFG_CUDA_CHECK(cudaMemcpyAsync(&n, dnum, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   EFG_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -138,9 +138,9 @@ void build_csr_device(Context& ctx, const int64_t* d_edges, int64_t k, DeviceCSR
   int64_t nloops = k - nend / 2;
   int sort_bits = nloops ? 64 : cbits;
   EFG_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, codes, codes_sorted, k, 0, sort_bits, s));
-  EFG_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(ctx.buf("cub").get(tmp), tmp, codes, codes_sorted, k, 0, sort_bits, s));
+  EFG_REGION("cub::DeviceRadixSort::SortKeys", s, EFG_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(ctx.buf("cub").get(tmp), tmp, codes, codes_sorted, k, 0, sort_bits, s)));
   EFG_CUDA_CHECK(cub::DeviceSelect::Unique(nullptr, tmp, codes_sorted, codes, dnum, k - nloops, s));
-  EFG_CUDA_CHECK(cub::DeviceSelect::Unique(ctx.buf("cub").get(tmp), tmp, codes_sorted, codes, dnum, k - nloops, s));
+  EFG_REGION("cub::DeviceSelect::Unique", s, EFG_CUDA_CHECK(cub::DeviceSelect::Unique(ctx.buf("cub").get(tmp), tmp, codes_sorted, codes, dnum, k - nloops, s)));
   int64_t m = 0;
   EFG_CUDA_CHECK(cudaMemcpyAsync(&m, dnum, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   EFG_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -149,7 +149,7 @@ void build_csr_device(Context& ctx, const int64_t* d_edges, int64_t k, DeviceCSR
   uint64_t* keys_sorted = ctx.buf("k1_keys_sorted").as<uint64_t>(2 * m);
   EFG_LAUNCH(k_symmetrise, ceil_div(m, B), B, 0, s, codes, m, n, keys);
   EFG_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(nullptr, tmp, keys, keys_sorted, 2 * m, 0, cbits, s));
-  EFG_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(ctx.buf("cub").get(tmp), tmp, keys, keys_sorted, 2 * m, 0, cbits, s));
+  EFG_REGION("cub::DeviceRadixSort::SortKeys", s, EFG_CUDA_CHECK(cub::DeviceRadixSort::SortKeys(ctx.buf("cub").get(tmp), tmp, keys, keys_sorted, 2 * m, 0, cbits, s)));
   out.alloc(n, m);
   EFG_LAUNCH(k_split_keys, ceil_div(2 * m, B), B, 0, s, keys_sorted, 2 * m, n, out.nbr, out.offsets);
   EFG_CUDA_CHECK(cudaMemcpyAsync(out.orig_ids, orig, n * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));

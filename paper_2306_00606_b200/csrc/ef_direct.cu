@@ -300,7 +300,7 @@ void ef_direct(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* tota
   int64_t* tstart = ctx.buf("d_tstart").as<int64_t>(cnt + 1);
   EFG_LAUNCH(k_task_counts, ceil_div(cnt + 1, B), B, 0, s, P.g.offsets, P.s1, r.lo, cnt, ntask);
   EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ntask, tstart, cnt + 1, s));
-  EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, ntask, tstart, cnt + 1, s));
+  EFG_REGION("cub::DeviceScan::ExclusiveSum", s, EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, ntask, tstart, cnt + 1, s)));
   int64_t ntasks = 0;
   EFG_CUDA_CHECK(cudaMemcpyAsync(&ntasks, tstart + cnt, sizeof ntasks, cudaMemcpyDeviceToHost, s));
   // hubs needing a bitmap
@@ -309,7 +309,7 @@ void ef_direct(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* tota
   cub::CountingInputIterator<int32_t> it((int32_t)r.lo);
   HubPred pred{P.deg};
   EFG_CUDA_CHECK(cub::DeviceSelect::If(nullptr, tmp, it, hubs, nh_d, cnt, pred, s));
-  EFG_CUDA_CHECK(cub::DeviceSelect::If(ctx.buf("cub").get(tmp), tmp, it, hubs, nh_d, cnt, pred, s));
+  EFG_REGION("cub::DeviceSelect::If", s, EFG_CUDA_CHECK(cub::DeviceSelect::If(ctx.buf("cub").get(tmp), tmp, it, hubs, nh_d, cnt, pred, s)));
   int64_t nhubs = 0;
   EFG_CUDA_CHECK(cudaMemcpyAsync(&nhubs, nh_d, sizeof nhubs, cudaMemcpyDeviceToHost, s));
   EFG_CUDA_CHECK(cudaStreamSynchronize(s));

@@ -409,14 +409,14 @@ static int64_t build_histograms(Context& ctx, Prepared& P, int64_t*& hoff, int32
   size_t tmp = 0;
   EFG_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, P.nd, snd, (int)m2, (int)n, P.g.offsets,
                                                     P.g.offsets + 1, s));
-  EFG_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(ctx.buf("cub").get(tmp), tmp, P.nd, snd, (int)m2, (int)n,
-                                                    P.g.offsets, P.g.offsets + 1, s));
+  EFG_REGION("cub::DeviceSegmentedSort::SortKeys", s, EFG_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(ctx.buf("cub").get(tmp), tmp, P.nd, snd, (int)m2, (int)n,
+                                                    P.g.offsets, P.g.offsets + 1, s)));
   int64_t* dcnt = ctx.buf("f_dcnt").as<int64_t>(n + 1);
   hoff = ctx.buf("f_hoff").as<int64_t>(n + 1);
   EFG_LAUNCH(k_rle_count, ceil_div(n * 32, B), B, 0, s, P.g.offsets, snd, n, dcnt);
   EFG_CUDA_CHECK(cudaMemsetAsync(dcnt + n, 0, sizeof(int64_t), s));
   EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, dcnt, hoff, n + 1, s));
-  EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dcnt, hoff, n + 1, s));
+  EFG_REGION("cub::DeviceScan::ExclusiveSum", s, EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dcnt, hoff, n + 1, s)));
   int64_t nh = 0;
   EFG_CUDA_CHECK(cudaMemcpyAsync(&nh, hoff + n, sizeof nh, cudaMemcpyDeviceToHost, s));
   EFG_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -454,7 +454,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     cub::CountingInputIterator<int32_t> rit(0);
     BigRow pred{hoff, kBig};
     EFG_CUDA_CHECK(cub::DeviceSelect::If(nullptr, tmp, rit, rows, nrows_d, n, pred, s));
-    EFG_CUDA_CHECK(cub::DeviceSelect::If(ctx.buf("cub").get(tmp), tmp, rit, rows, nrows_d, n, pred, s));
+    EFG_REGION("cub::DeviceSelect::If", s, EFG_CUDA_CHECK(cub::DeviceSelect::If(ctx.buf("cub").get(tmp), tmp, rit, rows, nrows_d, n, pred, s)));
     int64_t nrows = 0;
     EFG_CUDA_CHECK(cudaMemcpyAsync(&nrows, nrows_d, sizeof nrows, cudaMemcpyDeviceToHost, s));
     EFG_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -489,8 +489,8 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   for (int k = 0; k < 5; ++k) {
     DegClass pred{P.deg, k ? kClassHi[k - 1] : 0, kClassHi[k]};
     EFG_CUDA_CHECK(cub::DeviceSelect::If(nullptr, tmp, it, lists + k * cnt, ncls_d + k, cnt, pred, s));
-    EFG_CUDA_CHECK(
-        cub::DeviceSelect::If(ctx.buf("cub").get(tmp), tmp, it, lists + k * cnt, ncls_d + k, cnt, pred, s));
+    EFG_REGION("cub::DeviceSelect::If", s, EFG_CUDA_CHECK(
+        cub::DeviceSelect::If(ctx.buf("cub").get(tmp), tmp, it, lists + k * cnt, ncls_d + k, cnt, pred, s)));
   }
   int64_t ncls[5];
   EFG_CUDA_CHECK(cudaMemcpyAsync(ncls, ncls_d, sizeof ncls, cudaMemcpyDeviceToHost, s));

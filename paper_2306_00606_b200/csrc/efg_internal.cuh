@@ -3,6 +3,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "../../include/efg.h"
@@ -23,6 +24,21 @@ struct DeviceCSR {
   }
 };
 
+struct Profiler {
+  struct Rec {
+    std::string name;
+    cudaEvent_t a, b;
+  };
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  size_t used = 0;
+  std::vector<Rec> pending;
+  std::map<std::string, std::pair<double, int64_t>> totals;  // name -> (ms, launches)
+  cudaEvent_t take();
+  void resolve();  // after a stream sync
+  ~Profiler();
+};
+
 struct Context {
   int device = 0;
   int num_sms = kNumSMs;
@@ -31,6 +47,7 @@ struct Context {
   std::map<std::string, DevBuf> bufs;
   std::mutex mu;
   cudaEvent_t ev[16] = {};
+  Profiler prof;
   DeviceCSR csr;  // resident graph of efg_build_graph / efg_rmat_build
   DevBuf& buf(const std::string& name) { return bufs[name]; }
   ~Context();

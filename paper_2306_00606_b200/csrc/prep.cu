@@ -108,7 +108,7 @@ void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P)
   int32_t* dmax_d = ctx.buf("dmax").as<int32_t>(1);
   size_t tmp = 0;
   EFG_CUDA_CHECK(cub::DeviceReduce::Max(nullptr, tmp, P.deg, dmax_d, n, s));
-  EFG_CUDA_CHECK(cub::DeviceReduce::Max(ctx.buf("cub").get(tmp), tmp, P.deg, dmax_d, n, s));
+  EFG_REGION("cub::DeviceReduce::Max", s, EFG_CUDA_CHECK(cub::DeviceReduce::Max(ctx.buf("cub").get(tmp), tmp, P.deg, dmax_d, n, s)));
   int32_t dmax = 0;
   EFG_CUDA_CHECK(cudaMemcpyAsync(&dmax, dmax_d, sizeof dmax, cudaMemcpyDeviceToHost, s));
   EFG_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -117,7 +117,7 @@ void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P)
     cub::TransformInputIterator<int64_t, Choose2, const int32_t*> c2(P.deg, Choose2{});
     int64_t* sum_d = ctx.buf("sumc2").as<int64_t>(1);
     EFG_CUDA_CHECK(cub::DeviceReduce::Sum(nullptr, tmp, c2, sum_d, n, s));
-    EFG_CUDA_CHECK(cub::DeviceReduce::Sum(ctx.buf("cub").get(tmp), tmp, c2, sum_d, n, s));
+    EFG_REGION("cub::DeviceReduce::Sum", s, EFG_CUDA_CHECK(cub::DeviceReduce::Sum(ctx.buf("cub").get(tmp), tmp, c2, sum_d, n, s)));
     EFG_CUDA_CHECK(cudaMemcpyAsync(&P.sum_c2, sum_d, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
   }
   P.ftab_len = 3 * (int64_t)(dmax > 1 ? dmax : 1) + 8;
@@ -130,7 +130,7 @@ void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P)
   P.offp = ctx.buf("offp").as<int64_t>(n + 1);
   EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, dplus64, P.offp, n + 1, s));
   EFG_CUDA_CHECK(cudaMemsetAsync(dplus64 + n, 0, sizeof(int64_t), s));
-  EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dplus64, P.offp, n + 1, s));
+  EFG_REGION("cub::DeviceScan::ExclusiveSum", s, EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dplus64, P.offp, n + 1, s)));
   P.adjp = ctx.buf("adjp").as<int2>(m2 / 2 > 0 ? m2 / 2 : 1);
   EFG_LAUNCH(k_fill_adjp, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.offp, P.adjp);
   P.dplus = nullptr;  // |Adj+(v)| = offp[v+1] - offp[v]

@@ -34,8 +34,8 @@ void topk_device(Context& ctx, const double* d_ef, int64_t n, int64_t k, int64_t
   EFG_LAUNCH(k_topk_init, ceil_div(n, B), B, 0, s, d_ef, n, keys, ids);
   size_t tmp = 0;
   EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, keys, keys2, ids, ids2, n, 0, 64, s));
-  EFG_CUDA_CHECK(
-      cub::DeviceRadixSort::SortPairsDescending(ctx.buf("cub").get(tmp), tmp, keys, keys2, ids, ids2, n, 0, 64, s));
+  EFG_REGION("cub::DeviceRadixSort::SortPairsDescending", s, EFG_CUDA_CHECK(
+      cub::DeviceRadixSort::SortPairsDescending(ctx.buf("cub").get(tmp), tmp, keys, keys2, ids, ids2, n, 0, 64, s)));
   EFG_CUDA_CHECK(cudaMemcpyAsync(d_ids_out, ids2, (k < n ? k : n) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
 }
 

@@ -1,0 +1,80 @@
+"""Multi-GPU Expected Force: replicated graph, seeds sharded, one all-gather.
+
+One process per GPU (torch.distributed, NCCL over NVLink on B200 boxes).
+Every rank holds the full CSR in its HBM (370 MB at R-MAT22); K2 cuts the
+seed range into contiguous shards of equal engine work (`shard_bounds`, the
+same bounds on every rank because they depend only on the graph); each rank
+runs the EF kernels on its shard; the per-seed outputs (ef f64, cluster_total
+i64, flags u8 = 17 B/seed) are exchanged with ONE all-gather of a packed,
+padded byte buffer.  Seeds have a single owner and their sums run in a fixed
+order, so the result is bitwise identical for any world size.
+
+There is no reference counterpart (the reference is single-process threads,
+expected_force.py:163-167); SURVEY.md §8(e) specifies this path.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+RECORD_BYTES = 17  # f64 ef + i64 cluster_total + u8 flags
+
+
+def pack_shard(ef, total, flags, pad_to: int):
+    """Pack one shard's outputs into a uint8 tensor [pad_to * 17] (ef | total | flags)."""
+    import torch
+
+    L = ef.numel()
+    buf = torch.zeros(pad_to * RECORD_BYTES, dtype=torch.uint8, device=ef.device)
+    buf[: 8 * L] = ef.view(torch.uint8)
+    buf[8 * pad_to: 8 * pad_to + 8 * L] = total.view(torch.uint8)
+    buf[16 * pad_to: 16 * pad_to + L] = flags.view(torch.uint8)
+    return buf
+
+
+def unpack_all(gathered, bounds, pad_to: int):
+    """gathered: uint8 tensor [world * pad_to * 17] -> (ef, total, flags) over all seeds."""
+    import torch
+
+    world = len(bounds) - 1
+    parts = gathered.view(world, pad_to * RECORD_BYTES)
+    efs, tots, fls = [], [], []
+    for r in range(world):
+        L = int(bounds[r + 1] - bounds[r])
+        row = parts[r]
+        efs.append(row[: 8 * L].view(torch.float64))
+        tots.append(row[8 * pad_to: 8 * pad_to + 8 * L].view(torch.int64))
+        fls.append(row[16 * pad_to: 16 * pad_to + L])
+    return torch.cat(efs), torch.cat(tots), torch.cat(fls)
+
+
+def ef_sharded(dg, engine="factorized", group=None, compute=None, bounds=None):
+    """Expected Force of every seed of DeviceGraph `dg`, computed across the
+    ranks of `group`; returns device tensors (ef, cluster_total, flags) on
+    every rank.  `compute(dg, lo, hi, ef, total, flags)` defaults to the GPU
+    engine (device.ef_range); tests substitute a CPU stand-in under gloo."""
+    import torch
+    import torch.distributed as dist
+
+    from . import device as D
+
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if bounds is None:
+        bounds = D.shard_bounds(dg, world, engine) if world > 1 else np.array([0, dg.n], np.int64)
+    lo, hi = int(bounds[rank]), int(bounds[rank + 1])
+    pad_to = int(max(1, np.max(np.diff(bounds))))
+    dev = dg.offsets.device
+    ef = torch.empty(hi - lo, dtype=torch.float64, device=dev)
+    tot = torch.empty(hi - lo, dtype=torch.int64, device=dev)
+    fl = torch.empty(hi - lo, dtype=torch.uint8, device=dev)
+    if hi > lo:
+        if compute is None:
+            D.ef_range(dg, lo, hi, ef, tot, fl, engine=engine)
+        else:
+            compute(dg, lo, hi, ef, tot, fl)
+    if world == 1:
+        return ef, tot, fl
+    mine = pack_shard(ef, tot, fl, pad_to)
+    gathered = torch.empty(world * mine.numel(), dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(gathered, mine, group=group)
+    return unpack_all(gathered, bounds, pad_to)

@@ -1,0 +1,140 @@
+"""GPU parity against the reference's golden vectors and the CPU oracle.
+
+Bar (BASELINE.json): cluster counts, multiplicities (cluster_total) and flags
+bit-exact; EF |gpu - ref| <= 1e-9 |ref| + 1e-12 (fp64); T = sum w*d exact.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2306_00606_b200 as efg
+from paper_2306_00606_b200.expected_force import _run
+from paper_2306_00606_b200.graph import Graph
+from conftest import ef_close
+from oracle import ef as O
+
+pytestmark = pytest.mark.gpu
+ENGINES = ("factorized", "direct")
+
+
+def graph_of(case):
+    return Graph(case.n, case.m, case.get("offsets"), case.get("neighbors"), case.get("orig_ids"))
+
+
+def test_device_csr_builder_matches_reference(golden):
+    for name, case in golden.items():
+        edges = case.get("edges")
+        if edges is None:
+            continue
+        g = efg.build_graph(edges)
+        assert (g.n, g.m) == (case.n, case.m), name
+        if g.n:
+            assert np.array_equal(g.offsets, case.get("offsets")), name
+            assert np.array_equal(g.neighbors, case.get("neighbors")), name
+            assert np.array_equal(g.orig_ids, case.get("orig_ids")), name
+            assert g.neighbors.dtype == np.int32 and g.offsets.dtype == np.int64
+
+
+def test_csr_builder_edge_cases():
+    assert efg.build_graph([(3, 3)]).n == 0
+    g = efg.build_graph([(0, 1), (1, 0), (2, 2)])
+    assert (g.n, g.m) == (2, 1) and g.adjacency(0).tolist() == [1]
+    g = efg.build_graph([(5, 9)])
+    assert g.orig_ids.tolist() == [5, 9] and g.relabeling == {5: 0, 9: 1}
+    # huge and negative original ids keep their order (np.unique semantics)
+    g = efg.build_graph([(-7, 2**40), (2**40, 3), (-7, 3), (3, 3)])
+    assert g.orig_ids.tolist() == [-7, 3, 2**40] and g.m == 3
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_engines_match_reference_golden(golden, engine):
+    for name, case in golden.items():
+        if case.n == 0:
+            continue
+        g = graph_of(case)
+        r = efg.ef_cluster_centric(g, engine=engine)
+        assert np.array_equal(r.cluster_total, case.get("cluster_total")), name
+        assert np.array_equal(r.flags, case.get("flags")), name
+        assert ef_close(r.ef, case.get("ef")), (name, float(np.max(np.abs(r.ef - case.get("ef")))))
+        assert r.clusters_processed == case.meta["cluster_count"], name
+        ref_zero = case.get("ef") == 0.0
+        assert np.all(r.ef[ref_zero & (r.cluster_total > 0) & (case.get("flags") > 0)] == 0.0)
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_exact_T_and_W_against_oracle(golden, engine):
+    for name in ("ba2000", "rmat_12_8_3", "rmat_14_16_1", "er200_100", "k6", "star7_path3"):
+        case = golden[name]
+        r = _run(graph_of(case), 0, engine, None, want_tw=True)
+        _, _, _, T, W = O.ef_seeds(case.get("offsets"), case.get("neighbors"), threads=4)
+        assert np.array_equal(r.stats["T"], T), name
+        assert ef_close(r.stats["W"], W, rtol=1e-12, atol=1e-9), name
+
+
+def test_vertex_mode_counts_and_bitwise_dispatch(golden):
+    g = graph_of(golden["k5"])
+    r = efg.ef_vertex_centric(g)
+    assert r.clusters_processed == 3 * efg.cluster_count(g)
+    p4 = graph_of(golden["path4"])
+    assert np.array_equal(efg.ef(p4, mode="cluster_centric").ef, efg.ef(p4, mode="vertex_centric").ef)
+
+
+def test_closed_forms(golden):
+    r = efg.ef_cluster_centric(graph_of(golden["star3"]))
+    assert r.ef[0] == pytest.approx(math.log(6), abs=1e-12)
+    assert np.allclose(r.ef[1:], math.log(2), atol=1e-12)
+    r = efg.ef_vertex_centric(graph_of(golden["path4"]))
+    assert r.ef[0] == 0.0 and r.ef[3] == 0.0
+    assert r.ef[1] == pytest.approx(math.log(3), abs=1e-12)
+    for mode in ("cluster_centric", "vertex_centric"):
+        assert np.all(efg.ef(graph_of(golden["triangle"]), mode=mode).ef == 0.0)
+    r = efg.ef_cluster_centric(graph_of(golden["path4"]))
+    assert r.cluster_total[0] == 1 and r.ef[0] == 0.0
+    assert list(efg.ef_cluster_centric(graph_of(golden["edge"])).flags) == [1, 1]
+    assert set(efg.ef_cluster_centric(graph_of(golden["triangle"])).flags) == {2}
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_determinism_bitwise(golden, engine):
+    g = graph_of(golden["rmat_14_16_1"])
+    a = efg.ef_cluster_centric(g, engine=engine)
+    for workers, chunk in ((2, 1), (8, 100)):
+        b = efg.ef_cluster_centric(g, workers=workers, chunk_size=chunk, engine=engine)
+        assert np.array_equal(a.ef, b.ef) and np.array_equal(a.cluster_total, b.cluster_total)
+
+
+def test_engines_agree_closely(golden):
+    g = graph_of(golden["rmat_14_16_1"])
+    a = efg.ef_cluster_centric(g, engine="factorized")
+    b = efg.ef_cluster_centric(g, engine="direct")
+    assert np.array_equal(a.cluster_total, b.cluster_total)
+    assert ef_close(a.ef, b.ef, rtol=1e-13, atol=1e-13)
+
+
+def test_key_nodes_match_lexsort(golden):
+    case = golden["rmat_14_16_1"]
+    efv = case.get("ef")
+    ids = np.arange(efv.size)
+    for k in (1, 10, 113, efv.size):
+        want = np.lexsort((ids, -efv))[:k]
+        assert np.array_equal(efg.key_nodes(efv, k=k), want)
+    ties = np.array([1.0, 3.0, 3.0, 0.0, 3.0, -0.0, 0.0])
+    assert efg.key_nodes(ties, k=7).tolist() == np.lexsort((np.arange(7), -ties)).tolist()
+    assert efg.key_nodes(efv, frac=0.01).size == math.ceil(0.01 * efv.size)
+
+
+def test_generate_rmat_matches_reference_fingerprints():
+    import json
+    import hashlib
+    from conftest import GOLDEN
+    fps = json.loads((GOLDEN / "rmat_fingerprints.json").read_text())
+    for key in ("9,6,5", "12,8,3", "16,8,42"):
+        s, m, seed = map(int, key.split(","))
+        g, trunc = efg.generate_rmat(efg.RmatParams(scale=s, avg_degree=m, seed=seed))
+        h = hashlib.sha256()
+        h.update(np.int64([g.n, g.m]).tobytes())
+        for a in (g.offsets, g.neighbors, g.orig_ids):
+            h.update(np.ascontiguousarray(a).tobytes())
+        assert h.hexdigest() == fps[key]["sha256"], key
+        assert trunc == fps[key]["truncated"]

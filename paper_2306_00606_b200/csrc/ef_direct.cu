@@ -260,7 +260,9 @@ __global__ void k_direct_epilogue(const int64_t* __restrict__ offsets, const int
   }
   int64_t mass = dv * (dv - 1) + s1[v] - dv;
   double e = 0.0;
-  if (T > 0) e = log((double)T) - W / (double)T;
+  // entropy >= 0: clamp the last-ulp cancellation of ln T - W/T when only one
+  // positive-degree cluster class exists (EF mathematically 0)
+  if (T > 0) e = fmax(log((double)T) - W / (double)T, 0.0);
   ef[q] = e;
   total[q] = mass;
   flags[q] = mass == 0 ? 1 : (T == 0 ? 2 : 0);

@@ -34,26 +34,34 @@ namespace efg {
 
 namespace {
 
+constexpr int kTask = 2048;          // flattened triangle items per CTA chunk / hub task
+constexpr int kRun = 8;              // consecutive items per thread: independent loads in flight
+constexpr int kHashSlots = 8192;     // smem hash of Adj(v) for dv <= 4096
+constexpr int kHashMaxDeg = kHashSlots / 2;
+constexpr int kTaskThreads = 256;
+
 struct FArgs {
   const int64_t* offsets;
   const int32_t* nbr;
-  const int32_t* nd;
-  const int32_t* deg;
+  const int32_t* nd;       // degree of each adjacency entry
   const int64_t* s1;
   const double* F;
-  const int64_t* offp;
-  const int2* adjp;
+  const int64_t* ps;       // [2m] start of Adj+(nbr[e]) in adjp
+  const int32_t* pc;       // [2m] |Adj+(nbr[e])|
+  const int64_t* tp;       // [2m] row prefix of (pc + 1): flattened triangle items
+  const int32_t* adjj;     // oriented adjacency Adj+ (ascending j per row)
+  const int32_t* deg;
   const int64_t* hoff;
   const int32_t* hkey;
   const int32_t* hcnt;
   const double* ctab;
-  int64_t n;
   int64_t seed_lo;
-  double* ef;
-  int64_t* total;
-  uint8_t* flags;
-  int64_t* T_out;
-  double* W_out;
+  // per-seed partials, index v - seed_lo
+  int64_t* Tc;
+  double* Wc;
+  double* Ws;
+  int64_t* tri;
+  double* Wt;
 };
 
 // ---------------------------------------------------------------- H build
@@ -154,114 +162,13 @@ struct BigRow {
 };
 
 // ---------------------------------------------------------------- per seed
-__device__ __forceinline__ double ctab_lookup(const FArgs& a, int32_t i, int32_t y) {
-  int64_t lo = a.hoff[i], hi = a.hoff[i + 1] - 1;
-  while (lo < hi) {  // y is present: v (degree y) is a neighbour of i
-    int64_t mid = (lo + hi) >> 1;
-    if (__ldg(a.hkey + mid) < y) lo = mid + 1; else hi = mid;
-  }
-  return __ldg(a.ctab + lo);
-}
-
-__device__ __forceinline__ void finalize(const FArgs& a, int32_t v, int64_t dv, int64_t Tc, int64_t tri,
-                                         double Ws, double Wc, double Wt) {
-  const int64_t s1v = a.s1[v];
-  const int64_t T = dv * (dv - 1) * (dv - 4) + 2 * (dv - 1) * s1v + Tc - 8 * tri;
-  const int64_t mass = dv * (dv - 1) + s1v - dv;
-  const double W = (Ws + Wc) + 4.0 * Wt;
-  double efv = 0.0;
-  if (T > 0) efv = log((double)T) - W / (double)T;
-  uint8_t fl = mass == 0 ? 1 : (T == 0 ? 2 : 0);
-  const int64_t o = v - a.seed_lo;
-  a.ef[o] = efv;
-  a.total[o] = mass;
-  a.flags[o] = fl;
-  if (a.T_out) a.T_out[o] = T;
-  if (a.W_out) a.W_out[o] = W;
-}
-
 template <class T>
 __device__ __forceinline__ T warp_sum(T x) {
   for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   return x;
 }
 
-// Seeds with dv <= 32: one warp per seed.  A is kept sorted in shared memory
-// and membership is a 5-step binary search.
-constexpr int kWarpSeedWarps = 8;
-__global__ void __launch_bounds__(kWarpSeedWarps * 32)
-k_seed_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
-  __shared__ int32_t sA[kWarpSeedWarps][32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int64_t q = (int64_t)blockIdx.x * kWarpSeedWarps + w;
-  if (q >= count) return;
-  const int32_t v = seeds[q];
-  const int64_t ob = a.offsets[v];
-  const int32_t dv = (int32_t)(a.offsets[v + 1] - ob);
-  int32_t i = -1, di = 0;
-  int64_t Tc = 0;
-  double Wc = 0.0;
-  if (lane < dv) {
-    i = a.nbr[ob + lane];
-    di = a.nd[ob + lane];
-    Tc = (int64_t)(di - 1) * (dv + di - 4) + a.s1[i] - dv;
-    Wc = ctab_lookup(a, i, dv);
-  }
-  sA[w][lane] = lane < dv ? i : 0x7fffffff;
-  __syncwarp();
-  // stars over H_v (|D_v| <= dv <= 32)
-  const int64_t hb = a.hoff[v];
-  const int D = (int)(a.hoff[v + 1] - hb);
-  int32_t xa = 0, ha = 0;
-  if (lane < D) {
-    xa = a.hkey[hb + lane];
-    ha = a.hcnt[hb + lane];
-  }
-  const int64_t c = dv - 4;
-  double Ws = 0.0;
-  for (int bb = 0; bb < D; ++bb) {
-    int32_t xb = __shfl_sync(0xffffffffu, xa, bb);
-    int32_t hbv = __shfl_sync(0xffffffffu, ha, bb);
-    if (lane < bb) Ws += (double)((int64_t)ha * hbv) * a.F[c + xa + xb];
-  }
-  if (lane < D) Ws += (double)((int64_t)ha * (ha - 1) / 2) * a.F[c + 2 * xa];
-  Ws *= 2.0;
-  // triangles: 4 groups of 8 lanes, group g walks Adj+(A[x]) for x = g, g+4, ...
-  const int g = lane >> 3, sub = lane & 7;
-  int64_t tri = 0;
-  double Wt = 0.0;
-  for (int x = g; x < dv; x += 4) {
-    const int32_t ii = sA[w][x];
-    const int32_t dix = a.nd[ob + x];
-    const int64_t pb = a.offp[ii], pe = a.offp[ii + 1];
-    for (int64_t p = pb + sub; p < pe; p += 8) {
-      const int2 jd = a.adjp[p];
-      // binary search in sorted sA[w][0..dv)
-      int lo = 0, hi = dv;
-      while (lo < hi) {
-        int mid = (lo + hi) >> 1;
-        if (sA[w][mid] < jd.x) lo = mid + 1; else hi = mid;
-      }
-      if (lo < dv && sA[w][lo] == jd.x) {
-        const int64_t S = (int64_t)dv + dix + jd.y;
-        Wt += a.F[S - 6] - a.F[S - 4];
-        ++tri;
-      }
-    }
-  }
-  Tc = warp_sum(Tc);
-  tri = warp_sum(tri);
-  Ws = warp_sum(Ws);
-  Wc = warp_sum(Wc);
-  Wt = warp_sum(Wt);
-  if (lane == 0) finalize(a, v, dv, Tc, tri, Ws, Wc, Wt);
-}
-
-__device__ __forceinline__ uint32_t hslot(int32_t key, int shift) {
-  return ((uint32_t)key * 2654435761u) >> shift;
-}
-
-// Block-wide fixed-order reductions (deterministic).
+// Block-wide fixed-order sum (deterministic); result valid in thread 0.
 template <int THREADS, class T>
 __device__ __forceinline__ T block_sum(T x, T* scratch) {
   x = warp_sum(x);
@@ -272,151 +179,538 @@ __device__ __forceinline__ T block_sum(T x, T* scratch) {
   T r = 0;
   if (threadIdx.x == 0)
     for (int k = 0; k < THREADS / 32; ++k) r += scratch[k];
-  return r;  // valid in thread 0
+  return r;
 }
 
-// Seeds with 32 < dv <= SLOTS/2: one CTA per seed, A in a shared-memory hash
-// set (open addressing, load <= 1/2).  Seeds with larger dv (hubs) use a
-// per-CTA bitmap over node ids in global memory (BITMAP = true).
-template <int THREADS, int SLOTS, bool BITMAP>
-__global__ void __launch_bounds__(THREADS)
-k_seed_block(const int32_t* __restrict__ seeds, int64_t count, FArgs a, uint32_t* __restrict__ bitmaps,
-             int64_t bitmap_words) {
-  extern __shared__ int32_t table[];  // SLOTS entries (unused when BITMAP)
-  __shared__ double red_d[THREADS / 32];
-  __shared__ int64_t red_i[THREADS / 32];
+// Chain term of seed v (one group per row, slots strided over lanes):
+//   Tc(v) = sum_i (di-1)(dv+di-4) + S1(i) - dv          (chains through i, exact int)
+//   Wc(v) = sum_i C_i(dv),  C_i(dv) = sum_x H_i(x) F(dv+di-4+x) - F(2dv+di-4)
+// C_i(dv) is found by binary search of dv in i's distinct-degree list.
+__device__ __forceinline__ void chain_slot(const FArgs& a, int64_t e, int64_t dv, int64_t& Tc, double& Wc) {
+  const int32_t i = a.nbr[e];
+  const int64_t di = a.nd[e];
+  Tc += (di - 1) * (dv + di - 4) + a.s1[i] - dv;
+  int64_t lo = a.hoff[i], hi = a.hoff[i + 1] - 1;
+  while (lo < hi) {  // dv is present: v is a neighbour of i
+    int64_t mid = (lo + hi) >> 1;
+    if (__ldg(a.hkey + mid) < dv) lo = mid + 1; else hi = mid;
+  }
+  Wc += __ldg(a.ctab + lo);
+}
+
+__global__ void k_chain_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
+  const int lane = threadIdx.x & 31;
+  int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (q >= count) return;
+  const int32_t v = seeds[q];
+  const int64_t b = a.offsets[v], e = a.offsets[v + 1];
+  int64_t Tc = 0;
+  double Wc = 0.0;
+  for (int64_t p = b + lane; p < e; p += 32) chain_slot(a, p, e - b, Tc, Wc);
+  Tc = warp_sum(Tc);
+  Wc = warp_sum(Wc);
+  if (lane == 0) {
+    a.Tc[v - a.seed_lo] = Tc;
+    a.Wc[v - a.seed_lo] = Wc;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_chain_block(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
+  __shared__ int64_t red_i[8];
+  __shared__ double red_d[8];
   const int64_t q = blockIdx.x;
   if (q >= count) return;
   const int32_t v = seeds[q];
-  const int64_t ob = a.offsets[v];
-  const int32_t dv = (int32_t)(a.offsets[v + 1] - ob);
-  constexpr int kShift = 32 - __builtin_ctz(SLOTS);
-  uint32_t* bm = BITMAP ? bitmaps + (int64_t)blockIdx.x * bitmap_words : nullptr;
-  if (!BITMAP) {
-    for (int s = threadIdx.x; s < SLOTS; s += THREADS) table[s] = -1;
-    __syncthreads();
-  }
-  // insert A; per-neighbour chain terms
+  const int64_t b = a.offsets[v], e = a.offsets[v + 1];
   int64_t Tc = 0;
   double Wc = 0.0;
-  for (int x = threadIdx.x; x < dv; x += THREADS) {
-    const int32_t i = a.nbr[ob + x];
-    const int32_t di = a.nd[ob + x];
-    Tc += (int64_t)(di - 1) * (dv + di - 4) + a.s1[i] - dv;
-    Wc += ctab_lookup(a, i, dv);
-    if (BITMAP) {
-      atomicOr(bm + (i >> 5), 1u << (i & 31));
-    } else {
-      uint32_t s = hslot(i, kShift);
-      while (atomicCAS(&table[s], -1, i) != -1) s = (s + 1) & (SLOTS - 1);
-    }
+  for (int64_t p = b + threadIdx.x; p < e; p += 256) chain_slot(a, p, e - b, Tc, Wc);
+  Tc = block_sum<256>(Tc, red_i);
+  Wc = block_sum<256>(Wc, red_d);
+  if (threadIdx.x == 0) {
+    a.Tc[v - a.seed_lo] = Tc;
+    a.Wc[v - a.seed_lo] = Wc;
   }
-  // stars over H_v: thread handles rows a = t, t+THREADS, ...
+}
+
+// Stars over H_v, warp per seed (|D_v| <= 32):
+//   Ws = 2 [ sum_{a<b} h_a h_b F(dv-4+x_a+x_b) + sum_a C(h_a,2) F(dv-4+2x_a) ]
+__global__ void k_stars_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
+  const int lane = threadIdx.x & 31;
+  int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (q >= count) return;
+  const int32_t v = seeds[q];
+  const int64_t dv = a.offsets[v + 1] - a.offsets[v];
   const int64_t hb = a.hoff[v];
   const int D = (int)(a.hoff[v + 1] - hb);
+  int32_t xa = 0;
+  int64_t ha = 0;
+  if (lane < D) {
+    xa = a.hkey[hb + lane];
+    ha = a.hcnt[hb + lane];
+  }
   const int64_t c = dv - 4;
   double Ws = 0.0;
-  for (int ra = threadIdx.x; ra < D; ra += THREADS) {
-    const int32_t xa = a.hkey[hb + ra];
-    const int64_t ha = a.hcnt[hb + ra];
-    double acc = (double)(ha * (ha - 1) / 2) * a.F[c + 2 * xa];
-    const int64_t base = c + xa;
-    for (int rb = ra + 1; rb < D; ++rb) acc += (double)(ha * __ldg(a.hcnt + hb + rb)) * __ldg(a.F + base + __ldg(a.hkey + hb + rb));
+  for (int bb = 1; bb < D; ++bb) {
+    int32_t xb = __shfl_sync(0xffffffffu, xa, bb);
+    int64_t hbv = __shfl_sync(0xffffffffu, ha, bb);
+    if (lane < bb) Ws += (double)(ha * hbv) * __ldg(a.F + c + xa + xb);
+  }
+  if (lane < D && ha > 1) Ws += (double)(ha * (ha - 1) / 2) * __ldg(a.F + c + 2 * xa);
+  Ws = warp_sum(Ws);
+  if (lane == 0) a.Ws[v - a.seed_lo] = 2.0 * Ws;
+}
+
+// Stars for |D_v| > 32: CTA per seed, H_v staged in shared memory.
+__global__ void __launch_bounds__(256) k_stars_block(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
+  extern __shared__ int32_t sh[];
+  __shared__ double red[8];
+  const int64_t q = blockIdx.x;
+  if (q >= count) return;
+  const int32_t v = seeds[q];
+  const int64_t dv = a.offsets[v + 1] - a.offsets[v];
+  const int64_t hb = a.hoff[v];
+  const int D = (int)(a.hoff[v + 1] - hb);
+  int32_t* sk = sh;
+  int32_t* sc = sh + D;
+  for (int t = threadIdx.x; t < D; t += 256) {
+    sk[t] = a.hkey[hb + t];
+    sc[t] = a.hcnt[hb + t];
+  }
+  __syncthreads();
+  const int64_t c = dv - 4;
+  double Ws = 0.0;
+  // row ra pairs with rb > ra; rows dealt from both ends for balance
+  for (int r = threadIdx.x; r < D; r += 256) {
+    const int ra = (r & 1) ? D - 1 - (r >> 1) : (r >> 1);
+    const int64_t ha = sc[ra];
+    const int64_t base = c + sk[ra];
+    double acc = ha > 1 ? (double)(ha * (ha - 1) / 2) * __ldg(a.F + base + sk[ra]) : 0.0;
+    for (int rb = ra + 1; rb < D; ++rb) acc += (double)(ha * sc[rb]) * __ldg(a.F + base + sk[rb]);
     Ws += acc;
   }
-  Ws *= 2.0;
-  __syncthreads();  // membership structure complete
-  if (BITMAP) __threadfence_block();
-  // triangles: groups of 8 lanes walk Adj+(A[x])
-  constexpr int G = 8, NG = THREADS / G;
-  const int grp = threadIdx.x / G, sub = threadIdx.x & (G - 1);
-  int64_t tri = 0;
-  double Wt = 0.0;
-  for (int x = grp; x < dv; x += NG) {
-    const int32_t ii = a.nbr[ob + x];
-    const int32_t dix = a.nd[ob + x];
-    const int64_t pb = a.offp[ii], pe = a.offp[ii + 1];
-    for (int64_t p = pb + sub; p < pe; p += G) {
-      const int2 jd = a.adjp[p];
-      bool hit;
-      if (BITMAP) {
-        hit = (__ldcg(bm + (jd.x >> 5)) >> (jd.x & 31)) & 1u;
-      } else {
-        uint32_t s = hslot(jd.x, kShift);
-        int32_t k;
-        while ((k = table[s]) != jd.x && k != -1) s = (s + 1) & (SLOTS - 1);
-        hit = k == jd.x;
+  Ws = block_sum<256>(Ws, red);
+  if (threadIdx.x == 0) a.Ws[v - a.seed_lo] = 2.0 * Ws;
+}
+
+// ------------------------------------------------------------- triangles
+// W_t(v) = sum over triangles {v,i,j} of F(S-6) - F(S-4), S = dv+di+dj, and
+// t(v) = their number.  Every triangle at v is met exactly once as a probe
+// "j in Adj(v)?" for j in Adj+(i), i in Adj(v): the edge i-j lies in exactly
+// one of Adj+(i), Adj+(j).  A seed's probes form a flattened item space over
+// its rows x (row x = Adj+(A[x]), pc_x items); threads take runs of kRun
+// consecutive items, keep the current row in registers (no search per item)
+// and issue the run's loads before probing.  Membership is a shared-memory
+// hash of Adj(v) (load <= 1/4, linear probing) or, for hubs, a bitmap.
+
+// Open-addressing set of node ids in shared memory (SLOTS a power of two).
+template <int SLOTS>
+struct SmemSet {
+  int32_t* t;
+  static constexpr int kShift = 32 - __builtin_ctz(SLOTS);
+  __device__ __forceinline__ void clear(int tid, int nthr) {
+    for (int s = tid; s < SLOTS; s += nthr) t[s] = -1;
+  }
+  __device__ __forceinline__ void insert(int32_t key) {
+    uint32_t s = ((uint32_t)key * 2654435761u) >> kShift;
+    while (atomicCAS(&t[s], -1, key) != -1) s = (s + 1) & (SLOTS - 1);
+  }
+  __device__ __forceinline__ bool contains(int32_t key) const {
+    uint32_t s = ((uint32_t)key * 2654435761u) >> kShift;
+    int32_t k;
+    while ((k = t[s]) != key && k != -1) s = (s + 1) & (SLOTS - 1);
+    return k == key;
+  }
+};
+
+struct BitmapSet {
+  const uint32_t* bm;
+  __device__ __forceinline__ bool contains(int32_t j) const { return (__ldg(bm + (j >> 5)) >> (j & 31)) & 1u; }
+};
+
+// Items [qbeg, qend) of a seed whose rows 0..X-1 have prefix pre[0..X]
+// (shared memory) and Adj+ starts sps[0..X).  With `ph` the last item of every
+// row is a placeholder (hub tasks, whose prefixes count pc+1).
+template <class Set>
+__device__ __forceinline__ void tri_runs(const FArgs& a, int64_t ob_rows, int64_t dv, const int32_t* pre,
+                                         const int32_t* sps, int X, int qbeg, int qend, int tid, int nthr,
+                                         const Set& set, bool ph, int64_t& tri, double& Wt) {
+  for (int q0 = qbeg + tid * kRun; q0 < qend; q0 += nthr * kRun) {
+    int k = 0, hi = X;  // last row with pre[k] <= q0
+    while (hi - k > 1) {
+      int mid = (k + hi) >> 1;
+      if (pre[mid] <= q0) k = mid; else hi = mid;
+    }
+    int row_end = pre[k + 1] - (ph ? 1 : 0);
+    int ptr = sps[k] + (q0 - pre[k]);
+    int32_t jv[kRun];
+    int kr[kRun];
+#pragma unroll
+    for (int u = 0; u < kRun; ++u) {
+      const int q = q0 + u;
+      jv[u] = -1;
+      if (q < qend) {
+        while (q >= row_end) {
+          if (ph && q < pre[k + 1]) break;  // placeholder item of row k
+          ++k;
+          row_end = pre[k + 1] - (ph ? 1 : 0);
+          ptr = sps[k];
+        }
+        if (q < row_end) {
+          jv[u] = __ldg(a.adjj + ptr);
+          ++ptr;
+        }
+        kr[u] = k;
       }
-      if (hit) {
-        const int64_t S = (int64_t)dv + dix + jd.y;
-        Wt += a.F[S - 6] - a.F[S - 4];
+    }
+#pragma unroll
+    for (int u = 0; u < kRun; ++u) {
+      if (jv[u] >= 0 && set.contains(jv[u])) {
+        const int64_t S = dv + __ldg(a.nd + ob_rows + kr[u]) + __ldg(a.deg + jv[u]);
+        Wt += __ldg(a.F + S - 6) - __ldg(a.F + S - 4);
         ++tri;
       }
     }
   }
-  Tc = block_sum<THREADS>(Tc, red_i);
-  tri = block_sum<THREADS>(tri, red_i);
-  Ws = block_sum<THREADS>(Ws, red_d);
-  Wc = block_sum<THREADS>(Wc, red_d);
-  Wt = block_sum<THREADS>(Wt, red_d);
-  if (threadIdx.x == 0) finalize(a, v, dv, Tc, tri, Ws, Wc, Wt);
 }
 
-struct DegClass {
-  const int32_t* deg;
-  int32_t lo, hi;  // lo < deg <= hi
+// dv <= 32: warp per seed; per-warp 128-slot set and 33-entry row prefix.
+constexpr int kTriWarps = 8;
+__global__ void __launch_bounds__(kTriWarps * 32)
+k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
+  __shared__ int32_t sT[kTriWarps][128];
+  __shared__ int32_t sPre[kTriWarps][33];
+  __shared__ int32_t sPs[kTriWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * kTriWarps + w;
+  if (q >= count) return;
+  const int32_t v = seeds[q];
+  const int64_t ob = a.offsets[v];
+  const int dv = (int)(a.offsets[v + 1] - ob);
+  SmemSet<128> set{sT[w]};
+  set.clear(lane, 32);
+  __syncwarp();
+  int32_t cnt = 0;
+  if (lane < dv) {
+    set.insert(a.nbr[ob + lane]);
+    cnt = a.pc[ob + lane];
+    sPs[w][lane] = (int32_t)a.ps[ob + lane];
+  }
+  int32_t incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  sPre[w][lane + 1] = incl;
+  if (lane == 0) sPre[w][0] = 0;
+  const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  __syncwarp();
+  int64_t tri = 0;
+  double Wt = 0.0;
+  tri_runs(a, ob, dv, sPre[w], sPs[w], dv, 0, total, lane, 32, set, false, tri, Wt);
+  tri = warp_sum(tri);
+  Wt = warp_sum(Wt);
+  if (lane == 0) {
+    a.tri[v - a.seed_lo] = tri;
+    a.Wt[v - a.seed_lo] = Wt;
+  }
+}
+
+// 32 < dv <= MAXD: CTA per seed, every row staged (prefix by block scan).
+template <int THREADS, int MAXD>
+__global__ void __launch_bounds__(THREADS)
+k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
+  constexpr int SLOTS = 4 * MAXD;
+  extern __shared__ int32_t dyn[];
+  int32_t* table = dyn;                 // SLOTS
+  int32_t* pre = dyn + SLOTS;           // MAXD + 1
+  int32_t* sps = pre + MAXD + 1;        // MAXD
+  __shared__ int32_t wsum[THREADS / 32];
+  __shared__ int64_t red_i[THREADS / 32];
+  __shared__ double red_d[THREADS / 32];
+  constexpr int PER = (MAXD + THREADS - 1) / THREADS;
+  const int64_t qs = blockIdx.x;
+  if (qs >= count) return;
+  const int32_t v = seeds[qs];
+  const int64_t ob = a.offsets[v];
+  const int dv = (int)(a.offsets[v + 1] - ob);
+  SmemSet<SLOTS> set{table};
+  set.clear(threadIdx.x, THREADS);
+  __syncthreads();
+  // insert Adj(v); block exclusive scan of pc over the rows (PER rows per thread)
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int32_t loc[PER];
+  int32_t sum = 0;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int x = threadIdx.x * PER + u;
+    loc[u] = 0;
+    if (x < dv) {
+      set.insert(a.nbr[ob + x]);
+      loc[u] = a.pc[ob + x];
+      sps[x] = (int32_t)a.ps[ob + x];
+    }
+    sum += loc[u];
+  }
+  int32_t incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  int32_t wpre = 0;
+  for (int k = 0; k < w; ++k) wpre += wsum[k];
+  int32_t run = wpre + incl - sum;
+#pragma unroll
+  for (int u = 0; u < PER; ++u) {
+    const int x = threadIdx.x * PER + u;
+    if (x < dv) pre[x] = run;
+    run += loc[u];
+  }
+  int32_t total = 0;
+  for (int k = 0; k < THREADS / 32; ++k) total += wsum[k];
+  if (threadIdx.x == 0) pre[dv] = total;
+  __syncthreads();
+  int64_t tri = 0;
+  double Wt = 0.0;
+  tri_runs(a, ob, dv, pre, sps, dv, 0, total, threadIdx.x, THREADS, set, false, tri, Wt);
+  tri = block_sum<THREADS>(tri, red_i);
+  Wt = block_sum<THREADS>(Wt, red_d);
+  if (threadIdx.x == 0) {
+    a.tri[v - a.seed_lo] = tri;
+    a.Wt[v - a.seed_lo] = Wt;
+  }
+}
+
+// Hubs (dv > kHashMaxDeg): tasks of kTask items (prefix tp counts pc+1 so a
+// task spans at most kTask+1 rows), one CTA each; membership from the hub's
+// bitmap over node ids (built once, L2-resident while its tasks run).
+struct TriTasks {
+  const int32_t* seed;      // [ntasks]
+  const int32_t* x0;        // [ntasks] first row position of the task
+  const int64_t* first;     // [ntasks] index of the seed's first task
+  const int32_t* hub_slot;  // [n] bitmap index
+  const uint32_t* bitmaps;
+  int64_t words;
+  int64_t* ptri;            // [ntasks]
+  double* pWt;              // [ntasks]
+};
+
+__global__ void __launch_bounds__(kTaskThreads)
+k_tri_task(FArgs a, TriTasks tk, int64_t ntasks) {
+  __shared__ int32_t stp[kTask + 2];
+  __shared__ int32_t sps[kTask + 1];
+  __shared__ int64_t red_i[kTaskThreads / 32];
+  __shared__ double red_d[kTaskThreads / 32];
+  const int64_t t = blockIdx.x;
+  if (t >= ntasks) return;
+  const int32_t v = tk.seed[t];
+  const int64_t ob = a.offsets[v];
+  const int dv = (int)(a.offsets[v + 1] - ob);
+  const int64_t qa = (t - tk.first[t]) * (int64_t)kTask;
+  const int64_t work = a.tp[ob + dv - 1] + a.pc[ob + dv - 1] + 1;
+  const int64_t qb = qa + kTask < work ? qa + kTask : work;
+  const int xa = tk.x0[t];
+  const int X = dv - xa < kTask + 1 ? dv - xa : kTask + 1;
+  for (int k = threadIdx.x; k <= X; k += kTaskThreads) {
+    const int64_t e = ob + xa + k;
+    stp[k] = (int32_t)((xa + k < dv ? a.tp[e] : work) - qa);
+    if (k < X) sps[k] = (int32_t)a.ps[e];
+  }
+  __syncthreads();
+  BitmapSet set{tk.bitmaps + (int64_t)tk.hub_slot[v] * tk.words};
+  int64_t tri = 0;
+  double Wt = 0.0;
+  tri_runs(a, ob + xa, dv, stp, sps, X, 0, (int)(qb - qa), threadIdx.x, kTaskThreads, set, true, tri, Wt);
+  tri = block_sum<kTaskThreads>(tri, red_i);
+  Wt = block_sum<kTaskThreads>(Wt, red_d);
+  if (threadIdx.x == 0) {
+    tk.ptri[t] = tri;
+    tk.pWt[t] = Wt;
+  }
+}
+
+// Per-row exclusive prefix of (pc + 1) -> tp, and the seed's task count (warp per row).
+__global__ void k_tri_prefix(const int64_t* __restrict__ offsets, const int32_t* __restrict__ pc,
+                             const int32_t* __restrict__ seeds, int64_t count, int64_t* __restrict__ tp,
+                             int64_t* __restrict__ ntask) {
+  const int lane = threadIdx.x & 31;
+  int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (q >= count) return;
+  const int32_t v = seeds[q];
+  const int64_t b = offsets[v], e = offsets[v + 1];
+  int64_t carry = 0;
+  for (int64_t p0 = b; p0 < e; p0 += 32) {
+    const int64_t p = p0 + lane;
+    const int64_t x = p < e ? (int64_t)pc[p] + 1 : 0;
+    int64_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (p < e) tp[p] = carry + incl - x;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) ntask[q] = ceil_div(carry, kTask);
+}
+
+// Task records: for each slot, every task whose first item falls in it.
+__global__ void k_tri_fill(const int64_t* __restrict__ offsets, const int32_t* __restrict__ seeds, int64_t count,
+                           const int64_t* __restrict__ tp, const int32_t* __restrict__ pc,
+                           const int64_t* __restrict__ tstart, int32_t* __restrict__ tseed,
+                           int32_t* __restrict__ tx0, int64_t* __restrict__ tfirst) {
+  const int lane = threadIdx.x & 31;
+  int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (q >= count) return;
+  const int32_t v = seeds[q];
+  const int64_t b = offsets[v], e = offsets[v + 1];
+  const int64_t base = tstart[q];
+  for (int64_t p = b + lane; p < e; p += 32) {
+    const int64_t lo = tp[p], hi = lo + pc[p] + 1;  // items [lo, hi)
+    for (int64_t k = ceil_div(lo, kTask); k * kTask < hi; ++k) {
+      tseed[base + k] = v;
+      tx0[base + k] = (int32_t)(p - b);
+      tfirst[base + k] = base;
+    }
+  }
+}
+
+__global__ void k_tri_merge(const int32_t* __restrict__ seeds, int64_t count, const int64_t* __restrict__ tstart,
+                            const int64_t* __restrict__ ptri, const double* __restrict__ pWt, FArgs a) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const int32_t v = seeds[q];
+  int64_t tri = 0;
+  double Wt = 0.0;
+  for (int64_t t = tstart[q]; t < tstart[q + 1]; ++t) {
+    tri += ptri[t];
+    Wt += pWt[t];
+  }
+  a.tri[v - a.seed_lo] = tri;
+  a.Wt[v - a.seed_lo] = Wt;
+}
+
+__global__ void k_hub_bitmaps(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ offsets,
+                              const int32_t* __restrict__ nbr, uint32_t* __restrict__ bitmaps, int64_t words,
+                              int32_t* __restrict__ hub_slot) {
+  int64_t h = blockIdx.x;
+  if (h >= nhubs) return;
+  int32_t v = hubs[h];
+  if (threadIdx.x == 0) hub_slot[v] = (int32_t)h;
+  uint32_t* bm = bitmaps + h * words;
+  for (int64_t p = offsets[v] + threadIdx.x; p < offsets[v + 1]; p += blockDim.x) {
+    int32_t i = nbr[p];
+    atomicOr(bm + (i >> 5), 1u << (i & 31));
+  }
+}
+
+// Epilogue: closed-form T and mass, W, EF = ln T - W/T, flags.
+__global__ void k_epilogue(FArgs a, int64_t count, double* __restrict__ ef, int64_t* __restrict__ total,
+                           uint8_t* __restrict__ flags, int64_t* __restrict__ T_out, double* __restrict__ W_out) {
+  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const int64_t v = a.seed_lo + q;
+  const int64_t dv = a.offsets[v + 1] - a.offsets[v];
+  const int64_t s1v = a.s1[v];
+  const int64_t tri = a.tri[q];
+  const int64_t T = dv * (dv - 1) * (dv - 4) + 2 * (dv - 1) * s1v + a.Tc[q] - 8 * tri;
+  const int64_t mass = dv * (dv - 1) + s1v - dv;
+  const double W = (a.Ws[q] + a.Wc[q]) + 4.0 * a.Wt[q];
+  double e = 0.0;
+  // entropy >= 0: clamp the last-ulp cancellation of ln T - W/T when only one
+  // positive-degree cluster class exists (EF mathematically 0)
+  if (T > 0) e = fmax(log((double)T) - W / (double)T, 0.0);
+  ef[q] = e;
+  total[q] = mass;
+  flags[q] = mass == 0 ? 1 : (T == 0 ? 2 : 0);
+  if (T_out) T_out[q] = T;
+  if (W_out) W_out[q] = W;
+}
+
+struct DegRange {
+  const int64_t* offsets;
+  int64_t lo, hi;  // lo < dv <= hi
   __host__ __device__ bool operator()(const int32_t& v) const {
-    int32_t d = deg[v];
+    int64_t d = offsets[v + 1] - offsets[v];
     return d > lo && d <= hi;
   }
 };
 
-}  // namespace
+struct HistRange {
+  const int64_t* hoff;
+  int64_t lo, hi;  // lo < |D_v| <= hi
+  __host__ __device__ bool operator()(const int32_t& v) const {
+    int64_t d = hoff[v + 1] - hoff[v];
+    return d > lo && d <= hi;
+  }
+};
 
-// Class boundaries (by dv): warp | block-S | block-M | block-L | hub bitmap.
-static constexpr int32_t kClassHi[5] = {32, 256, 2048, 16384, 0x7fffffff};
+template <class Pred>
+int64_t select_seeds(Context& ctx, SeedRange r, Pred pred, int32_t* out, const char* tag) {
+  cudaStream_t s = ctx.stream;
+  size_t tmp = 0;
+  int64_t* nsel_d = ctx.buf(std::string("sel_") + tag).as<int64_t>(1);
+  cub::CountingInputIterator<int32_t> it((int32_t)r.lo);
+  const int64_t cnt = r.hi - r.lo;
+  EFG_CUDA_CHECK(cub::DeviceSelect::If(nullptr, tmp, it, out, nsel_d, cnt, pred, s));
+  EFG_REGION("cub::DeviceSelect::If", s,
+             EFG_CUDA_CHECK(cub::DeviceSelect::If(ctx.buf("cub").get(tmp), tmp, it, out, nsel_d, cnt, pred, s)));
+  int64_t nsel = 0;
+  EFG_CUDA_CHECK(cudaMemcpyAsync(&nsel, nsel_d, sizeof nsel, cudaMemcpyDeviceToHost, s));
+  EFG_CUDA_CHECK(cudaStreamSynchronize(s));
+  return nsel;
+}
 
-namespace {
-__global__ void k_seed_work(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
-                            const int64_t* __restrict__ offp, const int64_t* __restrict__ hoff, int64_t n,
-                            int64_t* __restrict__ work) {
+__global__ void k_seed_work(const int64_t* __restrict__ offsets, const int32_t* __restrict__ pcv,
+                            const int64_t* __restrict__ hoff, int64_t n, int64_t* __restrict__ work) {
   const int lane = threadIdx.x & 31;
   int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (v >= n) return;
   int64_t b = offsets[v], e = offsets[v + 1];
   int64_t w = 0;
-  for (int64_t p = b + lane; p < e; p += 32) {
-    int32_t i = nbr[p];
-    w += offp[i + 1] - offp[i] + 8;  // triangle probes + chain lookup
-  }
+  for (int64_t p = b + lane; p < e; p += 32) w += pcv[p] + 8;  // triangle probes + chain lookup
   w = warp_sum(w);
   if (lane == 0) {
     int64_t D = hoff[v + 1] - hoff[v];
     work[v] = w + D * (D + 1) / 2 + 64;
   }
 }
+
 }  // namespace
 
 // Neighbour-degree histograms H_i for every node (sorted distinct degrees +
 // counts).  Returns the number of entries.
-static int64_t build_histograms(Context& ctx, Prepared& P, int64_t*& hoff, int32_t*& hkey, int32_t*& hcnt) {
+static int64_t build_histograms(Context& ctx, Prepared& P, int64_t*& hoff, int32_t*& hkey, int32_t*& hcnt,
+                                int64_t* maxD = nullptr) {
   cudaStream_t s = ctx.stream;
   const int64_t n = P.g.n, m2 = P.g.m2;
   const int B = 256;
   EFG_REQUIRE(m2 < (int64_t(1) << 31), "adjacency too large for the segmented sort (2m >= 2^31)");
-  // 1. neighbour-degree histograms H_i (sorted distinct degrees + counts)
   int32_t* snd = ctx.buf("f_snd").as<int32_t>(m2);
   size_t tmp = 0;
   EFG_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, P.nd, snd, (int)m2, (int)n, P.g.offsets,
                                                     P.g.offsets + 1, s));
-  EFG_REGION("cub::DeviceSegmentedSort::SortKeys", s, EFG_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(ctx.buf("cub").get(tmp), tmp, P.nd, snd, (int)m2, (int)n,
-                                                    P.g.offsets, P.g.offsets + 1, s)));
+  EFG_REGION("cub::DeviceSegmentedSort::SortKeys", s,
+             EFG_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(ctx.buf("cub").get(tmp), tmp, P.nd, snd, (int)m2,
+                                                               (int)n, P.g.offsets, P.g.offsets + 1, s)));
   int64_t* dcnt = ctx.buf("f_dcnt").as<int64_t>(n + 1);
   hoff = ctx.buf("f_hoff").as<int64_t>(n + 1);
   EFG_LAUNCH(k_rle_count, ceil_div(n * 32, B), B, 0, s, P.g.offsets, snd, n, dcnt);
   EFG_CUDA_CHECK(cudaMemsetAsync(dcnt + n, 0, sizeof(int64_t), s));
   EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, dcnt, hoff, n + 1, s));
-  EFG_REGION("cub::DeviceScan::ExclusiveSum", s, EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dcnt, hoff, n + 1, s)));
+  EFG_REGION("cub::DeviceScan::ExclusiveSum", s,
+             EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dcnt, hoff, n + 1, s)));
+  if (maxD) {
+    int64_t* dmx = ctx.buf("f_maxD").as<int64_t>(1);
+    EFG_CUDA_CHECK(cub::DeviceReduce::Max(nullptr, tmp, dcnt, dmx, n, s));
+    EFG_REGION("cub::DeviceReduce::Max", s,
+               EFG_CUDA_CHECK(cub::DeviceReduce::Max(ctx.buf("cub").get(tmp), tmp, dcnt, dmx, n, s)));
+    EFG_CUDA_CHECK(cudaMemcpyAsync(maxD, dmx, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  }
   int64_t nh = 0;
   EFG_CUDA_CHECK(cudaMemcpyAsync(&nh, hoff + n, sizeof nh, cudaMemcpyDeviceToHost, s));
   EFG_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -431,8 +725,7 @@ void factorized_work(Context& ctx, Prepared& P, int64_t* d_work) {
   int32_t *hkey, *hcnt;
   build_histograms(ctx, P, hoff, hkey, hcnt);
   const int B = 256;
-  EFG_LAUNCH(k_seed_work, ceil_div(P.g.n * 32, B), B, 0, ctx.stream, P.g.offsets, P.g.nbr, P.offp, hoff, P.g.n,
-             d_work);
+  EFG_LAUNCH(k_seed_work, ceil_div(P.g.n * 32, B), B, 0, ctx.stream, P.g.offsets, P.pc, hoff, P.g.n, d_work);
 }
 
 void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* total, uint8_t* flags,
@@ -441,76 +734,121 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   const int64_t n = P.g.n;
   const int B = 256;
   size_t tmp = 0;
+  const int64_t cnt = r.hi - r.lo;
+  if (cnt <= 0) return;
   int64_t* hoff;
   int32_t *hkey, *hcnt;
-  const int64_t nh = build_histograms(ctx, P, hoff, hkey, hcnt);
+  int64_t maxD = 0;
+  const int64_t nh = build_histograms(ctx, P, hoff, hkey, hcnt, &maxD);
+  // 1. chain tables C_i(y): rows with <= 64 distinct degrees by 8-lane groups, the rest by CTAs
   double* ctab = ctx.buf("f_ctab").as<double>(nh);
-  // 2. chain tables: rows with <= kBig distinct degrees by 8-lane groups, the rest by CTAs
   {
     const int64_t kBig = 64;
     int32_t* rows = ctx.buf("f_rows").as<int32_t>(n);
-    int64_t* nrows_d = ctx.buf("f_nrows").as<int64_t>(1);
     EFG_LAUNCH(k_ctab_group<8>, ceil_div(n * 8, B), B, 0, s, hoff, hkey, hcnt, P.deg, P.ftab, n, kBig, ctab);
-    cub::CountingInputIterator<int32_t> rit(0);
-    BigRow pred{hoff, kBig};
-    EFG_CUDA_CHECK(cub::DeviceSelect::If(nullptr, tmp, rit, rows, nrows_d, n, pred, s));
-    EFG_REGION("cub::DeviceSelect::If", s, EFG_CUDA_CHECK(cub::DeviceSelect::If(ctx.buf("cub").get(tmp), tmp, rit, rows, nrows_d, n, pred, s)));
-    int64_t nrows = 0;
-    EFG_CUDA_CHECK(cudaMemcpyAsync(&nrows, nrows_d, sizeof nrows, cudaMemcpyDeviceToHost, s));
-    EFG_CUDA_CHECK(cudaStreamSynchronize(s));
+    const int64_t nrows = select_seeds(ctx, SeedRange{0, n}, BigRow{hoff, kBig}, rows, "bigrow");
     EFG_LAUNCH(k_ctab_block, nrows, 128, 0, s, rows, nrows, hoff, hkey, hcnt, P.deg, P.ftab, ctab);
   }
-  // 3. classify seeds of [lo, hi) by degree
-  const int64_t cnt = r.hi - r.lo;
   FArgs a;
   a.offsets = P.g.offsets;
   a.nbr = P.g.nbr;
   a.nd = P.nd;
-  a.deg = P.deg;
   a.s1 = P.s1;
   a.F = P.ftab;
-  a.offp = P.offp;
-  a.adjp = P.adjp;
+  a.ps = P.ps;
+  a.pc = P.pc;
+  a.tp = nullptr;
+  a.adjj = P.adjj;
+  a.deg = P.deg;
   a.hoff = hoff;
   a.hkey = hkey;
   a.hcnt = hcnt;
   a.ctab = ctab;
-  a.n = n;
   a.seed_lo = r.lo;
-  a.ef = ef;
-  a.total = total;
-  a.flags = flags;
-  a.T_out = T_out;
-  a.W_out = W_out;
-  if (cnt <= 0) return;
-  int32_t* lists = ctx.buf("f_lists").as<int32_t>(5 * cnt);
-  int64_t* ncls_d = ctx.buf("f_ncls").as<int64_t>(5);
-  cub::CountingInputIterator<int32_t> it((int32_t)r.lo);
-  for (int k = 0; k < 5; ++k) {
-    DegClass pred{P.deg, k ? kClassHi[k - 1] : 0, kClassHi[k]};
-    EFG_CUDA_CHECK(cub::DeviceSelect::If(nullptr, tmp, it, lists + k * cnt, ncls_d + k, cnt, pred, s));
-    EFG_REGION("cub::DeviceSelect::If", s, EFG_CUDA_CHECK(
-        cub::DeviceSelect::If(ctx.buf("cub").get(tmp), tmp, it, lists + k * cnt, ncls_d + k, cnt, pred, s)));
+  a.Tc = ctx.buf("f_Tc").as<int64_t>(cnt);
+  a.Wc = ctx.buf("f_Wc").as<double>(cnt);
+  a.Ws = ctx.buf("f_Ws").as<double>(cnt);
+  a.tri = ctx.buf("f_tri").as<int64_t>(cnt);
+  a.Wt = ctx.buf("f_Wt").as<double>(cnt);
+  // 2. chains: warp per row (dv <= 1024), CTA per row above
+  {
+    int32_t* list = ctx.buf("f_list_chain").as<int32_t>(cnt);
+    const int64_t nsmall = select_seeds(ctx, r, DegRange{P.g.offsets, -1, 1024}, list, "chain_s");
+    EFG_LAUNCH(k_chain_warp, ceil_div(nsmall * 32, B), B, 0, s, list, nsmall, a);
+    const int64_t nbig = select_seeds(ctx, r, DegRange{P.g.offsets, 1024, INT64_MAX}, list, "chain_b");
+    EFG_LAUNCH(k_chain_block, nbig, 256, 0, s, list, nbig, a);
   }
-  int64_t ncls[5];
-  EFG_CUDA_CHECK(cudaMemcpyAsync(ncls, ncls_d, sizeof ncls, cudaMemcpyDeviceToHost, s));
-  EFG_CUDA_CHECK(cudaStreamSynchronize(s));
-  // 4. hubs first (long CTAs), then descending classes
-  const int64_t words = ceil_div(n, 32);
-  if (ncls[4]) {
-    uint32_t* bms = ctx.buf("f_bitmaps").as<uint32_t>(ncls[4] * words);
-    EFG_CUDA_CHECK(cudaMemsetAsync(bms, 0, ncls[4] * words * sizeof(uint32_t), s));
-    EFG_LAUNCH((k_seed_block<1024, 32, true>), ncls[4], 1024, 0, s, lists + 4 * cnt, ncls[4], a, bms, words);
+  // 3. stars by |D_v|
+  {
+    int32_t* list = ctx.buf("f_list_stars").as<int32_t>(cnt);
+    const int64_t nsmall = select_seeds(ctx, r, HistRange{hoff, -1, 32}, list, "stars_s");
+    EFG_LAUNCH(k_stars_warp, ceil_div(nsmall * 32, B), B, 0, s, list, nsmall, a);
+    int32_t* list2 = ctx.buf("f_list_stars2").as<int32_t>(cnt);
+    const int64_t nbig = select_seeds(ctx, r, HistRange{hoff, 32, INT64_MAX}, list2, "stars_b");
+    if (nbig) {
+      const size_t smem = 8 * (size_t)maxD;
+      EFG_REQUIRE(smem <= 200 * 1024, "neighbour-degree histogram too wide for shared memory");
+      if (smem > 48 * 1024)
+        EFG_CUDA_CHECK(cudaFuncSetAttribute(k_stars_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      EFG_LAUNCH(k_stars_block, nbig, 256, smem, s, list2, nbig, a);
+    }
   }
-  if (ncls[3]) {
-    auto kern = k_seed_block<512, 32768, false>;
-    EFG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 32768 * 4));
-    EFG_LAUNCH(kern, ncls[3], 512, 32768 * 4, s, lists + 3 * cnt, ncls[3], a, nullptr, 0);
+  // 4. triangles
+  {
+    int32_t* list = ctx.buf("f_list_tri").as<int32_t>(cnt);
+    const int64_t nsm = select_seeds(ctx, r, DegRange{P.g.offsets, -1, 32}, list, "tri_s");
+    EFG_LAUNCH(k_tri_warp, ceil_div(nsm, kTriWarps), kTriWarps * 32, 0, s, list, nsm, a);
+    auto k_tri_seed_256 = k_tri_seed<128, 256>;
+    auto k_tri_seed_1024 = k_tri_seed<256, 1024>;
+    auto k_tri_seed_4096 = k_tri_seed<512, kHashMaxDeg>;
+    const int sm3 = 24 * kHashMaxDeg + 4;
+    EFG_CUDA_CHECK(cudaFuncSetAttribute(k_tri_seed_4096, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3));
+    const int64_t n1 = select_seeds(ctx, r, DegRange{P.g.offsets, 32, 256}, list, "tri_1");
+    EFG_LAUNCH(k_tri_seed_256, n1, 128, 24 * 256 + 4, s, list, n1, a);
+    const int64_t n2 = select_seeds(ctx, r, DegRange{P.g.offsets, 256, 1024}, list, "tri_2");
+    EFG_LAUNCH(k_tri_seed_1024, n2, 256, 24 * 1024 + 4, s, list, n2, a);
+    const int64_t n3 = select_seeds(ctx, r, DegRange{P.g.offsets, 1024, kHashMaxDeg}, list, "tri_3");
+    EFG_LAUNCH(k_tri_seed_4096, n3, 512, sm3, s, list, n3, a);
+    int32_t* hubs = ctx.buf("f_hubs").as<int32_t>(cnt);
+    const int64_t nhubs = select_seeds(ctx, r, DegRange{P.g.offsets, kHashMaxDeg, INT64_MAX}, hubs, "hubs");
+    if (nhubs) {
+      int64_t* tp = ctx.buf("f_tp").as<int64_t>(P.g.m2);
+      a.tp = tp;
+      int64_t* ntask = ctx.buf("f_ntask").as<int64_t>(nhubs + 1);
+      int64_t* tstart = ctx.buf("f_tstart").as<int64_t>(nhubs + 1);
+      EFG_LAUNCH(k_tri_prefix, ceil_div(nhubs * 32, B), B, 0, s, P.g.offsets, P.pc, hubs, nhubs, tp, ntask);
+      EFG_CUDA_CHECK(cudaMemsetAsync(ntask + nhubs, 0, sizeof(int64_t), s));
+      EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ntask, tstart, nhubs + 1, s));
+      EFG_REGION("cub::DeviceScan::ExclusiveSum", s,
+                 EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, ntask, tstart, nhubs + 1, s)));
+      int64_t ntasks = 0;
+      EFG_CUDA_CHECK(cudaMemcpyAsync(&ntasks, tstart + nhubs, sizeof ntasks, cudaMemcpyDeviceToHost, s));
+      EFG_CUDA_CHECK(cudaStreamSynchronize(s));
+      int32_t* tseed = ctx.buf("f_tseed").as<int32_t>(ntasks);
+      int32_t* tx0 = ctx.buf("f_tx0").as<int32_t>(ntasks);
+      int64_t* tfirst = ctx.buf("f_tfirst").as<int64_t>(ntasks);
+      EFG_LAUNCH(k_tri_fill, ceil_div(nhubs * 32, B), B, 0, s, P.g.offsets, hubs, nhubs, tp, P.pc, tstart, tseed, tx0,
+                 tfirst);
+      TriTasks tk;
+      tk.seed = tseed;
+      tk.x0 = tx0;
+      tk.first = tfirst;
+      tk.words = ceil_div(n, 32);
+      uint32_t* bms = ctx.buf("f_bitmaps").as<uint32_t>(nhubs * tk.words);
+      int32_t* hub_slot = ctx.buf("f_hub_slot").as<int32_t>(n);
+      EFG_CUDA_CHECK(cudaMemsetAsync(bms, 0, nhubs * tk.words * sizeof(uint32_t), s));
+      EFG_LAUNCH(k_hub_bitmaps, nhubs, 1024, 0, s, hubs, nhubs, P.g.offsets, P.g.nbr, bms, tk.words, hub_slot);
+      tk.hub_slot = hub_slot;
+      tk.bitmaps = bms;
+      tk.ptri = ctx.buf("f_ptri").as<int64_t>(ntasks);
+      tk.pWt = ctx.buf("f_pWt").as<double>(ntasks);
+      EFG_LAUNCH(k_tri_task, ntasks, kTaskThreads, 0, s, a, tk, ntasks);
+      EFG_LAUNCH(k_tri_merge, ceil_div(nhubs, B), B, 0, s, hubs, nhubs, tstart, tk.ptri, tk.pWt, a);
+      if (st) st->terms = ntasks;
+    }
   }
-  if (ncls[2]) EFG_LAUNCH((k_seed_block<256, 4096, false>), ncls[2], 256, 4096 * 4, s, lists + 2 * cnt, ncls[2], a, nullptr, 0);
-  if (ncls[1]) EFG_LAUNCH((k_seed_block<128, 512, false>), ncls[1], 128, 512 * 4, s, lists + 1 * cnt, ncls[1], a, nullptr, 0);
-  if (ncls[0]) EFG_LAUNCH(k_seed_warp, ceil_div(ncls[0], kWarpSeedWarps), kWarpSeedWarps * 32, 0, s, lists, ncls[0], a);
-  if (st) st->terms = nh;
+  // 5. epilogue
+  EFG_LAUNCH(k_epilogue, ceil_div(cnt, B), B, 0, s, a, cnt, ef, total, flags, T_out, W_out);
 }
 
 }  // namespace efg

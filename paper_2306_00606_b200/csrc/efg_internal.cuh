@@ -71,9 +71,10 @@ struct Prepared {
   double* ftab = nullptr;       // [3*dmax+8]  F[d] = d ln d (0 for d = 0)
   int64_t ftab_len = 0;
   // degree-ordered orientation: j in Adj+(i) iff (d_j, j) > (d_i, i)
-  int32_t* dplus = nullptr;     // [n]
   int64_t* offp = nullptr;      // [n+1]
-  int2* adjp = nullptr;         // [m]  (j, d_j), ascending j
+  int32_t* adjj = nullptr;      // [m]  Adj+ rows, ascending j
+  int64_t* ps = nullptr;        // [2m] per slot (v->i): offp[i]
+  int32_t* pc = nullptr;        // [2m] per slot (v->i): |Adj+(i)|
 };
 
 struct SeedRange {

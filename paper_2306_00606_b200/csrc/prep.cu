@@ -64,10 +64,10 @@ __global__ void k_row_sums(const int64_t* __restrict__ offsets, const int32_t* _
   }
 }
 
-// Warp per row: ordered compaction of Adj+(v) as packed (j, d_j).
+// Warp per row: ordered compaction of Adj+(v) (ascending j).
 __global__ void k_fill_adjp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
                             const int32_t* __restrict__ nd, int64_t n, const int64_t* __restrict__ offp,
-                            int2* __restrict__ adjp) {
+                            int32_t* __restrict__ adjj) {
   const int lane = threadIdx.x & 31;
   int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (v >= n) return;
@@ -84,9 +84,20 @@ __global__ void k_fill_adjp(const int64_t* __restrict__ offsets, const int32_t* 
       take = ranks_above(dj, j, dv, (int32_t)v);
     }
     unsigned mask = __ballot_sync(0xffffffffu, take);
-    if (take) adjp[out + __popc(mask & ((1u << lane) - 1))] = make_int2(j, dj);
+    if (take) adjj[out + __popc(mask & ((1u << lane) - 1))] = j;
     out += __popc(mask);
   }
+}
+
+// Per adjacency slot e = (v -> i): where Adj+(i) starts and how long it is.
+__global__ void k_slot_plus(const int32_t* __restrict__ nbr, int64_t m2, const int64_t* __restrict__ offp,
+                            int64_t* __restrict__ ps, int32_t* __restrict__ pc) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m2) return;
+  const int32_t i = nbr[e];
+  const int64_t a = offp[i];
+  ps[e] = a;
+  pc[e] = (int32_t)(offp[i + 1] - a);
 }
 
 struct Choose2 {
@@ -127,13 +138,16 @@ void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P)
   int64_t* dplus64 = ctx.buf("dplus64").as<int64_t>(n + 1);
   EFG_LAUNCH(k_row_sums, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.s1, dplus64);
   if (!need_orientation) return;
+  EFG_REQUIRE(m2 / 2 < (int64_t(1) << 31), "more than 2^31-1 edges: oriented adjacency index exceeds int32");
   P.offp = ctx.buf("offp").as<int64_t>(n + 1);
   EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, dplus64, P.offp, n + 1, s));
   EFG_CUDA_CHECK(cudaMemsetAsync(dplus64 + n, 0, sizeof(int64_t), s));
   EFG_REGION("cub::DeviceScan::ExclusiveSum", s, EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dplus64, P.offp, n + 1, s)));
-  P.adjp = ctx.buf("adjp").as<int2>(m2 / 2 > 0 ? m2 / 2 : 1);
-  EFG_LAUNCH(k_fill_adjp, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.offp, P.adjp);
-  P.dplus = nullptr;  // |Adj+(v)| = offp[v+1] - offp[v]
+  P.adjj = ctx.buf("adjj").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);
+  EFG_LAUNCH(k_fill_adjp, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.offp, P.adjj);
+  P.ps = ctx.buf("ps").as<int64_t>(m2);
+  P.pc = ctx.buf("pc").as<int32_t>(m2);
+  EFG_LAUNCH(k_slot_plus, ceil_div(m2, B), B, 0, s, g.nbr, m2, P.offp, P.ps, P.pc);
 }
 
 }  // namespace efg

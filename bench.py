@@ -76,6 +76,32 @@ def fingerprint(g):
     return h.hexdigest()
 
 
+# seed classes of the factorized engine's triangle kernels (csrc/ef_factor.cu): (kernel, lo < dv <= hi)
+TRI_CLASSES = [("k_tri_warp", 0, 32), ("k_tri_seed_256", 32, 256), ("k_tri_seed_1024", 256, 1024),
+               ("k_tri_seed_4096", 1024, 4096), ("k_tri_task", 4096, 1 << 40)]
+
+
+def kernel_bytes_model(offsets, neighbors):
+    """Algorithmic bytes per launch of each triangle-probe kernel:
+    per probe 4 B (the Adj+ entry j), per row 20 B (neighbour id, |Adj+|, Adj+
+    start, neighbour degree), per seed 40 B (offsets, outputs t and W_t)."""
+    deg = np.diff(offsets)
+    n = deg.size
+    src = np.repeat(np.arange(n), deg)
+    nd = deg[neighbors]
+    up = (nd > deg[src]) | ((nd == deg[src]) & (neighbors > src))
+    dplus = np.bincount(src[up], minlength=n)
+    probes_per_seed = np.add.reduceat(dplus[neighbors], offsets[:-1]) if neighbors.size else np.zeros(n)
+    out = {}
+    for name, lo, hi in TRI_CLASSES:
+        msk = (deg > lo) & (deg <= hi)
+        probes = int(probes_per_seed[msk].sum())
+        rows = int(deg[msk].sum())
+        seeds = int(msk.sum())
+        out[name] = {"probes": probes, "rows": rows, "seeds": seeds, "bytes": 4 * probes + 20 * rows + 40 * seeds}
+    return out
+
+
 def algorithmic_bytes_per_seed(offsets, neighbors):
     """B(v) = 16 + 8 dv + sum_{i in Adj v} (16 + 8 di) + 17 (int64 offsets,
     int32 ids and degrees, f64+i64+u8 outputs)."""
@@ -359,19 +385,33 @@ def main():
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel
+    # ---- roofline of the dominant kernel (live CUDA-event duration of the profiled step)
     peak, peak_kind = measured_peaks()
-    dom = max(kernels.items(), key=lambda kv: kv[1]["ms"]) if kernels else (None, {"ms": 0, "launches": 1})
-    b_seed = algorithmic_bytes_per_seed(np.asarray(g.offsets), np.asarray(g.neighbors))
-    b_alg = int(b_seed.sum())
+    dom = max(kernels.items(), key=lambda kv: kv[1]["ms"]) if kernels else (None, {"ms": 0.0, "launches": 1})
+    offs, nbrs = np.asarray(g.offsets), np.asarray(g.neighbors)
+    b_alg = int(algorithmic_bytes_per_seed(offs, nbrs).sum())
+    model = kernel_bytes_model(offs, nbrs) if args.engine == "factorized" else {}
     dom_ms = dom[1]["ms"] / max(dom[1]["launches"], 1)
+    dom_bytes = model.get(dom[0], {}).get("bytes")
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom[0])
+        except (OSError, ValueError):
+            traffic = None
     roofline = {
         "bound": "hbm", "kernel": dom[0], "unit": "GB/s", "peak": peak, "peak_kind": peak_kind,
-        "achieved": None, "frac": None, "traffic": None,
+        "achieved": dom_bytes / (dom_ms / 1e3) / 1e9 if dom_bytes else None,
+        "frac": dom_bytes / (dom_ms / 1e3) / 1e9 / peak if dom_bytes else None,
+        "traffic": traffic, "kernel_ms": dom_ms, "kernel_bytes_alg": dom_bytes,
+        "kernel_share_of_step": dom[1]["ms"] / sum(v["ms"] for v in kernels.values()) if kernels else None,
         "pass_achieved": b_alg / (ms_per_step / 1e3) / 1e9,
         "pass_frac": b_alg / (ms_per_step / 1e3) / 1e9 / peak,
         "bytes_alg_pass": b_alg,
-        "note": "pass_* = SURVEY 8(d) B_alg of the whole graph over the measured step time",
+        "note": "achieved = kernel_bytes_alg (4 B/probe + 20 B/row + 40 B/seed, DESIGN.md) / live event time; "
+                "pass_* = SURVEY 8(d) B_alg of the whole graph / step time; traffic = ncu dram bytes per launch "
+                "(profiles/dram_traffic.json)",
     }
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -392,6 +432,7 @@ def main():
         "cpu_baseline": cpu,
         "gpu_launches": int(st["launches"]) * args.steps,
         "kernels_ms": {k: round(v["ms"], 4) for k, v in sorted(kernels.items(), key=lambda kv: -kv[1]["ms"])},
+        "triangle_model": model,
         "clocks": clocks.summary(),
         "setup_s": setup_s,
         "stats": {k: v for k, v in st.items() if k not in ("T", "W")},

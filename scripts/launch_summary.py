@@ -1,0 +1,43 @@
+"""Summarise an ncu launch list (--metrics gpu__time_duration.sum,dram__bytes_*) into
+per-kernel totals for the LAST full EF pass of the run (the profiled step), and
+write profiles/dram_traffic.json (dram bytes per launch of each kernel)."""
+import collections
+import csv
+import json
+import re
+import sys
+
+
+def short(name):
+    name = re.sub(r"\(.*", "", name)
+    name = name.replace("efg::<unnamed>::", "").replace("void ", "")
+    return name.strip()
+
+
+path = sys.argv[1]
+out_json = sys.argv[2] if len(sys.argv) > 2 else None
+rows = [r for r in csv.reader(open(path)) if len(r) >= 15 and r[0] != "ID"]
+launch = collections.OrderedDict()
+for r in rows:
+    key = int(r[0])
+    d = launch.setdefault(key, {"name": r[4], "stream": r[6], "grid": r[8], "block": r[7]})
+    d[r[12]] = float(r[14].replace(",", ""))
+items = list(launch.values())
+# the profiled EF pass = from the last k_deg launch up to the first k_topk/end
+starts = [i for i, d in enumerate(items) if short(d["name"]) == "k_deg"]
+seg = items[starts[-1]:] if starts else items
+tot = collections.OrderedDict()
+for d in seg:
+    k = short(d["name"])
+    t = tot.setdefault(k, {"launches": 0, "ms": 0.0, "dram_bytes": 0.0})
+    t["launches"] += 1
+    t["ms"] += d.get("gpu__time_duration.sum", 0) / 1e6
+    t["dram_bytes"] += d.get("dram__bytes_read.sum", 0) + d.get("dram__bytes_write.sum", 0)
+all_ms = sum(t["ms"] for t in tot.values())
+print(f"{'kernel':45s} {'launches':>8s} {'ms':>9s} {'share':>6s} {'dram GB':>8s} {'GB/s':>8s}")
+for k, t in sorted(tot.items(), key=lambda kv: -kv[1]["ms"]):
+    print(f"{k[:45]:45s} {t['launches']:8d} {t['ms']:9.3f} {t['ms']/all_ms*100:5.1f}% {t['dram_bytes']/1e9:8.3f} "
+          f"{t['dram_bytes']/max(t['ms'],1e-9)/1e6:8.1f}")
+print(f"total {all_ms:.3f} ms over {sum(t['launches'] for t in tot.values())} launches (serialised, cold cache)")
+if out_json:
+    json.dump({k: t["dram_bytes"] / t["launches"] for k, t in tot.items()}, open(out_json, "w"), indent=1)

@@ -19,12 +19,17 @@ import numpy as np
 RECORD_BYTES = 17  # f64 ef + i64 cluster_total + u8 flags
 
 
+def row_bytes(pad_to: int) -> int:
+    """Bytes of one rank's packed record block: ef f64 | total i64 | flags u8 (8-aligned)."""
+    return 16 * pad_to + ((pad_to + 7) & ~7)
+
+
 def pack_shard(ef, total, flags, pad_to: int):
-    """Pack one shard's outputs into a uint8 tensor [pad_to * 17] (ef | total | flags)."""
+    """Pack one shard's outputs into a uint8 tensor [row_bytes(pad_to)] (ef | total | flags)."""
     import torch
 
     L = ef.numel()
-    buf = torch.zeros(pad_to * RECORD_BYTES, dtype=torch.uint8, device=ef.device)
+    buf = torch.zeros(row_bytes(pad_to), dtype=torch.uint8, device=ef.device)
     buf[: 8 * L] = ef.view(torch.uint8)
     buf[8 * pad_to: 8 * pad_to + 8 * L] = total.view(torch.uint8)
     buf[16 * pad_to: 16 * pad_to + L] = flags.view(torch.uint8)
@@ -36,7 +41,7 @@ def unpack_all(gathered, bounds, pad_to: int):
     import torch
 
     world = len(bounds) - 1
-    parts = gathered.view(world, pad_to * RECORD_BYTES)
+    parts = gathered.view(world, row_bytes(pad_to))
     efs, tots, fls = [], [], []
     for r in range(world):
         L = int(bounds[r + 1] - bounds[r])
@@ -75,6 +80,11 @@ def ef_sharded(dg, engine="factorized", group=None, compute=None, bounds=None):
     if world == 1:
         return ef, tot, fl
     mine = pack_shard(ef, tot, fl, pad_to)
-    gathered = torch.empty(world * mine.numel(), dtype=torch.uint8, device=dev)
-    dist.all_gather_into_tensor(gathered, mine, group=group)
+    if dist.get_backend(group) == "nccl":
+        gathered = torch.empty(world * mine.numel(), dtype=torch.uint8, device=dev)
+        dist.all_gather_into_tensor(gathered, mine, group=group)  # one NCCL all-gather over NVLink
+    else:  # gloo (CPU tests): list form
+        parts = [torch.empty_like(mine) for _ in range(world)]
+        dist.all_gather(parts, mine, group=group)
+        gathered = torch.cat(parts)
     return unpack_all(gathered, bounds, pad_to)

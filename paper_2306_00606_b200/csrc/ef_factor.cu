@@ -35,7 +35,6 @@ namespace efg {
 namespace {
 
 constexpr int kTask = 2048;          // flattened triangle items per CTA chunk / hub task
-constexpr int kRun = 8;              // consecutive items per thread: independent loads in flight
 constexpr int kHashSlots = 8192;     // smem hash of Adj(v) for dv <= 4096
 constexpr int kHashMaxDeg = kHashSlots / 2;
 constexpr int kTaskThreads = 256;
@@ -295,13 +294,17 @@ __global__ void __launch_bounds__(256) k_stars_block(const int32_t* __restrict__
 
 // ------------------------------------------------------------- triangles
 // W_t(v) = sum over triangles {v,i,j} of F(S-6) - F(S-4), S = dv+di+dj, and
-// t(v) = their number.  Every triangle at v is met exactly once as a probe
-// "j in Adj(v)?" for j in Adj+(i), i in Adj(v): the edge i-j lies in exactly
-// one of Adj+(i), Adj+(j).  A seed's probes form a flattened item space over
-// its rows x (row x = Adj+(A[x]), pc_x items); threads take runs of kRun
-// consecutive items, keep the current row in registers (no search per item)
-// and issue the run's loads before probing.  Membership is a shared-memory
-// hash of Adj(v) (load <= 1/4, linear probing) or, for hubs, a bitmap.
+// t(v) = their number.  Every triangle at v is found exactly once through the
+// row of its lower-ranked member i: j in Adj+(i) and j in Adj(v) (the edge
+// i-j lies in exactly one of Adj+(i), Adj+(j)).  Rows (i in Adj(v)) are long
+// -- at R-MAT22 96 % of all probes sit in rows of >= 64 entries -- so a warp
+// takes a whole row and its lanes stride it: the Adj+ loads are coalesced and
+// kUnroll of them are in flight per lane before the membership probes.
+// Membership: shared-memory hash of Adj(v) (load <= 1/4, linear probing) or,
+// for hubs, a bitmap over node ids.  Per-lane sums in a fixed assignment,
+// reduced in a fixed order (deterministic).
+
+constexpr int kUnroll = 4;
 
 // Open-addressing set of node ids in shared memory (SLOTS a power of two).
 template <int SLOTS>
@@ -328,45 +331,21 @@ struct BitmapSet {
   __device__ __forceinline__ bool contains(int32_t j) const { return (__ldg(bm + (j >> 5)) >> (j & 31)) & 1u; }
 };
 
-// Items [qbeg, qend) of a seed whose rows 0..X-1 have prefix pre[0..X]
-// (shared memory) and Adj+ starts sps[0..X).  With `ph` the last item of every
-// row is a placeholder (hub tasks, whose prefixes count pc+1).
+// One warp over entries [p0, p1) of row `row` (= Adj+(i), d_i = di).
 template <class Set>
-__device__ __forceinline__ void tri_runs(const FArgs& a, int64_t ob_rows, int64_t dv, const int32_t* pre,
-                                         const int32_t* sps, int X, int qbeg, int qend, int tid, int nthr,
-                                         const Set& set, bool ph, int64_t& tri, double& Wt) {
-  for (int q0 = qbeg + tid * kRun; q0 < qend; q0 += nthr * kRun) {
-    int k = 0, hi = X;  // last row with pre[k] <= q0
-    while (hi - k > 1) {
-      int mid = (k + hi) >> 1;
-      if (pre[mid] <= q0) k = mid; else hi = mid;
-    }
-    int row_end = pre[k + 1] - (ph ? 1 : 0);
-    int ptr = sps[k] + (q0 - pre[k]);
-    int32_t jv[kRun];
-    int kr[kRun];
+__device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restrict__ row, int32_t p0, int32_t p1,
+                                        int64_t base_s, int lane, const Set& set, int64_t& tri, double& Wt) {
+  for (int32_t p = p0 + lane; p < p1; p += 32 * kUnroll) {
+    int32_t j[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kRun; ++u) {
-      const int q = q0 + u;
-      jv[u] = -1;
-      if (q < qend) {
-        while (q >= row_end) {
-          if (ph && q < pre[k + 1]) break;  // placeholder item of row k
-          ++k;
-          row_end = pre[k + 1] - (ph ? 1 : 0);
-          ptr = sps[k];
-        }
-        if (q < row_end) {
-          jv[u] = __ldg(a.adjj + ptr);
-          ++ptr;
-        }
-        kr[u] = k;
-      }
-    }
+    for (int u = 0; u < kUnroll; ++u) j[u] = p + 32 * u < p1 ? __ldg(row + p + 32 * u) : -1;
+    bool hit[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kRun; ++u) {
-      if (jv[u] >= 0 && set.contains(jv[u])) {
-        const int64_t S = dv + __ldg(a.nd + ob_rows + kr[u]) + __ldg(a.deg + jv[u]);
+    for (int u = 0; u < kUnroll; ++u) hit[u] = j[u] >= 0 && set.contains(j[u]);
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (hit[u]) {
+        const int64_t S = base_s + __ldg(a.deg + j[u]);
         Wt += __ldg(a.F + S - 6) - __ldg(a.F + S - 4);
         ++tri;
       }
@@ -374,41 +353,37 @@ __device__ __forceinline__ void tri_runs(const FArgs& a, int64_t ob_rows, int64_
   }
 }
 
-// dv <= 32: warp per seed; per-warp 128-slot set and 33-entry row prefix.
+// Rows x = first, first+stride, ... < dv of seed v, one warp per row.
+template <class Set>
+__device__ __forceinline__ void tri_rows(const FArgs& a, int64_t ob, int dv, int first, int stride, int lane,
+                                         const Set& set, int64_t& tri, double& Wt) {
+  for (int x = first; x < dv; x += stride) {
+    const int64_t e = ob + x;
+    const int32_t pc = __ldg(a.pc + e);
+    if (pc == 0) continue;
+    tri_row(a, a.adjj + __ldg(a.ps + e), 0, pc, (int64_t)dv + __ldg(a.nd + e), lane, set, tri, Wt);
+  }
+}
+
+// dv <= 32: warp per seed (the warp walks the seed's rows one after another).
 constexpr int kTriWarps = 8;
 __global__ void __launch_bounds__(kTriWarps * 32)
 k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   __shared__ int32_t sT[kTriWarps][128];
-  __shared__ int32_t sPre[kTriWarps][33];
-  __shared__ int32_t sPs[kTriWarps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t q = (int64_t)blockIdx.x * kTriWarps + w;
-  if (q >= count) return;
-  const int32_t v = seeds[q];
+  const int64_t qs = (int64_t)blockIdx.x * kTriWarps + w;
+  if (qs >= count) return;
+  const int32_t v = seeds[qs];
   const int64_t ob = a.offsets[v];
   const int dv = (int)(a.offsets[v + 1] - ob);
   SmemSet<128> set{sT[w]};
   set.clear(lane, 32);
   __syncwarp();
-  int32_t cnt = 0;
-  if (lane < dv) {
-    set.insert(a.nbr[ob + lane]);
-    cnt = a.pc[ob + lane];
-    sPs[w][lane] = (int32_t)a.ps[ob + lane];
-  }
-  int32_t incl = cnt;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  sPre[w][lane + 1] = incl;
-  if (lane == 0) sPre[w][0] = 0;
-  const int32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  if (lane < dv) set.insert(a.nbr[ob + lane]);
   __syncwarp();
   int64_t tri = 0;
   double Wt = 0.0;
-  tri_runs(a, ob, dv, sPre[w], sPs[w], dv, 0, total, lane, 32, set, false, tri, Wt);
+  tri_rows(a, ob, dv, 0, 1, lane, set, tri, Wt);
   tri = warp_sum(tri);
   Wt = warp_sum(Wt);
   if (lane == 0) {
@@ -417,19 +392,14 @@ k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   }
 }
 
-// 32 < dv <= MAXD: CTA per seed, every row staged (prefix by block scan).
+// 32 < dv <= MAXD: CTA per seed, warps take rows round-robin.
 template <int THREADS, int MAXD>
 __global__ void __launch_bounds__(THREADS)
 k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   constexpr int SLOTS = 4 * MAXD;
-  extern __shared__ int32_t dyn[];
-  int32_t* table = dyn;                 // SLOTS
-  int32_t* pre = dyn + SLOTS;           // MAXD + 1
-  int32_t* sps = pre + MAXD + 1;        // MAXD
-  __shared__ int32_t wsum[THREADS / 32];
+  extern __shared__ int32_t table[];  // SLOTS
   __shared__ int64_t red_i[THREADS / 32];
   __shared__ double red_d[THREADS / 32];
-  constexpr int PER = (MAXD + THREADS - 1) / THREADS;
   const int64_t qs = blockIdx.x;
   if (qs >= count) return;
   const int32_t v = seeds[qs];
@@ -438,45 +408,11 @@ k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   SmemSet<SLOTS> set{table};
   set.clear(threadIdx.x, THREADS);
   __syncthreads();
-  // insert Adj(v); block exclusive scan of pc over the rows (PER rows per thread)
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  int32_t loc[PER];
-  int32_t sum = 0;
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int x = threadIdx.x * PER + u;
-    loc[u] = 0;
-    if (x < dv) {
-      set.insert(a.nbr[ob + x]);
-      loc[u] = a.pc[ob + x];
-      sps[x] = (int32_t)a.ps[ob + x];
-    }
-    sum += loc[u];
-  }
-  int32_t incl = sum;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) wsum[w] = incl;
-  __syncthreads();
-  int32_t wpre = 0;
-  for (int k = 0; k < w; ++k) wpre += wsum[k];
-  int32_t run = wpre + incl - sum;
-#pragma unroll
-  for (int u = 0; u < PER; ++u) {
-    const int x = threadIdx.x * PER + u;
-    if (x < dv) pre[x] = run;
-    run += loc[u];
-  }
-  int32_t total = 0;
-  for (int k = 0; k < THREADS / 32; ++k) total += wsum[k];
-  if (threadIdx.x == 0) pre[dv] = total;
+  for (int x = threadIdx.x; x < dv; x += THREADS) set.insert(a.nbr[ob + x]);
   __syncthreads();
   int64_t tri = 0;
   double Wt = 0.0;
-  tri_runs(a, ob, dv, pre, sps, dv, 0, total, threadIdx.x, THREADS, set, false, tri, Wt);
+  tri_rows(a, ob, dv, threadIdx.x >> 5, THREADS / 32, threadIdx.x & 31, set, tri, Wt);
   tri = block_sum<THREADS>(tri, red_i);
   Wt = block_sum<THREADS>(Wt, red_d);
   if (threadIdx.x == 0) {
@@ -485,9 +421,10 @@ k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   }
 }
 
-// Hubs (dv > kHashMaxDeg): tasks of kTask items (prefix tp counts pc+1 so a
-// task spans at most kTask+1 rows), one CTA each; membership from the hub's
-// bitmap over node ids (built once, L2-resident while its tasks run).
+// Hubs (dv > kHashMaxDeg): tasks of kTask items (prefix tp counts pc+1 per
+// row), one CTA each; warps take the task's rows, each restricted to the
+// task's item window; membership from the hub's bitmap over node ids (built
+// once per hub, L2-resident while its tasks run).
 struct TriTasks {
   const int32_t* seed;      // [ntasks]
   const int32_t* x0;        // [ntasks] first row position of the task
@@ -501,30 +438,31 @@ struct TriTasks {
 
 __global__ void __launch_bounds__(kTaskThreads)
 k_tri_task(FArgs a, TriTasks tk, int64_t ntasks) {
-  __shared__ int32_t stp[kTask + 2];
-  __shared__ int32_t sps[kTask + 1];
-  __shared__ int64_t red_i[kTaskThreads / 32];
-  __shared__ double red_d[kTaskThreads / 32];
+  constexpr int NW = kTaskThreads / 32;
+  __shared__ int64_t red_i[NW];
+  __shared__ double red_d[NW];
   const int64_t t = blockIdx.x;
   if (t >= ntasks) return;
   const int32_t v = tk.seed[t];
   const int64_t ob = a.offsets[v];
   const int dv = (int)(a.offsets[v + 1] - ob);
   const int64_t qa = (t - tk.first[t]) * (int64_t)kTask;
-  const int64_t work = a.tp[ob + dv - 1] + a.pc[ob + dv - 1] + 1;
-  const int64_t qb = qa + kTask < work ? qa + kTask : work;
+  const int64_t qb = qa + kTask;
   const int xa = tk.x0[t];
-  const int X = dv - xa < kTask + 1 ? dv - xa : kTask + 1;
-  for (int k = threadIdx.x; k <= X; k += kTaskThreads) {
-    const int64_t e = ob + xa + k;
-    stp[k] = (int32_t)((xa + k < dv ? a.tp[e] : work) - qa);
-    if (k < X) sps[k] = (int32_t)a.ps[e];
-  }
-  __syncthreads();
   BitmapSet set{tk.bitmaps + (int64_t)tk.hub_slot[v] * tk.words};
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t tri = 0;
   double Wt = 0.0;
-  tri_runs(a, ob + xa, dv, stp, sps, X, 0, (int)(qb - qa), threadIdx.x, kTaskThreads, set, true, tri, Wt);
+  // rows xa, xa+1, ... whose first item < qb (at most kTask + 1 rows)
+  for (int x = xa + w; x < dv && x <= xa + kTask; x += NW) {
+    const int64_t e = ob + x;
+    const int64_t r0 = a.tp[e];
+    if (r0 >= qb) break;
+    const int32_t pc = __ldg(a.pc + e);
+    const int32_t lo = (int32_t)(r0 > qa ? 0 : qa - r0);  // row items inside [qa, qb)
+    const int32_t hi = (int32_t)(r0 + pc < qb ? pc : qb - r0);
+    if (hi > lo) tri_row(a, a.adjj + __ldg(a.ps + e), lo, hi, (int64_t)dv + __ldg(a.nd + e), lane, set, tri, Wt);
+  }
   tri = block_sum<kTaskThreads>(tri, red_i);
   Wt = block_sum<kTaskThreads>(Wt, red_d);
   if (threadIdx.x == 0) {
@@ -801,12 +739,12 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     auto k_tri_seed_256 = k_tri_seed<128, 256>;
     auto k_tri_seed_1024 = k_tri_seed<256, 1024>;
     auto k_tri_seed_4096 = k_tri_seed<512, kHashMaxDeg>;
-    const int sm3 = 24 * kHashMaxDeg + 4;
+    const int sm3 = 16 * kHashMaxDeg;  // 4 * MAXD slots of int32
     EFG_CUDA_CHECK(cudaFuncSetAttribute(k_tri_seed_4096, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3));
     const int64_t n1 = select_seeds(ctx, r, DegRange{P.g.offsets, 32, 256}, list, "tri_1");
-    EFG_LAUNCH(k_tri_seed_256, n1, 128, 24 * 256 + 4, s, list, n1, a);
+    EFG_LAUNCH(k_tri_seed_256, n1, 128, 16 * 256, s, list, n1, a);
     const int64_t n2 = select_seeds(ctx, r, DegRange{P.g.offsets, 256, 1024}, list, "tri_2");
-    EFG_LAUNCH(k_tri_seed_1024, n2, 256, 24 * 1024 + 4, s, list, n2, a);
+    EFG_LAUNCH(k_tri_seed_1024, n2, 256, 16 * 1024, s, list, n2, a);
     const int64_t n3 = select_seeds(ctx, r, DegRange{P.g.offsets, 1024, kHashMaxDeg}, list, "tri_3");
     EFG_LAUNCH(k_tri_seed_4096, n3, 512, sm3, s, list, n3, a);
     int32_t* hubs = ctx.buf("f_hubs").as<int32_t>(cnt);

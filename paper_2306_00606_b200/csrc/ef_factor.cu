@@ -45,6 +45,7 @@ struct FArgs {
   const int32_t* nd;       // degree of each adjacency entry
   const int64_t* s1;
   const double* F;
+  const double* G;         // G[S] = F(S-6) - F(S-4): triangle correction per unit weight
   const int64_t* ps;       // [2m] start of Adj+(nbr[e]) in adjp
   const int32_t* pc;       // [2m] |Adj+(nbr[e])|
   const int64_t* tp;       // [2m] row prefix of (pc + 1): flattened triangle items
@@ -306,47 +307,56 @@ __global__ void __launch_bounds__(256) k_stars_block(const int32_t* __restrict__
 
 constexpr int kUnroll = 4;
 
-// Open-addressing set of node ids in shared memory (SLOTS a power of two).
+// Open-addressing map node id -> degree in shared memory (SLOTS a power of
+// two, int2 entries): a hit returns d_j from the same 8-byte load, so the
+// triangle term needs no dependent global gather.  Lookup returns -1 on miss.
 template <int SLOTS>
-struct SmemSet {
-  int32_t* t;
+struct SmemMap {
+  int2* t;
   static constexpr int kShift = 32 - __builtin_ctz(SLOTS);
   __device__ __forceinline__ void clear(int tid, int nthr) {
-    for (int s = tid; s < SLOTS; s += nthr) t[s] = -1;
+    for (int s = tid; s < SLOTS; s += nthr) t[s] = make_int2(-1, 0);
   }
-  __device__ __forceinline__ void insert(int32_t key) {
+  __device__ __forceinline__ void insert(int32_t key, int32_t deg) {
     uint32_t s = ((uint32_t)key * 2654435761u) >> kShift;
-    while (atomicCAS(&t[s], -1, key) != -1) s = (s + 1) & (SLOTS - 1);
+    while (atomicCAS(&t[s].x, -1, key) != -1) s = (s + 1) & (SLOTS - 1);
+    t[s].y = deg;
   }
-  __device__ __forceinline__ bool contains(int32_t key) const {
+  __device__ __forceinline__ int32_t degree(int32_t key) const {
     uint32_t s = ((uint32_t)key * 2654435761u) >> kShift;
-    int32_t k;
-    while ((k = t[s]) != key && k != -1) s = (s + 1) & (SLOTS - 1);
-    return k == key;
+    int2 k = t[s];
+    while (k.x != key && k.x != -1) {
+      s = (s + 1) & (SLOTS - 1);
+      k = t[s];
+    }
+    return k.x == key ? k.y : -1;
   }
 };
 
-struct BitmapSet {
+// Hubs: membership from a bitmap over node ids, d_j from the degree array.
+struct BitmapMap {
   const uint32_t* bm;
-  __device__ __forceinline__ bool contains(int32_t j) const { return (__ldg(bm + (j >> 5)) >> (j & 31)) & 1u; }
+  const int32_t* deg;
+  __device__ __forceinline__ int32_t degree(int32_t j) const {
+    return ((__ldg(bm + (j >> 5)) >> (j & 31)) & 1u) ? __ldg(deg + j) : -1;
+  }
 };
 
-// One warp over entries [p0, p1) of row `row` (= Adj+(i), d_i = di).
-template <class Set>
+// One warp over entries [p0, p1) of row `row` (= Adj+(i), s0 = dv + di).
+template <class Map>
 __device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restrict__ row, int32_t p0, int32_t p1,
-                                        int64_t base_s, int lane, const Set& set, int64_t& tri, double& Wt) {
+                                        int32_t s0, int lane, const Map& map, int64_t& tri, double& Wt) {
   for (int32_t p = p0 + lane; p < p1; p += 32 * kUnroll) {
     int32_t j[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) j[u] = p + 32 * u < p1 ? __ldg(row + p + 32 * u) : -1;
-    bool hit[kUnroll];
+    int32_t dj[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) hit[u] = j[u] >= 0 && set.contains(j[u]);
+    for (int u = 0; u < kUnroll; ++u) dj[u] = j[u] >= 0 ? map.degree(j[u]) : -1;
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
-      if (hit[u]) {
-        const int64_t S = base_s + __ldg(a.deg + j[u]);
-        Wt += __ldg(a.F + S - 6) - __ldg(a.F + S - 4);
+      if (dj[u] >= 0) {
+        Wt += __ldg(a.G + s0 + dj[u]);
         ++tri;
       }
     }
@@ -354,14 +364,14 @@ __device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restric
 }
 
 // Rows x = first, first+stride, ... < dv of seed v, one warp per row.
-template <class Set>
+template <class Map>
 __device__ __forceinline__ void tri_rows(const FArgs& a, int64_t ob, int dv, int first, int stride, int lane,
-                                         const Set& set, int64_t& tri, double& Wt) {
+                                         const Map& map, int64_t& tri, double& Wt) {
   for (int x = first; x < dv; x += stride) {
     const int64_t e = ob + x;
     const int32_t pc = __ldg(a.pc + e);
     if (pc == 0) continue;
-    tri_row(a, a.adjj + __ldg(a.ps + e), 0, pc, (int64_t)dv + __ldg(a.nd + e), lane, set, tri, Wt);
+    tri_row(a, a.adjj + __ldg(a.ps + e), 0, pc, dv + __ldg(a.nd + e), lane, map, tri, Wt);
   }
 }
 
@@ -369,21 +379,21 @@ __device__ __forceinline__ void tri_rows(const FArgs& a, int64_t ob, int dv, int
 constexpr int kTriWarps = 8;
 __global__ void __launch_bounds__(kTriWarps * 32)
 k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
-  __shared__ int32_t sT[kTriWarps][128];
+  __shared__ int2 sT[kTriWarps][128];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t qs = (int64_t)blockIdx.x * kTriWarps + w;
   if (qs >= count) return;
   const int32_t v = seeds[qs];
   const int64_t ob = a.offsets[v];
   const int dv = (int)(a.offsets[v + 1] - ob);
-  SmemSet<128> set{sT[w]};
-  set.clear(lane, 32);
+  SmemMap<128> map{sT[w]};
+  map.clear(lane, 32);
   __syncwarp();
-  if (lane < dv) set.insert(a.nbr[ob + lane]);
+  if (lane < dv) map.insert(a.nbr[ob + lane], a.nd[ob + lane]);
   __syncwarp();
   int64_t tri = 0;
   double Wt = 0.0;
-  tri_rows(a, ob, dv, 0, 1, lane, set, tri, Wt);
+  tri_rows(a, ob, dv, 0, 1, lane, map, tri, Wt);
   tri = warp_sum(tri);
   Wt = warp_sum(Wt);
   if (lane == 0) {
@@ -393,11 +403,11 @@ k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
 }
 
 // 32 < dv <= MAXD: CTA per seed, warps take rows round-robin.
-template <int THREADS, int MAXD>
+template <int THREADS, int MAXD, int LOADINV>
 __global__ void __launch_bounds__(THREADS)
 k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
-  constexpr int SLOTS = 4 * MAXD;
-  extern __shared__ int32_t table[];  // SLOTS
+  constexpr int SLOTS = LOADINV * MAXD;
+  extern __shared__ int2 table[];  // SLOTS
   __shared__ int64_t red_i[THREADS / 32];
   __shared__ double red_d[THREADS / 32];
   const int64_t qs = blockIdx.x;
@@ -405,14 +415,14 @@ k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   const int32_t v = seeds[qs];
   const int64_t ob = a.offsets[v];
   const int dv = (int)(a.offsets[v + 1] - ob);
-  SmemSet<SLOTS> set{table};
-  set.clear(threadIdx.x, THREADS);
+  SmemMap<SLOTS> map{table};
+  map.clear(threadIdx.x, THREADS);
   __syncthreads();
-  for (int x = threadIdx.x; x < dv; x += THREADS) set.insert(a.nbr[ob + x]);
+  for (int x = threadIdx.x; x < dv; x += THREADS) map.insert(a.nbr[ob + x], a.nd[ob + x]);
   __syncthreads();
   int64_t tri = 0;
   double Wt = 0.0;
-  tri_rows(a, ob, dv, threadIdx.x >> 5, THREADS / 32, threadIdx.x & 31, set, tri, Wt);
+  tri_rows(a, ob, dv, threadIdx.x >> 5, THREADS / 32, threadIdx.x & 31, map, tri, Wt);
   tri = block_sum<THREADS>(tri, red_i);
   Wt = block_sum<THREADS>(Wt, red_d);
   if (threadIdx.x == 0) {
@@ -449,7 +459,7 @@ k_tri_task(FArgs a, TriTasks tk, int64_t ntasks) {
   const int64_t qa = (t - tk.first[t]) * (int64_t)kTask;
   const int64_t qb = qa + kTask;
   const int xa = tk.x0[t];
-  BitmapSet set{tk.bitmaps + (int64_t)tk.hub_slot[v] * tk.words};
+  BitmapMap map{tk.bitmaps + (int64_t)tk.hub_slot[v] * tk.words, a.deg};
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   int64_t tri = 0;
   double Wt = 0.0;
@@ -461,7 +471,7 @@ k_tri_task(FArgs a, TriTasks tk, int64_t ntasks) {
     const int32_t pc = __ldg(a.pc + e);
     const int32_t lo = (int32_t)(r0 > qa ? 0 : qa - r0);  // row items inside [qa, qb)
     const int32_t hi = (int32_t)(r0 + pc < qb ? pc : qb - r0);
-    if (hi > lo) tri_row(a, a.adjj + __ldg(a.ps + e), lo, hi, (int64_t)dv + __ldg(a.nd + e), lane, set, tri, Wt);
+    if (hi > lo) tri_row(a, a.adjj + __ldg(a.ps + e), lo, hi, dv + __ldg(a.nd + e), lane, map, tri, Wt);
   }
   tri = block_sum<kTaskThreads>(tri, red_i);
   Wt = block_sum<kTaskThreads>(Wt, red_d);
@@ -693,6 +703,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   a.nd = P.nd;
   a.s1 = P.s1;
   a.F = P.ftab;
+  a.G = P.gtab;
   a.ps = P.ps;
   a.pc = P.pc;
   a.tp = nullptr;
@@ -736,15 +747,15 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     int32_t* list = ctx.buf("f_list_tri").as<int32_t>(cnt);
     const int64_t nsm = select_seeds(ctx, r, DegRange{P.g.offsets, -1, 32}, list, "tri_s");
     EFG_LAUNCH(k_tri_warp, ceil_div(nsm, kTriWarps), kTriWarps * 32, 0, s, list, nsm, a);
-    auto k_tri_seed_256 = k_tri_seed<128, 256>;
-    auto k_tri_seed_1024 = k_tri_seed<256, 1024>;
-    auto k_tri_seed_4096 = k_tri_seed<512, kHashMaxDeg>;
-    const int sm3 = 16 * kHashMaxDeg;  // 4 * MAXD slots of int32
+    auto k_tri_seed_256 = k_tri_seed<128, 256, 4>;
+    auto k_tri_seed_1024 = k_tri_seed<256, 1024, 4>;
+    auto k_tri_seed_4096 = k_tri_seed<512, kHashMaxDeg, 2>;
+    const int sm3 = 16 * kHashMaxDeg;  // 2 * MAXD int2 slots
     EFG_CUDA_CHECK(cudaFuncSetAttribute(k_tri_seed_4096, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3));
     const int64_t n1 = select_seeds(ctx, r, DegRange{P.g.offsets, 32, 256}, list, "tri_1");
-    EFG_LAUNCH(k_tri_seed_256, n1, 128, 16 * 256, s, list, n1, a);
+    EFG_LAUNCH(k_tri_seed_256, n1, 128, 32 * 256, s, list, n1, a);
     const int64_t n2 = select_seeds(ctx, r, DegRange{P.g.offsets, 256, 1024}, list, "tri_2");
-    EFG_LAUNCH(k_tri_seed_1024, n2, 256, 16 * 1024, s, list, n2, a);
+    EFG_LAUNCH(k_tri_seed_1024, n2, 256, 32 * 1024, s, list, n2, a);
     const int64_t n3 = select_seeds(ctx, r, DegRange{P.g.offsets, 1024, kHashMaxDeg}, list, "tri_3");
     EFG_LAUNCH(k_tri_seed_4096, n3, 512, sm3, s, list, n3, a);
     int32_t* hubs = ctx.buf("f_hubs").as<int32_t>(cnt);

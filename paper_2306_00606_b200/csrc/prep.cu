@@ -28,6 +28,12 @@ __global__ void k_ftab(double* __restrict__ F, int64_t len) {
   if (d < len) F[d] = d > 0 ? (double)d * log((double)d) : 0.0;
 }
 
+// G[S] = F(S-6) - F(S-4): the W change of one triangle cluster unit (S = dv+di+dj >= 6).
+__global__ void k_gtab(const double* __restrict__ F, double* __restrict__ G, int64_t len) {
+  int64_t S = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (S < len) G[S] = S >= 6 ? F[S - 6] - F[S - 4] : 0.0;
+}
+
 __global__ void k_nd(const int32_t* __restrict__ nbr, int64_t m2, const int32_t* __restrict__ deg,
                      int32_t* __restrict__ nd) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -134,6 +140,8 @@ void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P)
   P.ftab_len = 3 * (int64_t)(dmax > 1 ? dmax : 1) + 8;
   P.ftab = ctx.buf("ftab").as<double>(P.ftab_len);
   EFG_LAUNCH(k_ftab, ceil_div(P.ftab_len, B), B, 0, s, P.ftab, P.ftab_len);
+  P.gtab = ctx.buf("gtab").as<double>(P.ftab_len);
+  EFG_LAUNCH(k_gtab, ceil_div(P.ftab_len, B), B, 0, s, P.ftab, P.gtab, P.ftab_len);
   EFG_LAUNCH(k_nd, ceil_div(m2, B), B, 0, s, g.nbr, m2, P.deg, P.nd);
   int64_t* dplus64 = ctx.buf("dplus64").as<int64_t>(n + 1);
   EFG_LAUNCH(k_row_sums, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.s1, dplus64);

@@ -176,14 +176,41 @@ def context(device: int | None = None) -> Context:
         return c
 
 
+# Recycled page-locked blocks: cudaHostAlloc costs ~1 ms per 10 MB, so the
+# blocks behind released arrays are kept (per size, bounded) and reused.
+_pool: dict[int, list[int]] = {}
+_pool_bytes = 0
+_POOL_LIMIT = 8 << 30
+_pool_lock = threading.Lock()
+
+
+def _release(addr: int, nbytes: int) -> None:
+    global _pool_bytes
+    with _pool_lock:
+        if _pool_bytes + nbytes <= _POOL_LIMIT:
+            _pool.setdefault(nbytes, []).append(addr)
+            _pool_bytes += nbytes
+            return
+    lib().efg_host_free(ctypes.c_void_p(addr))
+
+
 def pinned_empty(shape, dtype) -> np.ndarray:
-    """numpy array backed by page-locked host memory (freed with the array)."""
+    """numpy array backed by page-locked host memory (block recycled when the array dies)."""
+    global _pool_bytes
     dtype = np.dtype(dtype)
     count = int(np.prod(shape)) if np.ndim(shape) else int(shape)
-    nbytes = max(1, count * dtype.itemsize)
-    raw = ctypes.c_void_p()
-    check(lib().efg_host_alloc(nbytes, ctypes.byref(raw)))
-    buf = (ctypes.c_char * nbytes).from_address(raw.value)
+    nbytes = max(64, (count * dtype.itemsize + 63) & ~63)
+    addr = None
+    with _pool_lock:
+        free = _pool.get(nbytes)
+        if free:
+            addr = free.pop()
+            _pool_bytes -= nbytes
+    if addr is None:
+        raw = ctypes.c_void_p()
+        check(lib().efg_host_alloc(nbytes, ctypes.byref(raw)))
+        addr = raw.value
+    buf = (ctypes.c_char * nbytes).from_address(addr)
     arr = np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
-    weakref.finalize(buf, lib().efg_host_free, raw)
+    weakref.finalize(buf, _release, addr, nbytes)
     return arr

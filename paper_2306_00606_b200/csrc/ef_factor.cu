@@ -307,29 +307,44 @@ __global__ void __launch_bounds__(256) k_stars_block(const int32_t* __restrict__
 
 constexpr int kUnroll = 4;
 
-// Open-addressing map node id -> degree in shared memory (SLOTS a power of
-// two, int2 entries): a hit returns d_j from the same 8-byte load, so the
-// triangle term needs no dependent global gather.  Lookup returns -1 on miss.
-template <int SLOTS>
+// Bucketised hash map node id -> degree in shared memory: NB buckets of 4
+// keys (one 16-byte load per probe, no per-lane probe loop in the common
+// case), filled slot 0..3 in order, linear probing over buckets only when a
+// bucket is full (rare at load <= 1/4).  With WITH_DEG the matching degree
+// comes from a parallel array, otherwise from the global degree array.
+template <int NB, bool WITH_DEG>
 struct SmemMap {
-  int2* t;
-  static constexpr int kShift = 32 - __builtin_ctz(SLOTS);
+  int4* keys;           // NB
+  int32_t* degs;        // 4 * NB (WITH_DEG)
+  const int32_t* gdeg;  // global degrees (!WITH_DEG)
+  __device__ __forceinline__ static uint32_t bucket(int32_t key) {
+    return ((uint32_t)key * 2654435761u) >> (32 - __builtin_ctz(NB));
+  }
   __device__ __forceinline__ void clear(int tid, int nthr) {
-    for (int s = tid; s < SLOTS; s += nthr) t[s] = make_int2(-1, 0);
+    for (int s = tid; s < NB; s += nthr) keys[s] = make_int4(-1, -1, -1, -1);
   }
   __device__ __forceinline__ void insert(int32_t key, int32_t deg) {
-    uint32_t s = ((uint32_t)key * 2654435761u) >> kShift;
-    while (atomicCAS(&t[s].x, -1, key) != -1) s = (s + 1) & (SLOTS - 1);
-    t[s].y = deg;
+    int32_t* flat = reinterpret_cast<int32_t*>(keys);
+    for (uint32_t b = bucket(key);; b = (b + 1) & (NB - 1)) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        if (atomicCAS(&flat[4 * b + k], -1, key) == -1) {
+          if (WITH_DEG) degs[4 * b + k] = deg;
+          return;
+        }
+      }
+    }
   }
   __device__ __forceinline__ int32_t degree(int32_t key) const {
-    uint32_t s = ((uint32_t)key * 2654435761u) >> kShift;
-    int2 k = t[s];
-    while (k.x != key && k.x != -1) {
-      s = (s + 1) & (SLOTS - 1);
-      k = t[s];
+    uint32_t b = bucket(key);
+    int4 q = keys[b];
+    while (true) {
+      const int k = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
+      if (k >= 0) return WITH_DEG ? degs[4 * b + k] : __ldg(gdeg + key);
+      if (q.w == -1) return -1;  // bucket not full: key absent
+      b = (b + 1) & (NB - 1);
+      q = keys[b];
     }
-    return k.x == key ? k.y : -1;
   }
 };
 
@@ -379,14 +394,15 @@ __device__ __forceinline__ void tri_rows(const FArgs& a, int64_t ob, int dv, int
 constexpr int kTriWarps = 8;
 __global__ void __launch_bounds__(kTriWarps * 32)
 k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
-  __shared__ int2 sT[kTriWarps][128];
+  __shared__ int4 sK[kTriWarps][32];
+  __shared__ int32_t sD[kTriWarps][128];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t qs = (int64_t)blockIdx.x * kTriWarps + w;
   if (qs >= count) return;
   const int32_t v = seeds[qs];
   const int64_t ob = a.offsets[v];
   const int dv = (int)(a.offsets[v + 1] - ob);
-  SmemMap<128> map{sT[w]};
+  SmemMap<32, true> map{sK[w], sD[w], nullptr};
   map.clear(lane, 32);
   __syncwarp();
   if (lane < dv) map.insert(a.nbr[ob + lane], a.nd[ob + lane]);
@@ -403,11 +419,11 @@ k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
 }
 
 // 32 < dv <= MAXD: CTA per seed, warps take rows round-robin.
-template <int THREADS, int MAXD, int LOADINV>
+// smem: 16 * NB (+ 16 * NB with degrees) bytes
+template <int THREADS, int NB, bool WITH_DEG>
 __global__ void __launch_bounds__(THREADS)
 k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
-  constexpr int SLOTS = LOADINV * MAXD;
-  extern __shared__ int2 table[];  // SLOTS
+  extern __shared__ int4 dyn4[];
   __shared__ int64_t red_i[THREADS / 32];
   __shared__ double red_d[THREADS / 32];
   const int64_t qs = blockIdx.x;
@@ -415,7 +431,7 @@ k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   const int32_t v = seeds[qs];
   const int64_t ob = a.offsets[v];
   const int dv = (int)(a.offsets[v + 1] - ob);
-  SmemMap<SLOTS> map{table};
+  SmemMap<NB, WITH_DEG> map{dyn4, reinterpret_cast<int32_t*>(dyn4 + NB), a.deg};
   map.clear(threadIdx.x, THREADS);
   __syncthreads();
   for (int x = threadIdx.x; x < dv; x += THREADS) map.insert(a.nbr[ob + x], a.nd[ob + x]);
@@ -483,11 +499,11 @@ k_tri_task(FArgs a, TriTasks tk, int64_t ntasks) {
 
 // Per-row exclusive prefix of (pc + 1) -> tp, and the seed's task count (warp per row).
 __global__ void k_tri_prefix(const int64_t* __restrict__ offsets, const int32_t* __restrict__ pc,
-                             const int32_t* __restrict__ seeds, int64_t count, int64_t* __restrict__ tp,
-                             int64_t* __restrict__ ntask) {
+                             const int32_t* __restrict__ seeds, const int64_t* __restrict__ count_dev,
+                             int64_t* __restrict__ tp, int64_t* __restrict__ ntask) {
   const int lane = threadIdx.x & 31;
   int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (q >= count) return;
+  if (q >= *count_dev) return;
   const int32_t v = seeds[q];
   const int64_t b = offsets[v], e = offsets[v + 1];
   int64_t carry = 0;
@@ -597,20 +613,22 @@ struct HistRange {
   }
 };
 
+// Seeds of r satisfying pred -> out (ascending); the count lands in *count_dev
+// (device memory, read back with all other counts in one synchronisation).
 template <class Pred>
-int64_t select_seeds(Context& ctx, SeedRange r, Pred pred, int32_t* out, const char* tag) {
+void select_seeds(Context& ctx, SeedRange r, Pred pred, int32_t* out, int64_t* count_dev) {
   cudaStream_t s = ctx.stream;
   size_t tmp = 0;
-  int64_t* nsel_d = ctx.buf(std::string("sel_") + tag).as<int64_t>(1);
   cub::CountingInputIterator<int32_t> it((int32_t)r.lo);
   const int64_t cnt = r.hi - r.lo;
-  EFG_CUDA_CHECK(cub::DeviceSelect::If(nullptr, tmp, it, out, nsel_d, cnt, pred, s));
+  EFG_CUDA_CHECK(cub::DeviceSelect::If(nullptr, tmp, it, out, count_dev, cnt, pred, s));
   EFG_REGION("cub::DeviceSelect::If", s,
-             EFG_CUDA_CHECK(cub::DeviceSelect::If(ctx.buf("cub").get(tmp), tmp, it, out, nsel_d, cnt, pred, s)));
-  int64_t nsel = 0;
-  EFG_CUDA_CHECK(cudaMemcpyAsync(&nsel, nsel_d, sizeof nsel, cudaMemcpyDeviceToHost, s));
-  EFG_CUDA_CHECK(cudaStreamSynchronize(s));
-  return nsel;
+             EFG_CUDA_CHECK(cub::DeviceSelect::If(ctx.buf("cub").get(tmp), tmp, it, out, count_dev, cnt, pred, s)));
+}
+
+__global__ void k_gather_count(const int64_t* __restrict__ arr, const int64_t* __restrict__ idx,
+                               int64_t* __restrict__ out) {
+  *out = arr[*idx];
 }
 
 __global__ void k_seed_work(const int64_t* __restrict__ offsets, const int32_t* __restrict__ pcv,
@@ -632,8 +650,10 @@ __global__ void k_seed_work(const int64_t* __restrict__ offsets, const int32_t* 
 
 // Neighbour-degree histograms H_i for every node (sorted distinct degrees +
 // counts).  Returns the number of entries.
-static int64_t build_histograms(Context& ctx, Prepared& P, int64_t*& hoff, int32_t*& hkey, int32_t*& hcnt,
-                                int64_t* maxD = nullptr) {
+// Neighbour-degree histograms H_i for every node: sorted distinct degrees
+// (hkey) with counts (hcnt), row offsets hoff.  Asynchronous: hkey/hcnt are
+// sized by the bound sum |D_i| <= 2m, the exact total stays on the device.
+static void build_histograms(Context& ctx, Prepared& P, int64_t*& hoff, int32_t*& hkey, int32_t*& hcnt) {
   cudaStream_t s = ctx.stream;
   const int64_t n = P.g.n, m2 = P.g.m2;
   const int B = 256;
@@ -652,20 +672,9 @@ static int64_t build_histograms(Context& ctx, Prepared& P, int64_t*& hoff, int32
   EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, dcnt, hoff, n + 1, s));
   EFG_REGION("cub::DeviceScan::ExclusiveSum", s,
              EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dcnt, hoff, n + 1, s)));
-  if (maxD) {
-    int64_t* dmx = ctx.buf("f_maxD").as<int64_t>(1);
-    EFG_CUDA_CHECK(cub::DeviceReduce::Max(nullptr, tmp, dcnt, dmx, n, s));
-    EFG_REGION("cub::DeviceReduce::Max", s,
-               EFG_CUDA_CHECK(cub::DeviceReduce::Max(ctx.buf("cub").get(tmp), tmp, dcnt, dmx, n, s)));
-    EFG_CUDA_CHECK(cudaMemcpyAsync(maxD, dmx, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-  }
-  int64_t nh = 0;
-  EFG_CUDA_CHECK(cudaMemcpyAsync(&nh, hoff + n, sizeof nh, cudaMemcpyDeviceToHost, s));
-  EFG_CUDA_CHECK(cudaStreamSynchronize(s));
-  hkey = ctx.buf("f_hkey").as<int32_t>(nh);
-  hcnt = ctx.buf("f_hcnt").as<int32_t>(nh);
+  hkey = ctx.buf("f_hkey").as<int32_t>(m2 > 0 ? m2 : 1);
+  hcnt = ctx.buf("f_hcnt").as<int32_t>(m2 > 0 ? m2 : 1);
   EFG_LAUNCH(k_rle_fill, ceil_div(n * 32, B), B, 0, s, P.g.offsets, snd, n, hoff, hkey, hcnt);
-  return nh;
 }
 
 void factorized_work(Context& ctx, Prepared& P, int64_t* d_work) {
@@ -675,6 +684,11 @@ void factorized_work(Context& ctx, Prepared& P, int64_t* d_work) {
   const int B = 256;
   EFG_LAUNCH(k_seed_work, ceil_div(P.g.n * 32, B), B, 0, ctx.stream, P.g.offsets, P.pc, hoff, P.g.n, d_work);
 }
+
+// The pass has exactly one host synchronisation after prepare(): every
+// class list and task count is produced on the device first, read back in a
+// single copy, and the compute kernels are then launched back to back.
+enum Slot { kBigRow, kChainS, kChainB, kStarS, kStarB, kTriS, kTri1, kTri2, kTri3, kHubs, kNTasks, kMaxD, kNSlots };
 
 void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* total, uint8_t* flags,
                    int64_t* T_out, double* W_out, efg_stats* st) {
@@ -686,17 +700,55 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   if (cnt <= 0) return;
   int64_t* hoff;
   int32_t *hkey, *hcnt;
-  int64_t maxD = 0;
-  const int64_t nh = build_histograms(ctx, P, hoff, hkey, hcnt, &maxD);
-  // 1. chain tables C_i(y): rows with <= 64 distinct degrees by 8-lane groups, the rest by CTAs
-  double* ctab = ctx.buf("f_ctab").as<double>(nh);
+  build_histograms(ctx, P, hoff, hkey, hcnt);
+  // ---- phase 1: class lists and counts on the device
+  int64_t* cdev = ctx.buf("f_counts").as<int64_t>(kNSlots);
+  const int64_t kBig = 64;
+  auto list = [&](const char* name, int64_t len) { return ctx.buf(name).as<int32_t>(len > 0 ? len : 1); };
+  int32_t* l_big = list("f_l_big", n);
+  int32_t* l_chs = list("f_l_chs", cnt);
+  int32_t* l_chb = list("f_l_chb", cnt);
+  int32_t* l_sts = list("f_l_sts", cnt);
+  int32_t* l_stb = list("f_l_stb", cnt);
+  int32_t* l_trs = list("f_l_trs", cnt);
+  int32_t* l_tr1 = list("f_l_tr1", cnt);
+  int32_t* l_tr2 = list("f_l_tr2", cnt);
+  int32_t* l_tr3 = list("f_l_tr3", cnt);
+  int32_t* l_hub = list("f_l_hub", cnt);
+  select_seeds(ctx, SeedRange{0, n}, BigRow{hoff, kBig}, l_big, cdev + kBigRow);
+  select_seeds(ctx, r, DegRange{P.g.offsets, -1, 1024}, l_chs, cdev + kChainS);
+  select_seeds(ctx, r, DegRange{P.g.offsets, 1024, INT64_MAX}, l_chb, cdev + kChainB);
+  select_seeds(ctx, r, HistRange{hoff, -1, 32}, l_sts, cdev + kStarS);
+  select_seeds(ctx, r, HistRange{hoff, 32, INT64_MAX}, l_stb, cdev + kStarB);
+  select_seeds(ctx, r, DegRange{P.g.offsets, -1, 32}, l_trs, cdev + kTriS);
+  select_seeds(ctx, r, DegRange{P.g.offsets, 32, 256}, l_tr1, cdev + kTri1);
+  select_seeds(ctx, r, DegRange{P.g.offsets, 256, 1024}, l_tr2, cdev + kTri2);
+  select_seeds(ctx, r, DegRange{P.g.offsets, 1024, kHashMaxDeg}, l_tr3, cdev + kTri3);
+  select_seeds(ctx, r, DegRange{P.g.offsets, kHashMaxDeg, INT64_MAX}, l_hub, cdev + kHubs);
   {
-    const int64_t kBig = 64;
-    int32_t* rows = ctx.buf("f_rows").as<int32_t>(n);
-    EFG_LAUNCH(k_ctab_group<8>, ceil_div(n * 8, B), B, 0, s, hoff, hkey, hcnt, P.deg, P.ftab, n, kBig, ctab);
-    const int64_t nrows = select_seeds(ctx, SeedRange{0, n}, BigRow{hoff, kBig}, rows, "bigrow");
-    EFG_LAUNCH(k_ctab_block, nrows, 128, 0, s, rows, nrows, hoff, hkey, hcnt, P.deg, P.ftab, ctab);
+    int64_t* dcnt = ctx.buf("f_dcnt").as<int64_t>(n + 1);  // per-node |D_i| (from build_histograms)
+    EFG_CUDA_CHECK(cub::DeviceReduce::Max(nullptr, tmp, dcnt, cdev + kMaxD, n, s));
+    EFG_REGION("cub::DeviceReduce::Max", s,
+               EFG_CUDA_CHECK(cub::DeviceReduce::Max(ctx.buf("cub").get(tmp), tmp, dcnt, cdev + kMaxD, n, s)));
   }
+  // hub tasks: items of a hub = sum over its rows of (|Adj+| + 1), cut every kTask
+  int64_t* tp = ctx.buf("f_tp").as<int64_t>(P.g.m2 > 0 ? P.g.m2 : 1);
+  int64_t* ntask = ctx.buf("f_ntask").as<int64_t>(cnt + 1);
+  int64_t* tstart = ctx.buf("f_tstart").as<int64_t>(cnt + 1);
+  EFG_CUDA_CHECK(cudaMemsetAsync(ntask, 0, (cnt + 1) * sizeof(int64_t), s));
+  EFG_LAUNCH(k_tri_prefix, ceil_div(cnt * 32, B), B, 0, s, P.g.offsets, P.pc, l_hub, cdev + kHubs, tp, ntask);
+  EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ntask, tstart, cnt + 1, s));
+  EFG_REGION("cub::DeviceScan::ExclusiveSum", s,
+             EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, ntask, tstart, cnt + 1, s)));
+  EFG_LAUNCH(k_gather_count, 1, 1, 0, s, tstart, cdev + kHubs, cdev + kNTasks);
+  int64_t c[kNSlots];
+  EFG_CUDA_CHECK(cudaMemcpyAsync(c, cdev, sizeof c, cudaMemcpyDeviceToHost, s));
+  EFG_CUDA_CHECK(cudaStreamSynchronize(s));
+  // ---- phase 2: compute kernels, no further host synchronisation
+  // 1. chain tables C_i(y): rows with <= 64 distinct degrees by 8-lane groups, the rest by CTAs
+  double* ctab = ctx.buf("f_ctab").as<double>(P.g.m2 > 0 ? P.g.m2 : 1);
+  EFG_LAUNCH(k_ctab_group<8>, ceil_div(n * 8, B), B, 0, s, hoff, hkey, hcnt, P.deg, P.ftab, n, kBig, ctab);
+  EFG_LAUNCH(k_ctab_block, c[kBigRow], 128, 0, s, l_big, c[kBigRow], hoff, hkey, hcnt, P.deg, P.ftab, ctab);
   FArgs a;
   a.offsets = P.g.offsets;
   a.nbr = P.g.nbr;
@@ -706,7 +758,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   a.G = P.gtab;
   a.ps = P.ps;
   a.pc = P.pc;
-  a.tp = nullptr;
+  a.tp = tp;
   a.adjj = P.adjj;
   a.deg = P.deg;
   a.hoff = hoff;
@@ -719,83 +771,56 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   a.Ws = ctx.buf("f_Ws").as<double>(cnt);
   a.tri = ctx.buf("f_tri").as<int64_t>(cnt);
   a.Wt = ctx.buf("f_Wt").as<double>(cnt);
-  // 2. chains: warp per row (dv <= 1024), CTA per row above
-  {
-    int32_t* list = ctx.buf("f_list_chain").as<int32_t>(cnt);
-    const int64_t nsmall = select_seeds(ctx, r, DegRange{P.g.offsets, -1, 1024}, list, "chain_s");
-    EFG_LAUNCH(k_chain_warp, ceil_div(nsmall * 32, B), B, 0, s, list, nsmall, a);
-    const int64_t nbig = select_seeds(ctx, r, DegRange{P.g.offsets, 1024, INT64_MAX}, list, "chain_b");
-    EFG_LAUNCH(k_chain_block, nbig, 256, 0, s, list, nbig, a);
+  // 2. triangles (the long kernels first)
+  const int64_t nhubs = c[kHubs], ntasks = c[kNTasks];
+  if (nhubs) {
+    int32_t* tseed = ctx.buf("f_tseed").as<int32_t>(ntasks);
+    int32_t* tx0 = ctx.buf("f_tx0").as<int32_t>(ntasks);
+    int64_t* tfirst = ctx.buf("f_tfirst").as<int64_t>(ntasks);
+    EFG_LAUNCH(k_tri_fill, ceil_div(nhubs * 32, B), B, 0, s, P.g.offsets, l_hub, nhubs, tp, P.pc, tstart, tseed, tx0,
+               tfirst);
+    TriTasks tk;
+    tk.seed = tseed;
+    tk.x0 = tx0;
+    tk.first = tfirst;
+    tk.words = ceil_div(n, 32);
+    uint32_t* bms = ctx.buf("f_bitmaps").as<uint32_t>(nhubs * tk.words);
+    int32_t* hub_slot = ctx.buf("f_hub_slot").as<int32_t>(n);
+    EFG_CUDA_CHECK(cudaMemsetAsync(bms, 0, nhubs * tk.words * sizeof(uint32_t), s));
+    EFG_LAUNCH(k_hub_bitmaps, nhubs, 1024, 0, s, l_hub, nhubs, P.g.offsets, P.g.nbr, bms, tk.words, hub_slot);
+    tk.hub_slot = hub_slot;
+    tk.bitmaps = bms;
+    tk.ptri = ctx.buf("f_ptri").as<int64_t>(ntasks);
+    tk.pWt = ctx.buf("f_pWt").as<double>(ntasks);
+    EFG_LAUNCH(k_tri_task, ntasks, kTaskThreads, 0, s, a, tk, ntasks);
+    EFG_LAUNCH(k_tri_merge, ceil_div(nhubs, B), B, 0, s, l_hub, nhubs, tstart, tk.ptri, tk.pWt, a);
+    if (st) st->terms = ntasks;
   }
-  // 3. stars by |D_v|
   {
-    int32_t* list = ctx.buf("f_list_stars").as<int32_t>(cnt);
-    const int64_t nsmall = select_seeds(ctx, r, HistRange{hoff, -1, 32}, list, "stars_s");
-    EFG_LAUNCH(k_stars_warp, ceil_div(nsmall * 32, B), B, 0, s, list, nsmall, a);
-    int32_t* list2 = ctx.buf("f_list_stars2").as<int32_t>(cnt);
-    const int64_t nbig = select_seeds(ctx, r, HistRange{hoff, 32, INT64_MAX}, list2, "stars_b");
-    if (nbig) {
-      const size_t smem = 8 * (size_t)maxD;
-      EFG_REQUIRE(smem <= 200 * 1024, "neighbour-degree histogram too wide for shared memory");
-      if (smem > 48 * 1024)
-        EFG_CUDA_CHECK(cudaFuncSetAttribute(k_stars_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      EFG_LAUNCH(k_stars_block, nbig, 256, smem, s, list2, nbig, a);
-    }
-  }
-  // 4. triangles
-  {
-    int32_t* list = ctx.buf("f_list_tri").as<int32_t>(cnt);
-    const int64_t nsm = select_seeds(ctx, r, DegRange{P.g.offsets, -1, 32}, list, "tri_s");
-    EFG_LAUNCH(k_tri_warp, ceil_div(nsm, kTriWarps), kTriWarps * 32, 0, s, list, nsm, a);
-    auto k_tri_seed_256 = k_tri_seed<128, 256, 4>;
-    auto k_tri_seed_1024 = k_tri_seed<256, 1024, 4>;
-    auto k_tri_seed_4096 = k_tri_seed<512, kHashMaxDeg, 2>;
-    const int sm3 = 16 * kHashMaxDeg;  // 2 * MAXD int2 slots
+    // buckets of 4 keys: dv <= 256 at load <= 1/8 with degrees, dv <= 1024 / 4096 at load <= 1/4
+    auto k_tri_seed_256 = k_tri_seed<128, 512, true>;
+    auto k_tri_seed_1024 = k_tri_seed<256, 1024, true>;
+    auto k_tri_seed_4096 = k_tri_seed<512, kHashMaxDeg, false>;
+    const int sm3 = 16 * kHashMaxDeg;
+    EFG_CUDA_CHECK(cudaFuncSetAttribute(k_tri_seed_1024, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 1024));
     EFG_CUDA_CHECK(cudaFuncSetAttribute(k_tri_seed_4096, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3));
-    const int64_t n1 = select_seeds(ctx, r, DegRange{P.g.offsets, 32, 256}, list, "tri_1");
-    EFG_LAUNCH(k_tri_seed_256, n1, 128, 32 * 256, s, list, n1, a);
-    const int64_t n2 = select_seeds(ctx, r, DegRange{P.g.offsets, 256, 1024}, list, "tri_2");
-    EFG_LAUNCH(k_tri_seed_1024, n2, 256, 32 * 1024, s, list, n2, a);
-    const int64_t n3 = select_seeds(ctx, r, DegRange{P.g.offsets, 1024, kHashMaxDeg}, list, "tri_3");
-    EFG_LAUNCH(k_tri_seed_4096, n3, 512, sm3, s, list, n3, a);
-    int32_t* hubs = ctx.buf("f_hubs").as<int32_t>(cnt);
-    const int64_t nhubs = select_seeds(ctx, r, DegRange{P.g.offsets, kHashMaxDeg, INT64_MAX}, hubs, "hubs");
-    if (nhubs) {
-      int64_t* tp = ctx.buf("f_tp").as<int64_t>(P.g.m2);
-      a.tp = tp;
-      int64_t* ntask = ctx.buf("f_ntask").as<int64_t>(nhubs + 1);
-      int64_t* tstart = ctx.buf("f_tstart").as<int64_t>(nhubs + 1);
-      EFG_LAUNCH(k_tri_prefix, ceil_div(nhubs * 32, B), B, 0, s, P.g.offsets, P.pc, hubs, nhubs, tp, ntask);
-      EFG_CUDA_CHECK(cudaMemsetAsync(ntask + nhubs, 0, sizeof(int64_t), s));
-      EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ntask, tstart, nhubs + 1, s));
-      EFG_REGION("cub::DeviceScan::ExclusiveSum", s,
-                 EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, ntask, tstart, nhubs + 1, s)));
-      int64_t ntasks = 0;
-      EFG_CUDA_CHECK(cudaMemcpyAsync(&ntasks, tstart + nhubs, sizeof ntasks, cudaMemcpyDeviceToHost, s));
-      EFG_CUDA_CHECK(cudaStreamSynchronize(s));
-      int32_t* tseed = ctx.buf("f_tseed").as<int32_t>(ntasks);
-      int32_t* tx0 = ctx.buf("f_tx0").as<int32_t>(ntasks);
-      int64_t* tfirst = ctx.buf("f_tfirst").as<int64_t>(ntasks);
-      EFG_LAUNCH(k_tri_fill, ceil_div(nhubs * 32, B), B, 0, s, P.g.offsets, hubs, nhubs, tp, P.pc, tstart, tseed, tx0,
-                 tfirst);
-      TriTasks tk;
-      tk.seed = tseed;
-      tk.x0 = tx0;
-      tk.first = tfirst;
-      tk.words = ceil_div(n, 32);
-      uint32_t* bms = ctx.buf("f_bitmaps").as<uint32_t>(nhubs * tk.words);
-      int32_t* hub_slot = ctx.buf("f_hub_slot").as<int32_t>(n);
-      EFG_CUDA_CHECK(cudaMemsetAsync(bms, 0, nhubs * tk.words * sizeof(uint32_t), s));
-      EFG_LAUNCH(k_hub_bitmaps, nhubs, 1024, 0, s, hubs, nhubs, P.g.offsets, P.g.nbr, bms, tk.words, hub_slot);
-      tk.hub_slot = hub_slot;
-      tk.bitmaps = bms;
-      tk.ptri = ctx.buf("f_ptri").as<int64_t>(ntasks);
-      tk.pWt = ctx.buf("f_pWt").as<double>(ntasks);
-      EFG_LAUNCH(k_tri_task, ntasks, kTaskThreads, 0, s, a, tk, ntasks);
-      EFG_LAUNCH(k_tri_merge, ceil_div(nhubs, B), B, 0, s, hubs, nhubs, tstart, tk.ptri, tk.pWt, a);
-      if (st) st->terms = ntasks;
-    }
+    EFG_LAUNCH(k_tri_seed_4096, c[kTri3], 512, sm3, s, l_tr3, c[kTri3], a);
+    EFG_LAUNCH(k_tri_seed_1024, c[kTri2], 256, 32 * 1024, s, l_tr2, c[kTri2], a);
+    EFG_LAUNCH(k_tri_seed_256, c[kTri1], 128, 32 * 512, s, l_tr1, c[kTri1], a);
+    EFG_LAUNCH(k_tri_warp, ceil_div(c[kTriS], kTriWarps), kTriWarps * 32, 0, s, l_trs, c[kTriS], a);
   }
+  // 3. chains: warp per row (dv <= 1024), CTA per row above
+  EFG_LAUNCH(k_chain_block, c[kChainB], 256, 0, s, l_chb, c[kChainB], a);
+  EFG_LAUNCH(k_chain_warp, ceil_div(c[kChainS] * 32, B), B, 0, s, l_chs, c[kChainS], a);
+  // 4. stars by |D_v|
+  if (c[kStarB]) {
+    const size_t smem = 8 * (size_t)c[kMaxD];
+    EFG_REQUIRE(smem <= 200 * 1024, "neighbour-degree histogram too wide for shared memory");
+    if (smem > 48 * 1024)
+      EFG_CUDA_CHECK(cudaFuncSetAttribute(k_stars_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    EFG_LAUNCH(k_stars_block, c[kStarB], 256, smem, s, l_stb, c[kStarB], a);
+  }
+  EFG_LAUNCH(k_stars_warp, ceil_div(c[kStarS] * 32, B), B, 0, s, l_sts, c[kStarS], a);
   // 5. epilogue
   EFG_LAUNCH(k_epilogue, ceil_div(cnt, B), B, 0, s, a, cnt, ef, total, flags, T_out, W_out);
 }

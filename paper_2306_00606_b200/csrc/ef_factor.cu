@@ -379,10 +379,11 @@ __device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restric
 }
 
 // Rows x = first, first+stride, ... < dv of seed v, one warp per row.
+// Rows ob+x, x = first, first+stride, ... < nrows (of a seed of degree dv).
 template <class Map>
-__device__ __forceinline__ void tri_rows(const FArgs& a, int64_t ob, int dv, int first, int stride, int lane,
-                                         const Map& map, int64_t& tri, double& Wt) {
-  for (int x = first; x < dv; x += stride) {
+__device__ __forceinline__ void tri_rows(const FArgs& a, int64_t ob, int nrows, int first, int stride, int lane,
+                                         const Map& map, int64_t& tri, double& Wt, int dv) {
+  for (int x = first; x < nrows; x += stride) {
     const int64_t e = ob + x;
     const int32_t pc = __ldg(a.pc + e);
     if (pc == 0) continue;
@@ -409,7 +410,7 @@ k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   __syncwarp();
   int64_t tri = 0;
   double Wt = 0.0;
-  tri_rows(a, ob, dv, 0, 1, lane, map, tri, Wt);
+  tri_rows(a, ob, dv, 0, 1, lane, map, tri, Wt, dv);
   tri = warp_sum(tri);
   Wt = warp_sum(Wt);
   if (lane == 0) {
@@ -438,7 +439,7 @@ k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   __syncthreads();
   int64_t tri = 0;
   double Wt = 0.0;
-  tri_rows(a, ob, dv, threadIdx.x >> 5, THREADS / 32, threadIdx.x & 31, map, tri, Wt);
+  tri_rows(a, ob, dv, threadIdx.x >> 5, THREADS / 32, threadIdx.x & 31, map, tri, Wt, dv);
   tri = block_sum<THREADS>(tri, red_i);
   Wt = block_sum<THREADS>(Wt, red_d);
   if (threadIdx.x == 0) {
@@ -495,6 +496,152 @@ k_tri_task(FArgs a, TriTasks tk, int64_t ntasks) {
     tk.ptri[t] = tri;
     tk.pWt[t] = Wt;
   }
+}
+
+// Hubs (dv > kHashMaxDeg), one 1024-thread CTA per hub, hubs in descending
+// work order.  Adj(v) membership in two levels: a shared-memory Bloom filter
+// of kFilterBits bits (one multiplicative hash; at most dv/kFilterBits false
+// positives) answers most probes, and only filter positives read the hub's
+// exact bitmap over node ids in global memory (L2-resident while the hub runs).
+constexpr int kHubThreads = 1024;
+constexpr uint32_t kFilterWords = 48 * 1024;            // 192 KB of shared memory
+constexpr uint32_t kFilterBits = kFilterWords * 32;
+
+struct HubMap {
+  const uint32_t* filt;  // shared
+  const uint32_t* bm;    // global exact bitmap
+  const int32_t* deg;
+  __device__ __forceinline__ static uint32_t fbit(int32_t j) {
+    return (uint32_t)(((uint64_t)((uint32_t)j * 2654435761u) * kFilterBits) >> 32);
+  }
+  __device__ __forceinline__ int32_t degree(int32_t j) const {
+    const uint32_t b = fbit(j);
+    if (!((filt[b >> 5] >> (b & 31)) & 1u)) return -1;
+    return ((__ldg(bm + (j >> 5)) >> (j & 31)) & 1u) ? __ldg(deg + j) : -1;
+  }
+};
+
+// Hub work is cut into tasks of about kHubTask probes (whole rows), so the
+// largest hubs spread over many SMs; each task rebuilds the filter (dv bits,
+// well below its probe count) and writes a partial merged per hub in task order.
+constexpr int64_t kHubTask = 1 << 20;
+
+struct HubTasks {
+  const int32_t* seed;  // [ntasks]
+  const int32_t* x0;    // [ntasks] first row
+  const int32_t* x1;    // [ntasks] end row
+  int64_t* ptri;
+  double* pWt;
+};
+
+__global__ void __launch_bounds__(kHubThreads, 1)
+k_tri_hub(HubTasks tk, int64_t ntasks, const uint32_t* __restrict__ bitmaps, int64_t words,
+          const int32_t* __restrict__ hub_slot, FArgs a) {
+  extern __shared__ uint32_t filt[];  // kFilterWords
+  __shared__ int64_t red_i[kHubThreads / 32];
+  __shared__ double red_d[kHubThreads / 32];
+  const int64_t t = blockIdx.x;
+  if (t >= ntasks) return;
+  const int32_t v = tk.seed[t];
+  const int64_t ob = a.offsets[v];
+  const int dv = (int)(a.offsets[v + 1] - ob);
+  for (uint32_t k = threadIdx.x; k < kFilterWords; k += kHubThreads) filt[k] = 0u;
+  __syncthreads();
+  for (int x = threadIdx.x; x < dv; x += kHubThreads) {
+    const uint32_t b = HubMap::fbit(a.nbr[ob + x]);
+    atomicOr(&filt[b >> 5], 1u << (b & 31));
+  }
+  __syncthreads();
+  HubMap map{filt, bitmaps + (int64_t)hub_slot[v] * words, a.deg};
+  int64_t tri = 0;
+  double Wt = 0.0;
+  const int x0 = tk.x0[t];
+  tri_rows(a, ob + x0, tk.x1[t] - x0, threadIdx.x >> 5, kHubThreads / 32, threadIdx.x & 31, map, tri, Wt, dv);
+  tri = block_sum<kHubThreads>(tri, red_i);
+  Wt = block_sum<kHubThreads>(Wt, red_d);
+  if (threadIdx.x == 0) {
+    tk.ptri[t] = tri;
+    tk.pWt[t] = Wt;
+  }
+}
+
+// Triangle probes of each hub (sort key for the hub order; task count),
+// warp per hub, grid-stride over the device-side hub count.
+__global__ void k_hub_work(const int32_t* __restrict__ hubs, const int64_t* __restrict__ nhubs_dev,
+                           const int64_t* __restrict__ offsets, const int32_t* __restrict__ pc,
+                           int64_t* __restrict__ work, unsigned long long* __restrict__ ntasks) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nhubs = *nhubs_dev;
+  for (int64_t h = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; h < nhubs;
+       h += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int32_t v = hubs[h];
+    int64_t w = 0;
+    for (int64_t p = offsets[v] + lane; p < offsets[v + 1]; p += 32) w += pc[p];
+    w = warp_sum(w);
+    if (lane == 0) {
+      work[h] = w;
+      atomicAdd(ntasks, (unsigned long long)ceil_div(w > 0 ? w : 1, kHubTask));
+    }
+  }
+}
+
+// Task records of the hubs (in descending work order): a warp walks the rows
+// of one hub; with lo_p the probes before row p, task k starts at the row p
+// where lo_{p-1} < k K <= lo_p (task 0 at row 0), k < nt; a task ends where
+// the next one starts.
+__global__ void k_hub_tasks(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ offsets,
+                            const int32_t* __restrict__ pc, const int64_t* __restrict__ tstart,
+                            int32_t* __restrict__ tseed, int32_t* __restrict__ tx0, int32_t* __restrict__ tx1) {
+  const int lane = threadIdx.x & 31;
+  const int64_t h = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (h >= nhubs) return;
+  const int32_t v = hubs[h];
+  const int64_t b = offsets[v], e = offsets[v + 1];
+  const int64_t t0 = tstart[h], nt = tstart[h + 1] - t0;
+  int64_t carry = 0;
+  for (int64_t p0 = b; p0 < e; p0 += 32) {
+    const int64_t p = p0 + lane;
+    const int64_t x = p < e ? pc[p] : 0;
+    int64_t incl = x;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (p < e) {
+      const int64_t lo = carry + incl - x;  // probes before row p
+      const int64_t kmin = p == b ? 0 : (lo - __ldg(pc + p - 1)) / kHubTask + 1;
+      const int64_t kmax = lo / kHubTask < nt - 1 ? lo / kHubTask : nt - 1;
+      for (int64_t k = kmin; k <= kmax; ++k) {
+        tseed[t0 + k] = v;
+        tx0[t0 + k] = (int32_t)(p - b);
+      }
+    }
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  __syncwarp();
+  for (int64_t k = lane; k < nt; k += 32) tx1[t0 + k] = k + 1 < nt ? tx0[t0 + k + 1] : (int32_t)(e - b);
+}
+
+__global__ void k_ceil_tasks(const int64_t* __restrict__ work, int64_t nhubs, int64_t* __restrict__ nt) {
+  const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (h < nhubs) nt[h] = ceil_div(work[h] > 0 ? work[h] : 1, kHubTask);
+  if (h == nhubs) nt[h] = 0;
+}
+
+__global__ void k_hub_merge(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ tstart,
+                            const int64_t* __restrict__ ptri, const double* __restrict__ pWt, FArgs a) {
+  const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (h >= nhubs) return;
+  int64_t tri = 0;
+  double Wt = 0.0;
+  for (int64_t t = tstart[h]; t < tstart[h + 1]; ++t) {
+    tri += ptri[t];
+    Wt += pWt[t];
+  }
+  const int32_t v = hubs[h];
+  a.tri[v - a.seed_lo] = tri;
+  a.Wt[v - a.seed_lo] = Wt;
 }
 
 // Per-row exclusive prefix of (pc + 1) -> tp, and the seed's task count (warp per row).
@@ -731,16 +878,10 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     EFG_REGION("cub::DeviceReduce::Max", s,
                EFG_CUDA_CHECK(cub::DeviceReduce::Max(ctx.buf("cub").get(tmp), tmp, dcnt, cdev + kMaxD, n, s)));
   }
-  // hub tasks: items of a hub = sum over its rows of (|Adj+| + 1), cut every kTask
-  int64_t* tp = ctx.buf("f_tp").as<int64_t>(P.g.m2 > 0 ? P.g.m2 : 1);
-  int64_t* ntask = ctx.buf("f_ntask").as<int64_t>(cnt + 1);
-  int64_t* tstart = ctx.buf("f_tstart").as<int64_t>(cnt + 1);
-  EFG_CUDA_CHECK(cudaMemsetAsync(ntask, 0, (cnt + 1) * sizeof(int64_t), s));
-  EFG_LAUNCH(k_tri_prefix, ceil_div(cnt * 32, B), B, 0, s, P.g.offsets, P.pc, l_hub, cdev + kHubs, tp, ntask);
-  EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, ntask, tstart, cnt + 1, s));
-  EFG_REGION("cub::DeviceScan::ExclusiveSum", s,
-             EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, ntask, tstart, cnt + 1, s)));
-  EFG_LAUNCH(k_gather_count, 1, 1, 0, s, tstart, cdev + kHubs, cdev + kNTasks);
+  int64_t* hw = ctx.buf("f_hub_work").as<int64_t>(2 * cnt + 2);
+  EFG_CUDA_CHECK(cudaMemsetAsync(cdev + kNTasks, 0, sizeof(int64_t), s));
+  EFG_LAUNCH(k_hub_work, 8 * ctx.num_sms, 256, 0, s, l_hub, cdev + kHubs, P.g.offsets, P.pc, hw,
+             reinterpret_cast<unsigned long long*>(cdev + kNTasks));
   int64_t c[kNSlots];
   EFG_CUDA_CHECK(cudaMemcpyAsync(c, cdev, sizeof c, cudaMemcpyDeviceToHost, s));
   EFG_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -758,7 +899,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   a.G = P.gtab;
   a.ps = P.ps;
   a.pc = P.pc;
-  a.tp = tp;
+  a.tp = nullptr;
   a.adjj = P.adjj;
   a.deg = P.deg;
   a.hoff = hoff;
@@ -774,26 +915,38 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   // 2. triangles (the long kernels first)
   const int64_t nhubs = c[kHubs], ntasks = c[kNTasks];
   if (nhubs) {
-    int32_t* tseed = ctx.buf("f_tseed").as<int32_t>(ntasks);
-    int32_t* tx0 = ctx.buf("f_tx0").as<int32_t>(ntasks);
-    int64_t* tfirst = ctx.buf("f_tfirst").as<int64_t>(ntasks);
-    EFG_LAUNCH(k_tri_fill, ceil_div(nhubs * 32, B), B, 0, s, P.g.offsets, l_hub, nhubs, tp, P.pc, tstart, tseed, tx0,
-               tfirst);
-    TriTasks tk;
+    // exact bitmaps; hubs sorted by descending triangle work; tasks of ~kHubTask probes
+    const int64_t words = ceil_div(n, 32);
+    uint32_t* bms = ctx.buf("f_bitmaps").as<uint32_t>(nhubs * words);
+    int32_t* hub_slot = ctx.buf("f_hub_slot").as<int32_t>(n);
+    EFG_CUDA_CHECK(cudaMemsetAsync(bms, 0, nhubs * words * sizeof(uint32_t), s));
+    EFG_LAUNCH(k_hub_bitmaps, nhubs, 1024, 0, s, l_hub, nhubs, P.g.offsets, P.g.nbr, bms, words, hub_slot);
+    int64_t* hw_sorted = hw + nhubs;
+    int32_t* hs = ctx.buf("f_hub_sorted").as<int32_t>(nhubs);
+    EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, hw, hw_sorted, l_hub, hs, nhubs, 0, 64, s));
+    EFG_REGION("cub::DeviceRadixSort::SortPairsDescending", s,
+               EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(ctx.buf("cub").get(tmp), tmp, hw, hw_sorted,
+                                                                        l_hub, hs, nhubs, 0, 64, s)));
+    int64_t* hnt = ctx.buf("f_hub_nt").as<int64_t>(nhubs + 1);
+    int64_t* tstart = ctx.buf("f_hub_tstart").as<int64_t>(nhubs + 1);
+    EFG_LAUNCH(k_ceil_tasks, ceil_div(nhubs + 1, B), B, 0, s, hw_sorted, nhubs, hnt);
+    EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, hnt, tstart, nhubs + 1, s));
+    EFG_REGION("cub::DeviceScan::ExclusiveSum", s,
+               EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, hnt, tstart, nhubs + 1, s)));
+    HubTasks tk;
+    int32_t* tseed = ctx.buf("f_hub_tseed").as<int32_t>(ntasks);
+    int32_t* tx0 = ctx.buf("f_hub_tx0").as<int32_t>(ntasks);
+    int32_t* tx1 = ctx.buf("f_hub_tx1").as<int32_t>(ntasks);
+    EFG_LAUNCH(k_hub_tasks, ceil_div(nhubs * 32, B), B, 0, s, hs, nhubs, P.g.offsets, P.pc, tstart, tseed, tx0, tx1);
     tk.seed = tseed;
     tk.x0 = tx0;
-    tk.first = tfirst;
-    tk.words = ceil_div(n, 32);
-    uint32_t* bms = ctx.buf("f_bitmaps").as<uint32_t>(nhubs * tk.words);
-    int32_t* hub_slot = ctx.buf("f_hub_slot").as<int32_t>(n);
-    EFG_CUDA_CHECK(cudaMemsetAsync(bms, 0, nhubs * tk.words * sizeof(uint32_t), s));
-    EFG_LAUNCH(k_hub_bitmaps, nhubs, 1024, 0, s, l_hub, nhubs, P.g.offsets, P.g.nbr, bms, tk.words, hub_slot);
-    tk.hub_slot = hub_slot;
-    tk.bitmaps = bms;
-    tk.ptri = ctx.buf("f_ptri").as<int64_t>(ntasks);
-    tk.pWt = ctx.buf("f_pWt").as<double>(ntasks);
-    EFG_LAUNCH(k_tri_task, ntasks, kTaskThreads, 0, s, a, tk, ntasks);
-    EFG_LAUNCH(k_tri_merge, ceil_div(nhubs, B), B, 0, s, l_hub, nhubs, tstart, tk.ptri, tk.pWt, a);
+    tk.x1 = tx1;
+    tk.ptri = ctx.buf("f_hub_ptri").as<int64_t>(ntasks);
+    tk.pWt = ctx.buf("f_hub_pWt").as<double>(ntasks);
+    const int smh = kFilterWords * 4;
+    EFG_CUDA_CHECK(cudaFuncSetAttribute(k_tri_hub, cudaFuncAttributeMaxDynamicSharedMemorySize, smh));
+    EFG_LAUNCH(k_tri_hub, ntasks, kHubThreads, smh, s, tk, ntasks, bms, words, hub_slot, a);
+    EFG_LAUNCH(k_hub_merge, ceil_div(nhubs, B), B, 0, s, hs, nhubs, tstart, tk.ptri, tk.pWt, a);
     if (st) st->terms = ntasks;
   }
   {

@@ -34,7 +34,6 @@ namespace efg {
 
 namespace {
 
-constexpr int kTask = 2048;          // flattened triangle items per CTA chunk / hub task
 constexpr int kHashSlots = 8192;     // smem hash of Adj(v) for dv <= 4096
 constexpr int kHashMaxDeg = kHashSlots / 2;
 constexpr int kTaskThreads = 256;
@@ -335,6 +334,23 @@ struct SmemMap {
       }
     }
   }
+  // phase 1: slot of key or -1 (one 16-byte load; the loop only runs past full buckets)
+  __device__ __forceinline__ int32_t probe(int32_t key) const {
+    uint32_t b = bucket(key);
+    int4 q = keys[b];
+    int k = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
+    while (k < 0 && q.w != -1) {  // bucket full: key may sit further on
+      b = (b + 1) & (NB - 1);
+      q = keys[b];
+      k = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
+    }
+    return k >= 0 ? (int32_t)(4 * b + k) : -1;
+  }
+  // phase 2: degree of a key found at `slot`
+  __device__ __forceinline__ int32_t finish(int32_t key, int32_t slot) const {
+    return WITH_DEG ? degs[slot] : __ldg(gdeg + key);
+  }
+  static constexpr bool kPhased = false;  // fused lookup schedules better for smem maps
   __device__ __forceinline__ int32_t degree(int32_t key) const {
     uint32_t b = bucket(key);
     int4 q = keys[b];
@@ -348,31 +364,44 @@ struct SmemMap {
   }
 };
 
-// Hubs: membership from a bitmap over node ids, d_j from the degree array.
-struct BitmapMap {
-  const uint32_t* bm;
-  const int32_t* deg;
-  __device__ __forceinline__ int32_t degree(int32_t j) const {
-    return ((__ldg(bm + (j >> 5)) >> (j & 31)) & 1u) ? __ldg(deg + j) : -1;
-  }
-};
 
-// One warp over entries [p0, p1) of row `row` (= Adj+(i), s0 = dv + di).
+
+// One warp over entries [p0, p1) of row `row` (= Adj+(i), s0 = dv + di), in
+// phases so that each phase's loads are issued together: kUnroll entry loads,
+// kUnroll membership probes, kUnroll degree lookups for the hits, kUnroll
+// G-table gathers, then the (fixed-order) accumulation.
 template <class Map>
 __device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restrict__ row, int32_t p0, int32_t p1,
                                         int32_t s0, int lane, const Map& map, int64_t& tri, double& Wt) {
   for (int32_t p = p0 + lane; p < p1; p += 32 * kUnroll) {
-    int32_t j[kUnroll];
+    int32_t j[kUnroll], dj[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) j[u] = p + 32 * u < p1 ? __ldg(row + p + 32 * u) : -1;
-    int32_t dj[kUnroll];
+    if constexpr (Map::kPhased) {
+      int32_t tag[kUnroll];
+      double g[kUnroll];
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) dj[u] = j[u] >= 0 ? map.degree(j[u]) : -1;
+      for (int u = 0; u < kUnroll; ++u) tag[u] = j[u] >= 0 ? map.probe(j[u]) : -1;
 #pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      if (dj[u] >= 0) {
-        Wt += __ldg(a.G + s0 + dj[u]);
-        ++tri;
+      for (int u = 0; u < kUnroll; ++u) dj[u] = tag[u] >= 0 ? map.finish(j[u], tag[u]) : -1;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) g[u] = dj[u] >= 0 ? __ldg(a.G + s0 + dj[u]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        if (dj[u] >= 0) {
+          Wt += g[u];
+          ++tri;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) dj[u] = j[u] >= 0 ? map.degree(j[u]) : -1;
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        if (dj[u] >= 0) {
+          Wt += __ldg(a.G + s0 + dj[u]);
+          ++tri;
+        }
       }
     }
   }
@@ -448,56 +477,6 @@ k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   }
 }
 
-// Hubs (dv > kHashMaxDeg): tasks of kTask items (prefix tp counts pc+1 per
-// row), one CTA each; warps take the task's rows, each restricted to the
-// task's item window; membership from the hub's bitmap over node ids (built
-// once per hub, L2-resident while its tasks run).
-struct TriTasks {
-  const int32_t* seed;      // [ntasks]
-  const int32_t* x0;        // [ntasks] first row position of the task
-  const int64_t* first;     // [ntasks] index of the seed's first task
-  const int32_t* hub_slot;  // [n] bitmap index
-  const uint32_t* bitmaps;
-  int64_t words;
-  int64_t* ptri;            // [ntasks]
-  double* pWt;              // [ntasks]
-};
-
-__global__ void __launch_bounds__(kTaskThreads)
-k_tri_task(FArgs a, TriTasks tk, int64_t ntasks) {
-  constexpr int NW = kTaskThreads / 32;
-  __shared__ int64_t red_i[NW];
-  __shared__ double red_d[NW];
-  const int64_t t = blockIdx.x;
-  if (t >= ntasks) return;
-  const int32_t v = tk.seed[t];
-  const int64_t ob = a.offsets[v];
-  const int dv = (int)(a.offsets[v + 1] - ob);
-  const int64_t qa = (t - tk.first[t]) * (int64_t)kTask;
-  const int64_t qb = qa + kTask;
-  const int xa = tk.x0[t];
-  BitmapMap map{tk.bitmaps + (int64_t)tk.hub_slot[v] * tk.words, a.deg};
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  int64_t tri = 0;
-  double Wt = 0.0;
-  // rows xa, xa+1, ... whose first item < qb (at most kTask + 1 rows)
-  for (int x = xa + w; x < dv && x <= xa + kTask; x += NW) {
-    const int64_t e = ob + x;
-    const int64_t r0 = a.tp[e];
-    if (r0 >= qb) break;
-    const int32_t pc = __ldg(a.pc + e);
-    const int32_t lo = (int32_t)(r0 > qa ? 0 : qa - r0);  // row items inside [qa, qb)
-    const int32_t hi = (int32_t)(r0 + pc < qb ? pc : qb - r0);
-    if (hi > lo) tri_row(a, a.adjj + __ldg(a.ps + e), lo, hi, dv + __ldg(a.nd + e), lane, map, tri, Wt);
-  }
-  tri = block_sum<kTaskThreads>(tri, red_i);
-  Wt = block_sum<kTaskThreads>(Wt, red_d);
-  if (threadIdx.x == 0) {
-    tk.ptri[t] = tri;
-    tk.pWt[t] = Wt;
-  }
-}
-
 // Hubs (dv > kHashMaxDeg), one 1024-thread CTA per hub, hubs in descending
 // work order.  Adj(v) membership in two levels: a shared-memory Bloom filter
 // of kFilterBits bits (one multiplicative hash; at most dv/kFilterBits false
@@ -514,10 +493,18 @@ struct HubMap {
   __device__ __forceinline__ static uint32_t fbit(int32_t j) {
     return (uint32_t)(((uint64_t)((uint32_t)j * 2654435761u) * kFilterBits) >> 32);
   }
-  __device__ __forceinline__ int32_t degree(int32_t j) const {
+  static constexpr bool kPhased = true;  // global loads: issue each phase's loads together
+  __device__ __forceinline__ int32_t degree(int32_t j) const { return probe(j) >= 0 ? finish(j, 0) : -1; }
+  // phase 1: shared-memory filter
+  __device__ __forceinline__ int32_t probe(int32_t j) const {
     const uint32_t b = fbit(j);
-    if (!((filt[b >> 5] >> (b & 31)) & 1u)) return -1;
-    return ((__ldg(bm + (j >> 5)) >> (j & 31)) & 1u) ? __ldg(deg + j) : -1;
+    return ((filt[b >> 5] >> (b & 31)) & 1u) ? 0 : -1;
+  }
+  // phase 2: exact bitmap word and degree fetched together
+  __device__ __forceinline__ int32_t finish(int32_t j, int32_t) const {
+    const uint32_t w = __ldg(bm + (j >> 5));
+    const int32_t d = __ldg(deg + j);
+    return ((w >> (j & 31)) & 1u) ? d : -1;
   }
 };
 
@@ -644,67 +631,6 @@ __global__ void k_hub_merge(const int32_t* __restrict__ hubs, int64_t nhubs, con
   a.Wt[v - a.seed_lo] = Wt;
 }
 
-// Per-row exclusive prefix of (pc + 1) -> tp, and the seed's task count (warp per row).
-__global__ void k_tri_prefix(const int64_t* __restrict__ offsets, const int32_t* __restrict__ pc,
-                             const int32_t* __restrict__ seeds, const int64_t* __restrict__ count_dev,
-                             int64_t* __restrict__ tp, int64_t* __restrict__ ntask) {
-  const int lane = threadIdx.x & 31;
-  int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (q >= *count_dev) return;
-  const int32_t v = seeds[q];
-  const int64_t b = offsets[v], e = offsets[v + 1];
-  int64_t carry = 0;
-  for (int64_t p0 = b; p0 < e; p0 += 32) {
-    const int64_t p = p0 + lane;
-    const int64_t x = p < e ? (int64_t)pc[p] + 1 : 0;
-    int64_t incl = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (p < e) tp[p] = carry + incl - x;
-    carry += __shfl_sync(0xffffffffu, incl, 31);
-  }
-  if (lane == 0) ntask[q] = ceil_div(carry, kTask);
-}
-
-// Task records: for each slot, every task whose first item falls in it.
-__global__ void k_tri_fill(const int64_t* __restrict__ offsets, const int32_t* __restrict__ seeds, int64_t count,
-                           const int64_t* __restrict__ tp, const int32_t* __restrict__ pc,
-                           const int64_t* __restrict__ tstart, int32_t* __restrict__ tseed,
-                           int32_t* __restrict__ tx0, int64_t* __restrict__ tfirst) {
-  const int lane = threadIdx.x & 31;
-  int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (q >= count) return;
-  const int32_t v = seeds[q];
-  const int64_t b = offsets[v], e = offsets[v + 1];
-  const int64_t base = tstart[q];
-  for (int64_t p = b + lane; p < e; p += 32) {
-    const int64_t lo = tp[p], hi = lo + pc[p] + 1;  // items [lo, hi)
-    for (int64_t k = ceil_div(lo, kTask); k * kTask < hi; ++k) {
-      tseed[base + k] = v;
-      tx0[base + k] = (int32_t)(p - b);
-      tfirst[base + k] = base;
-    }
-  }
-}
-
-__global__ void k_tri_merge(const int32_t* __restrict__ seeds, int64_t count, const int64_t* __restrict__ tstart,
-                            const int64_t* __restrict__ ptri, const double* __restrict__ pWt, FArgs a) {
-  int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (q >= count) return;
-  const int32_t v = seeds[q];
-  int64_t tri = 0;
-  double Wt = 0.0;
-  for (int64_t t = tstart[q]; t < tstart[q + 1]; ++t) {
-    tri += ptri[t];
-    Wt += pWt[t];
-  }
-  a.tri[v - a.seed_lo] = tri;
-  a.Wt[v - a.seed_lo] = Wt;
-}
-
 __global__ void k_hub_bitmaps(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ offsets,
                               const int32_t* __restrict__ nbr, uint32_t* __restrict__ bitmaps, int64_t words,
                               int32_t* __restrict__ hub_slot) {
@@ -773,11 +699,6 @@ void select_seeds(Context& ctx, SeedRange r, Pred pred, int32_t* out, int64_t* c
              EFG_CUDA_CHECK(cub::DeviceSelect::If(ctx.buf("cub").get(tmp), tmp, it, out, count_dev, cnt, pred, s)));
 }
 
-__global__ void k_gather_count(const int64_t* __restrict__ arr, const int64_t* __restrict__ idx,
-                               int64_t* __restrict__ out) {
-  *out = arr[*idx];
-}
-
 __global__ void k_seed_work(const int64_t* __restrict__ offsets, const int32_t* __restrict__ pcv,
                             const int64_t* __restrict__ hoff, int64_t n, int64_t* __restrict__ work) {
   const int lane = threadIdx.x & 31;
@@ -795,8 +716,6 @@ __global__ void k_seed_work(const int64_t* __restrict__ offsets, const int32_t* 
 
 }  // namespace
 
-// Neighbour-degree histograms H_i for every node (sorted distinct degrees +
-// counts).  Returns the number of entries.
 // Neighbour-degree histograms H_i for every node: sorted distinct degrees
 // (hkey) with counts (hcnt), row offsets hoff.  Asynchronous: hkey/hcnt are
 // sized by the bound sum |D_i| <= 2m, the exact total stays on the device.

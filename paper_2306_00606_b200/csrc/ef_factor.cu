@@ -508,10 +508,10 @@ struct HubMap {
   }
 };
 
-// Hub work is cut into tasks of about kHubTask probes (whole rows), so the
-// largest hubs spread over many SMs; each task rebuilds the filter (dv bits,
-// well below its probe count) and writes a partial merged per hub in task order.
-constexpr int64_t kHubTask = 1 << 20;
+// Hub work is cut into tasks of kHubRows consecutive rows, so the largest
+// hubs spread over many SMs; each task rebuilds the filter (dv bits, well
+// below its probe count) and writes a partial merged per hub in task order.
+constexpr int64_t kHubRows = 8192;
 
 struct HubTasks {
   const int32_t* seed;  // [ntasks]
@@ -552,8 +552,8 @@ k_tri_hub(HubTasks tk, int64_t ntasks, const uint32_t* __restrict__ bitmaps, int
   }
 }
 
-// Triangle probes of each hub (sort key for the hub order; task count),
-// warp per hub, grid-stride over the device-side hub count.
+// Triangle probes of each hub (sort key for the hub order), warp per hub,
+// grid-stride over the device-side hub count; total task count.
 __global__ void k_hub_work(const int32_t* __restrict__ hubs, const int64_t* __restrict__ nhubs_dev,
                            const int64_t* __restrict__ offsets, const int32_t* __restrict__ pc,
                            int64_t* __restrict__ work, unsigned long long* __restrict__ ntasks) {
@@ -567,53 +567,31 @@ __global__ void k_hub_work(const int32_t* __restrict__ hubs, const int64_t* __re
     w = warp_sum(w);
     if (lane == 0) {
       work[h] = w;
-      atomicAdd(ntasks, (unsigned long long)ceil_div(w > 0 ? w : 1, kHubTask));
+      atomicAdd(ntasks, (unsigned long long)ceil_div(offsets[v + 1] - offsets[v], kHubRows));
     }
   }
 }
 
-// Task records of the hubs (in descending work order): a warp walks the rows
-// of one hub; with lo_p the probes before row p, task k starts at the row p
-// where lo_{p-1} < k K <= lo_p (task 0 at row 0), k < nt; a task ends where
-// the next one starts.
+__global__ void k_hub_ntasks(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ offsets,
+                             int64_t* __restrict__ nt) {
+  const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (h < nhubs) nt[h] = ceil_div(offsets[hubs[h] + 1] - offsets[hubs[h]], kHubRows);
+  if (h == nhubs) nt[h] = 0;
+}
+
+// Task records (thread per hub, tasks of one hub contiguous, hubs in order).
 __global__ void k_hub_tasks(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ offsets,
-                            const int32_t* __restrict__ pc, const int64_t* __restrict__ tstart,
-                            int32_t* __restrict__ tseed, int32_t* __restrict__ tx0, int32_t* __restrict__ tx1) {
-  const int lane = threadIdx.x & 31;
-  const int64_t h = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+                            const int64_t* __restrict__ tstart, int32_t* __restrict__ tseed,
+                            int32_t* __restrict__ tx0, int32_t* __restrict__ tx1) {
+  const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (h >= nhubs) return;
   const int32_t v = hubs[h];
-  const int64_t b = offsets[v], e = offsets[v + 1];
-  const int64_t t0 = tstart[h], nt = tstart[h + 1] - t0;
-  int64_t carry = 0;
-  for (int64_t p0 = b; p0 < e; p0 += 32) {
-    const int64_t p = p0 + lane;
-    const int64_t x = p < e ? pc[p] : 0;
-    int64_t incl = x;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    if (p < e) {
-      const int64_t lo = carry + incl - x;  // probes before row p
-      const int64_t kmin = p == b ? 0 : (lo - __ldg(pc + p - 1)) / kHubTask + 1;
-      const int64_t kmax = lo / kHubTask < nt - 1 ? lo / kHubTask : nt - 1;
-      for (int64_t k = kmin; k <= kmax; ++k) {
-        tseed[t0 + k] = v;
-        tx0[t0 + k] = (int32_t)(p - b);
-      }
-    }
-    carry += __shfl_sync(0xffffffffu, incl, 31);
+  const int64_t dv = offsets[v + 1] - offsets[v];
+  for (int64_t t = tstart[h], x = 0; t < tstart[h + 1]; ++t, x += kHubRows) {
+    tseed[t] = v;
+    tx0[t] = (int32_t)x;
+    tx1[t] = (int32_t)(x + kHubRows < dv ? x + kHubRows : dv);
   }
-  __syncwarp();
-  for (int64_t k = lane; k < nt; k += 32) tx1[t0 + k] = k + 1 < nt ? tx0[t0 + k + 1] : (int32_t)(e - b);
-}
-
-__global__ void k_ceil_tasks(const int64_t* __restrict__ work, int64_t nhubs, int64_t* __restrict__ nt) {
-  const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (h < nhubs) nt[h] = ceil_div(work[h] > 0 ? work[h] : 1, kHubTask);
-  if (h == nhubs) nt[h] = 0;
 }
 
 __global__ void k_hub_merge(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ tstart,
@@ -848,7 +826,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
                                                                         l_hub, hs, nhubs, 0, 64, s)));
     int64_t* hnt = ctx.buf("f_hub_nt").as<int64_t>(nhubs + 1);
     int64_t* tstart = ctx.buf("f_hub_tstart").as<int64_t>(nhubs + 1);
-    EFG_LAUNCH(k_ceil_tasks, ceil_div(nhubs + 1, B), B, 0, s, hw_sorted, nhubs, hnt);
+    EFG_LAUNCH(k_hub_ntasks, ceil_div(nhubs + 1, B), B, 0, s, hs, nhubs, P.g.offsets, hnt);
     EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, hnt, tstart, nhubs + 1, s));
     EFG_REGION("cub::DeviceScan::ExclusiveSum", s,
                EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, hnt, tstart, nhubs + 1, s)));
@@ -856,7 +834,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     int32_t* tseed = ctx.buf("f_hub_tseed").as<int32_t>(ntasks);
     int32_t* tx0 = ctx.buf("f_hub_tx0").as<int32_t>(ntasks);
     int32_t* tx1 = ctx.buf("f_hub_tx1").as<int32_t>(ntasks);
-    EFG_LAUNCH(k_hub_tasks, ceil_div(nhubs * 32, B), B, 0, s, hs, nhubs, P.g.offsets, P.pc, tstart, tseed, tx0, tx1);
+    EFG_LAUNCH(k_hub_tasks, ceil_div(nhubs, B), B, 0, s, hs, nhubs, P.g.offsets, tstart, tseed, tx0, tx1);
     tk.seed = tseed;
     tk.x0 = tx0;
     tk.x1 = tx1;

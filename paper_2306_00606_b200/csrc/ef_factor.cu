@@ -36,7 +36,6 @@ namespace {
 
 constexpr int kHashSlots = 8192;     // smem hash of Adj(v) for dv <= 4096
 constexpr int kHashMaxDeg = kHashSlots / 2;
-constexpr int kTaskThreads = 256;
 
 struct FArgs {
   const int64_t* offsets;
@@ -47,10 +46,9 @@ struct FArgs {
   const double* G;         // G[S] = F(S-6) - F(S-4): triangle correction per unit weight
   const int64_t* ps;       // [2m] start of Adj+(nbr[e]) in adjp
   const int32_t* pc;       // [2m] |Adj+(nbr[e])|
-  const int64_t* tp;       // [2m] row prefix of (pc + 1): flattened triangle items
   const int32_t* adjj;     // oriented adjacency Adj+ (ascending j per row)
   const int32_t* deg;
-  const int64_t* hoff;
+  const int32_t* dcnt;     // |D_i|: H_i = hkey/hcnt[offsets[i], offsets[i] + dcnt[i])
   const int32_t* hkey;
   const int32_t* hcnt;
   const double* ctab;
@@ -64,67 +62,161 @@ struct FArgs {
 };
 
 // ---------------------------------------------------------------- H build
-// Warp per row: number of distinct values in the sorted neighbour-degree row.
-__global__ void k_rle_count(const int64_t* __restrict__ offsets, const int32_t* __restrict__ snd,
-                            int64_t n, int64_t* __restrict__ dcnt) {
+// H_i (the histogram of the degrees of Adj(i): distinct values ascending, with
+// counts) is stored in adjacency-slot space: row i occupies hkey/hcnt
+// [offsets[i], offsets[i] + dcnt[i]) (|D_i| <= d_i), so no scan/compaction pass
+// is needed.  Rows are sorted by size class: a warp bitonic sort in registers
+// (d <= 32), a CTA radix sort in shared memory (d <= 2048), CUB's segmented
+// sort for the few larger rows followed by a CTA run-length pass.
+
+// d <= 32: warp per row, 32-lane bitonic sort of the neighbour degrees.
+__global__ void k_hist_warp(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
+                            const int32_t* __restrict__ nd, int32_t* __restrict__ hkey, int32_t* __restrict__ hcnt,
+                            int32_t* __restrict__ dcnt) {
   const int lane = threadIdx.x & 31;
-  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (v >= n) return;
-  int64_t b = offsets[v], e = offsets[v + 1];
-  int c = 0;
-  for (int64_t p = b + lane; p < e; p += 32) c += (p == b) || (snd[p] != snd[p - 1]);
-  for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if (lane == 0) dcnt[v] = c;
+  const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (q >= count) return;
+  const int32_t i = rows[q];
+  const int64_t b = offsets[i];
+  const int d = (int)(offsets[i + 1] - b);
+  int32_t x = lane < d ? nd[b + lane] : 0x7fffffff;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+      const bool up = (lane & k) == 0;          // ascending block
+      const bool lower = (lane & j) == 0;
+      x = (lower == up) ? min(x, y) : max(x, y);
+    }
+  }
+  const int32_t prev = __shfl_up_sync(0xffffffffu, x, 1);
+  const bool head = lane < d && (lane == 0 || x != prev);
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  if (head) {
+    const unsigned above = heads & ~((2u << lane) - 1);   // heads after this lane
+    const int next = above ? __ffs(above) - 1 : d;
+    const int r = __popc(heads & ((1u << lane) - 1));
+    hkey[b + r] = x;
+    hcnt[b + r] = next - lane;
+  }
+  if (lane == 0) dcnt[i] = __popc(heads);
 }
 
-// Warp per row: (key, count) runs of the sorted row, ascending key.  Heads
-// are compacted first (their row-relative positions parked in hcnt), then
-// each run length is the distance to the next head.
-__global__ void k_rle_fill(const int64_t* __restrict__ offsets, const int32_t* __restrict__ snd, int64_t n,
-                           const int64_t* __restrict__ hoff, int32_t* __restrict__ hkey,
-                           int32_t* __restrict__ hcnt) {
-  const int lane = threadIdx.x & 31;
-  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (v >= n) return;
-  const int64_t b = offsets[v], e = offsets[v + 1];
-  const int64_t h0 = hoff[v], h1 = hoff[v + 1];
-  int64_t out = h0;
-  for (int64_t p0 = b; p0 < e; p0 += 32) {
-    int64_t p = p0 + lane;
-    bool head = p < e && ((p == b) || (snd[p] != snd[p - 1]));
-    unsigned mask = __ballot_sync(0xffffffffu, head);
+// 32 < d <= THREADS*ITEMS: CTA per row, radix sort in shared memory over the
+// bits degrees actually use (keys < 2^bits; padding = 2^bits - 1 sorts last).
+constexpr int kHistThreads = 256, kHistItems = 8;
+template <int kHistThreads, int kHistItems>
+__global__ void __launch_bounds__(kHistThreads)
+k_hist_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
+             const int32_t* __restrict__ nd, int32_t* __restrict__ hkey, int32_t* __restrict__ hcnt,
+             int32_t* __restrict__ dcnt, int bits) {
+  using Sort = cub::BlockRadixSort<uint32_t, kHistThreads, kHistItems>;
+  using Scan = cub::BlockScan<int32_t, kHistThreads>;
+  __shared__ union {
+    typename Sort::TempStorage sort;
+    typename Scan::TempStorage scan;
+  } tmp;
+  __shared__ uint32_t keys[kHistThreads * kHistItems + 1];
+  __shared__ int32_t hpos[kHistThreads * kHistItems + 1];
+  const int64_t q = blockIdx.x;
+  if (q >= count) return;
+  const int32_t i = rows[q];
+  const int64_t b = offsets[i];
+  const int d = (int)(offsets[i + 1] - b);
+  uint32_t k[kHistItems];
+  const uint32_t pad = (1u << bits) - 1;
+#pragma unroll
+  for (int u = 0; u < kHistItems; ++u) {
+    const int p = threadIdx.x * kHistItems + u;
+    k[u] = p < d ? (uint32_t)nd[b + p] : pad;
+  }
+  Sort(tmp.sort).Sort(k, 0, bits);  // blocked arrangement, ascending
+#pragma unroll
+  for (int u = 0; u < kHistItems; ++u) keys[threadIdx.x * kHistItems + u] = k[u];
+  __syncthreads();
+  int32_t nh = 0;
+  bool hd[kHistItems];
+#pragma unroll
+  for (int u = 0; u < kHistItems; ++u) {
+    const int p = threadIdx.x * kHistItems + u;
+    hd[u] = p < d && (p == 0 || keys[p] != keys[p - 1]);
+    nh += hd[u];
+  }
+  int32_t rank, total;
+  Scan(tmp.scan).ExclusiveSum(nh, rank, total);
+#pragma unroll
+  for (int u = 0; u < kHistItems; ++u) {
+    if (hd[u]) {
+      hpos[rank] = threadIdx.x * kHistItems + u;
+      hkey[b + rank] = (int32_t)k[u];
+      ++rank;
+    }
+  }
+  if (threadIdx.x == 0) hpos[total] = d;
+  __syncthreads();
+  for (int r = threadIdx.x; r < total; r += kHistThreads) hcnt[b + r] = hpos[r + 1] - hpos[r];
+  if (threadIdx.x == 0) dcnt[i] = total;
+}
+
+// d > 2048: run-length pass over a row already sorted in `snd` (CTA per row).
+__global__ void __launch_bounds__(256)
+k_hist_rle(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
+           const int32_t* __restrict__ snd, int32_t* __restrict__ hkey, int32_t* __restrict__ hcnt,
+           int32_t* __restrict__ dcnt) {
+  using Scan = cub::BlockScan<int32_t, 256>;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int32_t carry;
+  const int64_t q = blockIdx.x;
+  if (q >= count) return;
+  const int32_t i = rows[q];
+  const int64_t b = offsets[i];
+  const int d = (int)(offsets[i + 1] - b);
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  // pass 1: heads -> hkey, head position parked in hcnt
+  for (int p0 = 0; p0 < d; p0 += 256) {
+    const int p = p0 + threadIdx.x;
+    const bool head = p < d && (p == 0 || snd[b + p] != snd[b + p - 1]);
+    int32_t rank, tot;
+    Scan(tmp).ExclusiveSum((int32_t)head, rank, tot);
+    const int32_t base = carry;
     if (head) {
-      int64_t slot = out + __popc(mask & ((1u << lane) - 1));
-      hkey[slot] = snd[p];
-      hcnt[slot] = (int32_t)(p - b);
+      hkey[b + base + rank] = snd[b + p];
+      hcnt[b + base + rank] = p;
     }
-    out += __popc(mask);
+    __syncthreads();
+    if (threadIdx.x == 0) carry = base + tot;
+    __syncthreads();
   }
-  __syncwarp();
-  for (int64_t s0 = h0; s0 < h1; s0 += 32) {
-    int64_t sl = s0 + lane;
+  const int32_t total = carry;
+  // pass 2: counts = distance to the next head (read all, then write)
+  for (int r0 = 0; r0 < total; r0 += 256) {
+    const int r = r0 + threadIdx.x;
     int32_t cur = 0, nxt = 0;
-    if (sl < h1) {
-      cur = hcnt[sl];
-      nxt = sl + 1 < h1 ? hcnt[sl + 1] : (int32_t)(e - b);
+    if (r < total) {
+      cur = hcnt[b + r];
+      nxt = r + 1 < total ? hcnt[b + r + 1] : d;
     }
-    __syncwarp();
-    if (sl < h1) hcnt[sl] = nxt - cur;
-    __syncwarp();
+    __syncthreads();
+    if (r < total) hcnt[b + r] = nxt - cur;
+    __syncthreads();
   }
+  if (threadIdx.x == 0) dcnt[i] = total;
 }
 
 // Chain table, group of G lanes per row i: for every distinct neighbour
 // degree y of i, C_i(y) = sum_a h_a F[y + di - 4 + x_a] - F[2y + di - 4].
 template <int G>
-__global__ void k_ctab_group(const int64_t* __restrict__ hoff, const int32_t* __restrict__ hkey,
+__global__ void k_ctab_group(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
+                             const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey,
                              const int32_t* __restrict__ hcnt, const int32_t* __restrict__ deg,
-                             const double* __restrict__ F, int64_t n, int64_t big, double* __restrict__ ctab) {
+                             const double* __restrict__ F, double* __restrict__ ctab) {
   const int sub = threadIdx.x & (G - 1);
-  int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
-  if (i >= n) return;
-  int64_t b = hoff[i], e = hoff[i + 1];
-  if (e - b > big) return;  // k_ctab_block
+  int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
+  if (q >= count) return;
+  const int32_t i = rows[q];
+  int64_t b = offsets[i], e = b + dcnt[i];
   int32_t di = deg[i];
   for (int64_t o = b + sub; o < e; o += G) {
     int32_t y = hkey[o];
@@ -136,14 +228,14 @@ __global__ void k_ctab_group(const int64_t* __restrict__ hoff, const int32_t* __
 }
 
 // Rows with many distinct degrees: one CTA per row, threads over outputs.
-__global__ void k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __restrict__ hoff,
-                             const int32_t* __restrict__ hkey, const int32_t* __restrict__ hcnt,
-                             const int32_t* __restrict__ deg, const double* __restrict__ F,
-                             double* __restrict__ ctab) {
+__global__ void k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __restrict__ offsets,
+                             const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey,
+                             const int32_t* __restrict__ hcnt, const int32_t* __restrict__ deg,
+                             const double* __restrict__ F, double* __restrict__ ctab) {
   int64_t r = blockIdx.x;
   if (r >= nrows) return;
   int32_t i = rows[r];
-  int64_t b = hoff[i], e = hoff[i + 1];
+  int64_t b = offsets[i], e = b + dcnt[i];
   int32_t di = deg[i];
   for (int64_t o = b + threadIdx.x; o < e; o += blockDim.x) {
     int32_t y = hkey[o];
@@ -153,12 +245,6 @@ __global__ void k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, co
     ctab[o] = acc - __ldg(F + base + y);
   }
 }
-
-struct BigRow {
-  const int64_t* hoff;
-  int64_t big;
-  __host__ __device__ bool operator()(const int32_t& i) const { return hoff[i + 1] - hoff[i] > big; }
-};
 
 // ---------------------------------------------------------------- per seed
 template <class T>
@@ -189,7 +275,7 @@ __device__ __forceinline__ void chain_slot(const FArgs& a, int64_t e, int64_t dv
   const int32_t i = a.nbr[e];
   const int64_t di = a.nd[e];
   Tc += (di - 1) * (dv + di - 4) + a.s1[i] - dv;
-  int64_t lo = a.hoff[i], hi = a.hoff[i + 1] - 1;
+  int64_t lo = a.offsets[i], hi = lo + a.dcnt[i] - 1;
   while (lo < hi) {  // dv is present: v is a neighbour of i
     int64_t mid = (lo + hi) >> 1;
     if (__ldg(a.hkey + mid) < dv) lo = mid + 1; else hi = mid;
@@ -240,8 +326,8 @@ __global__ void k_stars_warp(const int32_t* __restrict__ seeds, int64_t count, F
   if (q >= count) return;
   const int32_t v = seeds[q];
   const int64_t dv = a.offsets[v + 1] - a.offsets[v];
-  const int64_t hb = a.hoff[v];
-  const int D = (int)(a.hoff[v + 1] - hb);
+  const int64_t hb = a.offsets[v];
+  const int D = a.dcnt[v];
   int32_t xa = 0;
   int64_t ha = 0;
   if (lane < D) {
@@ -262,21 +348,15 @@ __global__ void k_stars_warp(const int32_t* __restrict__ seeds, int64_t count, F
 
 // Stars for |D_v| > 32: CTA per seed, H_v staged in shared memory.
 __global__ void __launch_bounds__(256) k_stars_block(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
-  extern __shared__ int32_t sh[];
   __shared__ double red[8];
   const int64_t q = blockIdx.x;
   if (q >= count) return;
   const int32_t v = seeds[q];
-  const int64_t dv = a.offsets[v + 1] - a.offsets[v];
-  const int64_t hb = a.hoff[v];
-  const int D = (int)(a.hoff[v + 1] - hb);
-  int32_t* sk = sh;
-  int32_t* sc = sh + D;
-  for (int t = threadIdx.x; t < D; t += 256) {
-    sk[t] = a.hkey[hb + t];
-    sc[t] = a.hcnt[hb + t];
-  }
-  __syncthreads();
+  const int64_t hb = a.offsets[v];
+  const int64_t dv = a.offsets[v + 1] - hb;
+  const int D = a.dcnt[v];
+  const int32_t* __restrict__ sk = a.hkey + hb;
+  const int32_t* __restrict__ sc = a.hcnt + hb;
   const int64_t c = dv - 4;
   double Ws = 0.0;
   // row ra pairs with rb > ra; rows dealt from both ends for balance
@@ -655,15 +735,6 @@ struct DegRange {
   }
 };
 
-struct HistRange {
-  const int64_t* hoff;
-  int64_t lo, hi;  // lo < |D_v| <= hi
-  __host__ __device__ bool operator()(const int32_t& v) const {
-    int64_t d = hoff[v + 1] - hoff[v];
-    return d > lo && d <= hi;
-  }
-};
-
 // Seeds of r satisfying pred -> out (ascending); the count lands in *count_dev
 // (device memory, read back with all other counts in one synchronisation).
 template <class Pred>
@@ -678,7 +749,7 @@ void select_seeds(Context& ctx, SeedRange r, Pred pred, int32_t* out, int64_t* c
 }
 
 __global__ void k_seed_work(const int64_t* __restrict__ offsets, const int32_t* __restrict__ pcv,
-                            const int64_t* __restrict__ hoff, int64_t n, int64_t* __restrict__ work) {
+                            const int32_t* __restrict__ dcnt, int64_t n, int64_t* __restrict__ work) {
   const int lane = threadIdx.x & 31;
   int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (v >= n) return;
@@ -687,106 +758,158 @@ __global__ void k_seed_work(const int64_t* __restrict__ offsets, const int32_t* 
   for (int64_t p = b + lane; p < e; p += 32) w += pcv[p] + 8;  // triangle probes + chain lookup
   w = warp_sum(w);
   if (lane == 0) {
-    int64_t D = hoff[v + 1] - hoff[v];
+    int64_t D = dcnt[v];
     work[v] = w + D * (D + 1) / 2 + 64;
   }
 }
 
 }  // namespace
 
-// Neighbour-degree histograms H_i for every node: sorted distinct degrees
-// (hkey) with counts (hcnt), row offsets hoff.  Asynchronous: hkey/hcnt are
-// sized by the bound sum |D_i| <= 2m, the exact total stays on the device.
-static void build_histograms(Context& ctx, Prepared& P, int64_t*& hoff, int32_t*& hkey, int32_t*& hcnt) {
+// Segment bounds of listed rows (CUB segmented sort over non-contiguous rows).
+struct RowBegin {
+  const int32_t* rows;
+  const int64_t* off;
+  __host__ __device__ int64_t operator()(const int64_t& k) const { return off[rows[k]]; }
+};
+struct RowEnd {
+  const int32_t* rows;
+  const int64_t* off;
+  __host__ __device__ int64_t operator()(const int64_t& k) const { return off[rows[k] + 1]; }
+};
+
+// Class lists by degree (all known before any histogram is built).
+struct Lists {
+  int32_t *hw, *hs, *hb, *hl;     // histogram rows: d <= 32, <= 256, <= 2048, > 2048 (all nodes)
+  int32_t *cg, *cb;               // chain tables: d <= 64, > 64 (all nodes)
+  int32_t *chs, *chb;             // chain sums: seeds dv <= 1024, > 1024
+  int32_t *sts, *stb;             // stars: dv <= 32, > 32
+  int32_t *trs, *tr1, *tr2, *tr3, *hub;  // triangles
+};
+enum Slot {
+  kHW, kHS, kHB, kHL, kCG, kCB, kChS, kChB, kStS, kStB, kTrS, kTr1, kTr2, kTr3, kHubs, kNTasks, kNSlots
+};
+constexpr int64_t kHistWarpMax = 32, kHistBlockMax = kHistThreads * kHistItems, kCtabGroupMax = 64;
+
+static Lists make_lists(Context& ctx, const Prepared& P, SeedRange r, int64_t* cdev, bool seeds) {
+  const int64_t n = P.g.n, cnt = r.hi - r.lo;
+  auto list = [&](const char* name, int64_t len) { return ctx.buf(name).as<int32_t>(len > 0 ? len : 1); };
+  const int64_t* off = P.g.offsets;
+  const SeedRange all{0, n};
+  Lists L{};
+  L.hw = list("f_l_hw", n);
+  L.hs = list("f_l_hs", n);
+  L.hb = list("f_l_hb", n);
+  L.hl = list("f_l_hl", n);
+  select_seeds(ctx, all, DegRange{off, -1, kHistWarpMax}, L.hw, cdev + kHW);
+  select_seeds(ctx, all, DegRange{off, kHistWarpMax, 256}, L.hs, cdev + kHS);
+  select_seeds(ctx, all, DegRange{off, 256, kHistBlockMax}, L.hb, cdev + kHB);
+  select_seeds(ctx, all, DegRange{off, kHistBlockMax, INT64_MAX}, L.hl, cdev + kHL);
+  if (!seeds) return L;
+  L.cg = list("f_l_cg", n);
+  L.cb = list("f_l_cb", n);
+  select_seeds(ctx, all, DegRange{off, -1, kCtabGroupMax}, L.cg, cdev + kCG);
+  select_seeds(ctx, all, DegRange{off, kCtabGroupMax, INT64_MAX}, L.cb, cdev + kCB);
+  L.chs = list("f_l_chs", cnt);
+  L.chb = list("f_l_chb", cnt);
+  L.sts = list("f_l_sts", cnt);
+  L.stb = list("f_l_stb", cnt);
+  L.trs = list("f_l_trs", cnt);
+  L.tr1 = list("f_l_tr1", cnt);
+  L.tr2 = list("f_l_tr2", cnt);
+  L.tr3 = list("f_l_tr3", cnt);
+  L.hub = list("f_l_hub", cnt);
+  select_seeds(ctx, r, DegRange{off, -1, 1024}, L.chs, cdev + kChS);
+  select_seeds(ctx, r, DegRange{off, 1024, INT64_MAX}, L.chb, cdev + kChB);
+  select_seeds(ctx, r, DegRange{off, -1, 32}, L.sts, cdev + kStS);
+  select_seeds(ctx, r, DegRange{off, 32, INT64_MAX}, L.stb, cdev + kStB);
+  select_seeds(ctx, r, DegRange{off, -1, 32}, L.trs, cdev + kTrS);
+  select_seeds(ctx, r, DegRange{off, 32, 256}, L.tr1, cdev + kTr1);
+  select_seeds(ctx, r, DegRange{off, 256, 1024}, L.tr2, cdev + kTr2);
+  select_seeds(ctx, r, DegRange{off, 1024, kHashMaxDeg}, L.tr3, cdev + kTr3);
+  select_seeds(ctx, r, DegRange{off, kHashMaxDeg, INT64_MAX}, L.hub, cdev + kHubs);
+  return L;
+}
+
+// Neighbour-degree histograms H_i for every node (slot space, see H build).
+static void build_histograms(Context& ctx, const Prepared& P, const Lists& L, const int64_t* c, int32_t* hkey,
+                             int32_t* hcnt, int32_t* dcnt) {
   cudaStream_t s = ctx.stream;
-  const int64_t n = P.g.n, m2 = P.g.m2;
   const int B = 256;
-  EFG_REQUIRE(m2 < (int64_t(1) << 31), "adjacency too large for the segmented sort (2m >= 2^31)");
-  int32_t* snd = ctx.buf("f_snd").as<int32_t>(m2);
-  size_t tmp = 0;
-  EFG_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, P.nd, snd, (int)m2, (int)n, P.g.offsets,
-                                                    P.g.offsets + 1, s));
-  EFG_REGION("cub::DeviceSegmentedSort::SortKeys", s,
-             EFG_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(ctx.buf("cub").get(tmp), tmp, P.nd, snd, (int)m2,
-                                                               (int)n, P.g.offsets, P.g.offsets + 1, s)));
-  int64_t* dcnt = ctx.buf("f_dcnt").as<int64_t>(n + 1);
-  hoff = ctx.buf("f_hoff").as<int64_t>(n + 1);
-  EFG_LAUNCH(k_rle_count, ceil_div(n * 32, B), B, 0, s, P.g.offsets, snd, n, dcnt);
-  EFG_CUDA_CHECK(cudaMemsetAsync(dcnt + n, 0, sizeof(int64_t), s));
-  EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, dcnt, hoff, n + 1, s));
-  EFG_REGION("cub::DeviceScan::ExclusiveSum", s,
-             EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dcnt, hoff, n + 1, s)));
-  hkey = ctx.buf("f_hkey").as<int32_t>(m2 > 0 ? m2 : 1);
-  hcnt = ctx.buf("f_hcnt").as<int32_t>(m2 > 0 ? m2 : 1);
-  EFG_LAUNCH(k_rle_fill, ceil_div(n * 32, B), B, 0, s, P.g.offsets, snd, n, hoff, hkey, hcnt);
+  const int64_t* off = P.g.offsets;
+  EFG_LAUNCH(k_hist_warp, ceil_div(c[kHW] * 32, B), B, 0, s, L.hw, c[kHW], off, P.nd, hkey, hcnt, dcnt);
+  int bits = 1;
+  while (bits < 31 && (int64_t(1) << bits) <= (int64_t)P.dmax + 1) ++bits;
+  EFG_LAUNCH((k_hist_block<64, 4>), c[kHS], 64, 0, s, L.hs, c[kHS], off, P.nd, hkey, hcnt, dcnt, bits);
+  EFG_LAUNCH((k_hist_block<kHistThreads, kHistItems>), c[kHB], kHistThreads, 0, s, L.hb, c[kHB], off, P.nd, hkey,
+             hcnt, dcnt, bits);
+  if (c[kHL]) {
+    // few large rows: CUB segmented sort in place of their slot ranges, then run lengths
+    const int64_t m2 = P.g.m2;
+    EFG_REQUIRE(m2 < (int64_t(1) << 31), "adjacency too large for the segmented sort (2m >= 2^31)");
+    int32_t* snd = ctx.buf("f_snd").as<int32_t>(m2);
+    cub::CountingInputIterator<int64_t> ci(0);
+    cub::TransformInputIterator<int64_t, RowBegin, cub::CountingInputIterator<int64_t>> bi(ci, RowBegin{L.hl, off});
+    cub::TransformInputIterator<int64_t, RowEnd, cub::CountingInputIterator<int64_t>> ei(ci, RowEnd{L.hl, off});
+    size_t tmp = 0;
+    EFG_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, P.nd, snd, (int)m2, (int)c[kHL], bi, ei, s));
+    EFG_REGION("cub::DeviceSegmentedSort::SortKeys", s,
+               EFG_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(ctx.buf("cub").get(tmp), tmp, P.nd, snd, (int)m2,
+                                                                 (int)c[kHL], bi, ei, s)));
+    EFG_LAUNCH(k_hist_rle, c[kHL], 256, 0, s, L.hl, c[kHL], off, snd, hkey, hcnt, dcnt);
+  }
+}
+
+static int64_t read_counts(Context& ctx, const int64_t* cdev, int64_t* c) {
+  EFG_CUDA_CHECK(cudaMemcpyAsync(c, cdev, kNSlots * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
+  EFG_CUDA_CHECK(cudaStreamSynchronize(ctx.stream));
+  return 0;
 }
 
 void factorized_work(Context& ctx, Prepared& P, int64_t* d_work) {
-  int64_t* hoff;
-  int32_t *hkey, *hcnt;
-  build_histograms(ctx, P, hoff, hkey, hcnt);
+  const int64_t n = P.g.n, m2 = P.g.m2 > 0 ? P.g.m2 : 1;
+  int64_t* cdev = ctx.buf("f_counts").as<int64_t>(kNSlots);
+  EFG_CUDA_CHECK(cudaMemsetAsync(cdev, 0, kNSlots * sizeof(int64_t), ctx.stream));
+  Lists L = make_lists(ctx, P, SeedRange{0, n}, cdev, false);
+  int64_t c[kNSlots];
+  read_counts(ctx, cdev, c);
+  int32_t* hkey = ctx.buf("f_hkey").as<int32_t>(m2);
+  int32_t* hcnt = ctx.buf("f_hcnt").as<int32_t>(m2);
+  int32_t* dcnt = ctx.buf("f_dcnt").as<int32_t>(n);
+  build_histograms(ctx, P, L, c, hkey, hcnt, dcnt);
   const int B = 256;
-  EFG_LAUNCH(k_seed_work, ceil_div(P.g.n * 32, B), B, 0, ctx.stream, P.g.offsets, P.pc, hoff, P.g.n, d_work);
+  EFG_LAUNCH(k_seed_work, ceil_div(n * 32, B), B, 0, ctx.stream, P.g.offsets, P.pc, dcnt, n, d_work);
 }
 
-// The pass has exactly one host synchronisation after prepare(): every
-// class list and task count is produced on the device first, read back in a
-// single copy, and the compute kernels are then launched back to back.
-enum Slot { kBigRow, kChainS, kChainB, kStarS, kStarB, kTriS, kTri1, kTri2, kTri3, kHubs, kNTasks, kMaxD, kNSlots };
-
+// The pass has exactly one host synchronisation after prepare(): every class
+// list (by degree) and the hub task count are produced on the device first
+// and read back in a single copy; the kernels are then launched back to back.
 void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* total, uint8_t* flags,
                    int64_t* T_out, double* W_out, efg_stats* st) {
   cudaStream_t s = ctx.stream;
-  const int64_t n = P.g.n;
+  const int64_t n = P.g.n, m2 = P.g.m2 > 0 ? P.g.m2 : 1;
   const int B = 256;
   size_t tmp = 0;
   const int64_t cnt = r.hi - r.lo;
   if (cnt <= 0) return;
-  int64_t* hoff;
-  int32_t *hkey, *hcnt;
-  build_histograms(ctx, P, hoff, hkey, hcnt);
-  // ---- phase 1: class lists and counts on the device
+  // ---- phase 1: class lists and counts on the device, one read-back
   int64_t* cdev = ctx.buf("f_counts").as<int64_t>(kNSlots);
-  const int64_t kBig = 64;
-  auto list = [&](const char* name, int64_t len) { return ctx.buf(name).as<int32_t>(len > 0 ? len : 1); };
-  int32_t* l_big = list("f_l_big", n);
-  int32_t* l_chs = list("f_l_chs", cnt);
-  int32_t* l_chb = list("f_l_chb", cnt);
-  int32_t* l_sts = list("f_l_sts", cnt);
-  int32_t* l_stb = list("f_l_stb", cnt);
-  int32_t* l_trs = list("f_l_trs", cnt);
-  int32_t* l_tr1 = list("f_l_tr1", cnt);
-  int32_t* l_tr2 = list("f_l_tr2", cnt);
-  int32_t* l_tr3 = list("f_l_tr3", cnt);
-  int32_t* l_hub = list("f_l_hub", cnt);
-  select_seeds(ctx, SeedRange{0, n}, BigRow{hoff, kBig}, l_big, cdev + kBigRow);
-  select_seeds(ctx, r, DegRange{P.g.offsets, -1, 1024}, l_chs, cdev + kChainS);
-  select_seeds(ctx, r, DegRange{P.g.offsets, 1024, INT64_MAX}, l_chb, cdev + kChainB);
-  select_seeds(ctx, r, HistRange{hoff, -1, 32}, l_sts, cdev + kStarS);
-  select_seeds(ctx, r, HistRange{hoff, 32, INT64_MAX}, l_stb, cdev + kStarB);
-  select_seeds(ctx, r, DegRange{P.g.offsets, -1, 32}, l_trs, cdev + kTriS);
-  select_seeds(ctx, r, DegRange{P.g.offsets, 32, 256}, l_tr1, cdev + kTri1);
-  select_seeds(ctx, r, DegRange{P.g.offsets, 256, 1024}, l_tr2, cdev + kTri2);
-  select_seeds(ctx, r, DegRange{P.g.offsets, 1024, kHashMaxDeg}, l_tr3, cdev + kTri3);
-  select_seeds(ctx, r, DegRange{P.g.offsets, kHashMaxDeg, INT64_MAX}, l_hub, cdev + kHubs);
-  {
-    int64_t* dcnt = ctx.buf("f_dcnt").as<int64_t>(n + 1);  // per-node |D_i| (from build_histograms)
-    EFG_CUDA_CHECK(cub::DeviceReduce::Max(nullptr, tmp, dcnt, cdev + kMaxD, n, s));
-    EFG_REGION("cub::DeviceReduce::Max", s,
-               EFG_CUDA_CHECK(cub::DeviceReduce::Max(ctx.buf("cub").get(tmp), tmp, dcnt, cdev + kMaxD, n, s)));
-  }
+  EFG_CUDA_CHECK(cudaMemsetAsync(cdev, 0, kNSlots * sizeof(int64_t), s));
+  Lists L = make_lists(ctx, P, r, cdev, true);
   int64_t* hw = ctx.buf("f_hub_work").as<int64_t>(2 * cnt + 2);
-  EFG_CUDA_CHECK(cudaMemsetAsync(cdev + kNTasks, 0, sizeof(int64_t), s));
-  EFG_LAUNCH(k_hub_work, 8 * ctx.num_sms, 256, 0, s, l_hub, cdev + kHubs, P.g.offsets, P.pc, hw,
+  EFG_LAUNCH(k_hub_work, 8 * ctx.num_sms, 256, 0, s, L.hub, cdev + kHubs, P.g.offsets, P.pc, hw,
              reinterpret_cast<unsigned long long*>(cdev + kNTasks));
   int64_t c[kNSlots];
-  EFG_CUDA_CHECK(cudaMemcpyAsync(c, cdev, sizeof c, cudaMemcpyDeviceToHost, s));
-  EFG_CUDA_CHECK(cudaStreamSynchronize(s));
-  // ---- phase 2: compute kernels, no further host synchronisation
-  // 1. chain tables C_i(y): rows with <= 64 distinct degrees by 8-lane groups, the rest by CTAs
-  double* ctab = ctx.buf("f_ctab").as<double>(P.g.m2 > 0 ? P.g.m2 : 1);
-  EFG_LAUNCH(k_ctab_group<8>, ceil_div(n * 8, B), B, 0, s, hoff, hkey, hcnt, P.deg, P.ftab, n, kBig, ctab);
-  EFG_LAUNCH(k_ctab_block, c[kBigRow], 128, 0, s, l_big, c[kBigRow], hoff, hkey, hcnt, P.deg, P.ftab, ctab);
+  read_counts(ctx, cdev, c);
+  // ---- phase 2: no further host synchronisation
+  int32_t* hkey = ctx.buf("f_hkey").as<int32_t>(m2);
+  int32_t* hcnt = ctx.buf("f_hcnt").as<int32_t>(m2);
+  int32_t* dcnt = ctx.buf("f_dcnt").as<int32_t>(n);
+  build_histograms(ctx, P, L, c, hkey, hcnt, dcnt);
+  // 1. chain tables C_i(y): rows with d <= 64 by 8-lane groups, the rest by CTAs
+  double* ctab = ctx.buf("f_ctab").as<double>(m2);
+  EFG_LAUNCH(k_ctab_group<8>, ceil_div(c[kCG] * 8, B), B, 0, s, L.cg, c[kCG], P.g.offsets, dcnt, hkey, hcnt, P.deg,
+             P.ftab, ctab);
+  EFG_LAUNCH(k_ctab_block, c[kCB], 128, 0, s, L.cb, c[kCB], P.g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab);
   FArgs a;
   a.offsets = P.g.offsets;
   a.nbr = P.g.nbr;
@@ -796,10 +919,9 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   a.G = P.gtab;
   a.ps = P.ps;
   a.pc = P.pc;
-  a.tp = nullptr;
   a.adjj = P.adjj;
   a.deg = P.deg;
-  a.hoff = hoff;
+  a.dcnt = dcnt;
   a.hkey = hkey;
   a.hcnt = hcnt;
   a.ctab = ctab;
@@ -812,18 +934,18 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   // 2. triangles (the long kernels first)
   const int64_t nhubs = c[kHubs], ntasks = c[kNTasks];
   if (nhubs) {
-    // exact bitmaps; hubs sorted by descending triangle work; tasks of ~kHubTask probes
+    // exact bitmaps; hubs sorted by descending triangle work; tasks of kHubRows rows
     const int64_t words = ceil_div(n, 32);
     uint32_t* bms = ctx.buf("f_bitmaps").as<uint32_t>(nhubs * words);
     int32_t* hub_slot = ctx.buf("f_hub_slot").as<int32_t>(n);
     EFG_CUDA_CHECK(cudaMemsetAsync(bms, 0, nhubs * words * sizeof(uint32_t), s));
-    EFG_LAUNCH(k_hub_bitmaps, nhubs, 1024, 0, s, l_hub, nhubs, P.g.offsets, P.g.nbr, bms, words, hub_slot);
+    EFG_LAUNCH(k_hub_bitmaps, nhubs, 1024, 0, s, L.hub, nhubs, P.g.offsets, P.g.nbr, bms, words, hub_slot);
     int64_t* hw_sorted = hw + nhubs;
     int32_t* hs = ctx.buf("f_hub_sorted").as<int32_t>(nhubs);
-    EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, hw, hw_sorted, l_hub, hs, nhubs, 0, 64, s));
+    EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, hw, hw_sorted, L.hub, hs, nhubs, 0, 64, s));
     EFG_REGION("cub::DeviceRadixSort::SortPairsDescending", s,
                EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(ctx.buf("cub").get(tmp), tmp, hw, hw_sorted,
-                                                                        l_hub, hs, nhubs, 0, 64, s)));
+                                                                        L.hub, hs, nhubs, 0, 64, s)));
     int64_t* hnt = ctx.buf("f_hub_nt").as<int64_t>(nhubs + 1);
     int64_t* tstart = ctx.buf("f_hub_tstart").as<int64_t>(nhubs + 1);
     EFG_LAUNCH(k_hub_ntasks, ceil_div(nhubs + 1, B), B, 0, s, hs, nhubs, P.g.offsets, hnt);
@@ -854,23 +976,17 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     const int sm3 = 16 * kHashMaxDeg;
     EFG_CUDA_CHECK(cudaFuncSetAttribute(k_tri_seed_1024, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 1024));
     EFG_CUDA_CHECK(cudaFuncSetAttribute(k_tri_seed_4096, cudaFuncAttributeMaxDynamicSharedMemorySize, sm3));
-    EFG_LAUNCH(k_tri_seed_4096, c[kTri3], 512, sm3, s, l_tr3, c[kTri3], a);
-    EFG_LAUNCH(k_tri_seed_1024, c[kTri2], 256, 32 * 1024, s, l_tr2, c[kTri2], a);
-    EFG_LAUNCH(k_tri_seed_256, c[kTri1], 128, 32 * 512, s, l_tr1, c[kTri1], a);
-    EFG_LAUNCH(k_tri_warp, ceil_div(c[kTriS], kTriWarps), kTriWarps * 32, 0, s, l_trs, c[kTriS], a);
+    EFG_LAUNCH(k_tri_seed_4096, c[kTr3], 512, sm3, s, L.tr3, c[kTr3], a);
+    EFG_LAUNCH(k_tri_seed_1024, c[kTr2], 256, 32 * 1024, s, L.tr2, c[kTr2], a);
+    EFG_LAUNCH(k_tri_seed_256, c[kTr1], 128, 32 * 512, s, L.tr1, c[kTr1], a);
+    EFG_LAUNCH(k_tri_warp, ceil_div(c[kTrS], kTriWarps), kTriWarps * 32, 0, s, L.trs, c[kTrS], a);
   }
   // 3. chains: warp per row (dv <= 1024), CTA per row above
-  EFG_LAUNCH(k_chain_block, c[kChainB], 256, 0, s, l_chb, c[kChainB], a);
-  EFG_LAUNCH(k_chain_warp, ceil_div(c[kChainS] * 32, B), B, 0, s, l_chs, c[kChainS], a);
-  // 4. stars by |D_v|
-  if (c[kStarB]) {
-    const size_t smem = 8 * (size_t)c[kMaxD];
-    EFG_REQUIRE(smem <= 200 * 1024, "neighbour-degree histogram too wide for shared memory");
-    if (smem > 48 * 1024)
-      EFG_CUDA_CHECK(cudaFuncSetAttribute(k_stars_block, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    EFG_LAUNCH(k_stars_block, c[kStarB], 256, smem, s, l_stb, c[kStarB], a);
-  }
-  EFG_LAUNCH(k_stars_warp, ceil_div(c[kStarS] * 32, B), B, 0, s, l_sts, c[kStarS], a);
+  EFG_LAUNCH(k_chain_block, c[kChB], 256, 0, s, L.chb, c[kChB], a);
+  EFG_LAUNCH(k_chain_warp, ceil_div(c[kChS] * 32, B), B, 0, s, L.chs, c[kChS], a);
+  // 4. stars: warp per seed (dv <= 32, so |D_v| <= 32), CTA per seed above
+  EFG_LAUNCH(k_stars_block, c[kStB], 256, 0, s, L.stb, c[kStB], a);
+  EFG_LAUNCH(k_stars_warp, ceil_div(c[kStS] * 32, B), B, 0, s, L.sts, c[kStS], a);
   // 5. epilogue
   EFG_LAUNCH(k_epilogue, ceil_div(cnt, B), B, 0, s, a, cnt, ef, total, flags, T_out, W_out);
 }

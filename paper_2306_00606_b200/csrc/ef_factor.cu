@@ -228,6 +228,7 @@ __global__ void k_ctab_group(const int32_t* __restrict__ rows, int64_t count, co
 }
 
 // Rows with many distinct degrees: one CTA per row, threads over outputs.
+constexpr int kCtabStage = 2048;
 __global__ void k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __restrict__ offsets,
                              const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey,
                              const int32_t* __restrict__ hcnt, const int32_t* __restrict__ deg,
@@ -235,13 +236,14 @@ __global__ void k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, co
   int64_t r = blockIdx.x;
   if (r >= nrows) return;
   int32_t i = rows[r];
-  int64_t b = offsets[i], e = b + dcnt[i];
-  int32_t di = deg[i];
-  for (int64_t o = b + threadIdx.x; o < e; o += blockDim.x) {
+  const int64_t b = offsets[i];
+  const int D = dcnt[i];
+  const int32_t di = deg[i];
+  for (int64_t o = b + threadIdx.x; o < b + D; o += blockDim.x) {
     int32_t y = hkey[o];
     int64_t base = (int64_t)y + di - 4;
     double acc = 0.0;
-    for (int64_t q = b; q < e; ++q) acc += (double)__ldg(hcnt + q) * __ldg(F + base + __ldg(hkey + q));
+    for (int64_t q = b; q < b + D; ++q) acc += (double)__ldg(hcnt + q) * __ldg(F + base + __ldg(hkey + q));
     ctab[o] = acc - __ldg(F + base + y);
   }
 }
@@ -359,6 +361,32 @@ __global__ void __launch_bounds__(256) k_stars_block(const int32_t* __restrict__
   const int32_t* __restrict__ sc = a.hcnt + hb;
   const int64_t c = dv - 4;
   double Ws = 0.0;
+  if (D <= kCtabStage) {
+    // staged H_v; warp w takes the row pair (ra, D-1-ra) -- D-1 terms per pair --
+    // and its lanes walk rb > ra, so a warp's F gathers F[c + x_ra + x_rb] are nearby
+    __shared__ int2 sh[kCtabStage];
+    for (int t = threadIdx.x; t < D; t += 256) sh[t] = make_int2(sk[t], sc[t]);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int pr = w; pr < (D + 1) / 2; pr += 8) {
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int ra = side ? D - 1 - pr : pr;
+        if (side && ra == pr) break;
+        const int2 xa = sh[ra];
+        const int64_t ha = xa.y;
+        const int64_t base = c + xa.x;
+        if (lane == 0 && ha > 1) Ws += (double)(ha * (ha - 1) / 2) * __ldg(a.F + base + xa.x);
+        for (int rb = ra + 1 + lane; rb < D; rb += 32) {
+          const int2 xb = sh[rb];
+          Ws += (double)(ha * xb.y) * __ldg(a.F + base + xb.x);
+        }
+      }
+    }
+    Ws = block_sum<256>(Ws, red);
+    if (threadIdx.x == 0) a.Ws[v - a.seed_lo] = 2.0 * Ws;
+    return;
+  }
   // row ra pairs with rb > ra; rows dealt from both ends for balance
   for (int r = threadIdx.x; r < D; r += 256) {
     const int ra = (r & 1) ? D - 1 - (r >> 1) : (r >> 1);

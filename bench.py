@@ -36,6 +36,14 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+METRICS = {
+    "rmat22": "EF seeds/sec, full-graph Expected Force (R-MAT scale-22, 44M edges)",
+    "er1m": "EF seeds/sec, full-graph Expected Force (Erdos-Renyi n=1M, avg degree 16)",
+    "ws4m": "EF seeds/sec, full-graph Expected Force (Watts-Strogatz n=4M, k=20, p=0.05)",
+    "chunglu": "EF seeds/sec, full-graph Expected Force (Chung-Lu gamma=2.1, n=2^20)",
+    "ba2000": "EF seeds/sec, full-graph Expected Force (Barabasi-Albert n=2000, m=3)",
+}
+
 CONFIGS = {
     # name: (description, builder kwargs)
     "rmat22": "R-MAT scale-22 avg-degree 21 seed 0 (reference generate_rmat), ~44M undirected edges",
@@ -239,7 +247,7 @@ def run_reference(args):
     t_full = float(np.median(times))
     value = n / t_full
     line = {
-        "metric": "EF seeds/sec, full-graph Expected Force (R-MAT scale-22, 44M edges)",
+        "metric": METRICS[args.config],
         "value": value, "unit": "seeds/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": t_full * 1e3, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64+int64", "data": "synthetic", "impl": "reference",
@@ -420,7 +428,7 @@ def main():
         cpu = {"value": n / t_full, "unit": "seeds/s", "cores": threads, "kind": "port",
                "sample": f"{sample}; {sample_s:.1f} s of CPU work, extrapolated by work ratio to {t_full:.0f} s"}
     line = {
-        "metric": "EF seeds/sec, full-graph Expected Force (R-MAT scale-22, 44M edges)",
+        "metric": METRICS[args.config],
         "value": value, "unit": "seeds/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64+int64", "data": "synthetic",

@@ -383,7 +383,9 @@ def main():
         t_e2e = float(np.median(times))
         e2e = {"value": n / t_e2e, "unit": "seeds/s", "h2d_bytes_per_step": int(r.stats["h2d_bytes"]),
                "d2h_bytes_per_step": int(r.stats["d2h_bytes"]), "ms_per_step": t_e2e * 1e3,
-               "ms_h2d": r.stats["ms_h2d"], "ms_d2h": r.stats["ms_d2h"]}
+               "ms_h2d": r.stats["ms_h2d"], "ms_d2h": r.stats["ms_d2h"], "ms_device_events": r.stats["ms_device"],
+               "ms_prepare": r.stats["ms_prepare"], "ms_enumerate": r.stats["ms_enumerate"],
+               "ms_wall_all": [round(t * 1e3, 2) for t in times]}
         # parity spot check of the timed output against the e2e output
         assert np.array_equal(out[0].cpu().numpy(), r.ef)
 

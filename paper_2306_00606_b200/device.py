@@ -42,6 +42,16 @@ def _ctx_for(t):
     return _native.context(t.device.index if t.device.index is not None else 0)
 
 
+# torch reports its default (legacy) stream as handle 0; the C ABI reads NULL
+# as "use the library's own stream", so name the legacy stream explicitly.
+_CUDA_STREAM_LEGACY = 0x1
+
+
+def _bind_stream(ctx, stream) -> None:
+    h = stream.cuda_stream or _CUDA_STREAM_LEGACY
+    _native.check(_native.lib().efg_set_stream(ctx.handle, ctypes.c_void_p(h)))
+
+
 def ef_range(dg: DeviceGraph, lo: int, hi: int, out_ef, out_total, out_flags, engine="factorized",
              T=None, W=None, stats: bool = False, stream=None):
     """EF of seeds [lo, hi) into device tensors (index = seed - lo).  Returns a
@@ -52,7 +62,7 @@ def ef_range(dg: DeviceGraph, lo: int, hi: int, out_ef, out_total, out_flags, en
     ctx = _ctx_for(dg.offsets)
     L = _native.lib()
     s = torch.cuda.current_stream(dg.offsets.device) if stream is None else stream
-    _native.check(L.efg_set_stream(ctx.handle, ctypes.c_void_p(s.cuda_stream)))
+    _bind_stream(ctx, s)
     st = _native.Stats() if stats else None
     _native.check(L.efg_expected_force_device(
         ctx.handle, _dptr(dg.offsets), _dptr(dg.neighbors), dg.n, int(lo), int(hi), _engine_code(engine),
@@ -67,7 +77,7 @@ def shard_bounds(dg: DeviceGraph, parts: int, engine="factorized") -> np.ndarray
 
     ctx = _ctx_for(dg.offsets)
     L = _native.lib()
-    _native.check(L.efg_set_stream(ctx.handle, ctypes.c_void_p(torch.cuda.current_stream(dg.offsets.device).cuda_stream)))
+    _bind_stream(ctx, torch.cuda.current_stream(dg.offsets.device))
     out = np.zeros(parts + 1, np.int64)
     _native.check(L.efg_shard_bounds(ctx.handle, _dptr(dg.offsets), _dptr(dg.neighbors), dg.n,
                                      _engine_code(engine), int(parts), _native.ptr(out)))
@@ -80,7 +90,7 @@ def topk(ef_tensor, k: int) -> np.ndarray:
 
     ctx = _ctx_for(ef_tensor)
     L = _native.lib()
-    _native.check(L.efg_set_stream(ctx.handle, ctypes.c_void_p(torch.cuda.current_stream(ef_tensor.device).cuda_stream)))
+    _bind_stream(ctx, torch.cuda.current_stream(ef_tensor.device))
     k = min(int(k), ef_tensor.numel())
     out = np.empty(k, np.int64)
     if k:

@@ -10,12 +10,14 @@
 //   T = sum w d (exact, int64), mass = sum w, W = sum w d ln d,
 //   EF = ln T - W/T  (expected_force.py:322-324).
 // The clusters are not visited one by one.  They are summed in classes:
-//   * stars without the triangle term depend on (di, dj) only, so they are a
-//     self-convolution of v's neighbour-degree histogram H_v (|D_v|^2 terms
-//     instead of C(dv,2));
 //   * chains through i without the triangle term depend on v only through
 //     dv, so C_i(y) = sum_x H_i(x) F(y+di-4+x) - F(2y+di-4) is tabulated
 //     once per (i, distinct neighbour degree y) and looked up by each seed;
+//   * stars without the triangle term depend on (di, dj) only: a
+//     self-convolution of v's neighbour-degree histogram H_v, which equals
+//     v's own chain table weighted by H_v:
+//       2[sum_{a<b} h_a h_b F(dv-4+x_a+x_b) + sum_a C(h_a,2) F(dv-4+2x_a)]
+//         = sum_b h_b C_v(x_b)                    (|D_v| terms, no pair loop);
 //   * a cluster whose three nodes form a triangle has degree D-2 instead of
 //     D = dv+di+dj-4; each triangle at v carries star weight 2 and two chains
 //     (v->i->j, v->j->i), so the correction is 4 (F(D-2) - F(D)) per triangle,
@@ -292,13 +294,16 @@ __global__ void k_chain_warp(const int32_t* __restrict__ seeds, int64_t count, F
   const int32_t v = seeds[q];
   const int64_t b = a.offsets[v], e = a.offsets[v + 1];
   int64_t Tc = 0;
-  double Wc = 0.0;
+  double Wc = 0.0, Ws = 0.0;
   for (int64_t p = b + lane; p < e; p += 32) chain_slot(a, p, e - b, Tc, Wc);
+  for (int64_t h = b + lane; h < b + a.dcnt[v]; h += 32) Ws += (double)a.hcnt[h] * a.ctab[h];
   Tc = warp_sum(Tc);
   Wc = warp_sum(Wc);
+  Ws = warp_sum(Ws);
   if (lane == 0) {
     a.Tc[v - a.seed_lo] = Tc;
     a.Wc[v - a.seed_lo] = Wc;
+    a.Ws[v - a.seed_lo] = Ws;
   }
 }
 
@@ -310,94 +315,17 @@ __global__ void __launch_bounds__(256) k_chain_block(const int32_t* __restrict__
   const int32_t v = seeds[q];
   const int64_t b = a.offsets[v], e = a.offsets[v + 1];
   int64_t Tc = 0;
-  double Wc = 0.0;
+  double Wc = 0.0, Ws = 0.0;
   for (int64_t p = b + threadIdx.x; p < e; p += 256) chain_slot(a, p, e - b, Tc, Wc);
+  for (int64_t h = b + threadIdx.x; h < b + a.dcnt[v]; h += 256) Ws += (double)a.hcnt[h] * a.ctab[h];
   Tc = block_sum<256>(Tc, red_i);
   Wc = block_sum<256>(Wc, red_d);
+  Ws = block_sum<256>(Ws, red_d);
   if (threadIdx.x == 0) {
     a.Tc[v - a.seed_lo] = Tc;
     a.Wc[v - a.seed_lo] = Wc;
+    a.Ws[v - a.seed_lo] = Ws;
   }
-}
-
-// Stars over H_v, warp per seed (|D_v| <= 32):
-//   Ws = 2 [ sum_{a<b} h_a h_b F(dv-4+x_a+x_b) + sum_a C(h_a,2) F(dv-4+2x_a) ]
-__global__ void k_stars_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
-  const int lane = threadIdx.x & 31;
-  int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (q >= count) return;
-  const int32_t v = seeds[q];
-  const int64_t dv = a.offsets[v + 1] - a.offsets[v];
-  const int64_t hb = a.offsets[v];
-  const int D = a.dcnt[v];
-  int32_t xa = 0;
-  int64_t ha = 0;
-  if (lane < D) {
-    xa = a.hkey[hb + lane];
-    ha = a.hcnt[hb + lane];
-  }
-  const int64_t c = dv - 4;
-  double Ws = 0.0;
-  for (int bb = 1; bb < D; ++bb) {
-    int32_t xb = __shfl_sync(0xffffffffu, xa, bb);
-    int64_t hbv = __shfl_sync(0xffffffffu, ha, bb);
-    if (lane < bb) Ws += (double)(ha * hbv) * __ldg(a.F + c + xa + xb);
-  }
-  if (lane < D && ha > 1) Ws += (double)(ha * (ha - 1) / 2) * __ldg(a.F + c + 2 * xa);
-  Ws = warp_sum(Ws);
-  if (lane == 0) a.Ws[v - a.seed_lo] = 2.0 * Ws;
-}
-
-// Stars for |D_v| > 32: CTA per seed, H_v staged in shared memory.
-__global__ void __launch_bounds__(256) k_stars_block(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
-  __shared__ double red[8];
-  const int64_t q = blockIdx.x;
-  if (q >= count) return;
-  const int32_t v = seeds[q];
-  const int64_t hb = a.offsets[v];
-  const int64_t dv = a.offsets[v + 1] - hb;
-  const int D = a.dcnt[v];
-  const int32_t* __restrict__ sk = a.hkey + hb;
-  const int32_t* __restrict__ sc = a.hcnt + hb;
-  const int64_t c = dv - 4;
-  double Ws = 0.0;
-  if (D <= kCtabStage) {
-    // staged H_v; warp w takes the row pair (ra, D-1-ra) -- D-1 terms per pair --
-    // and its lanes walk rb > ra, so a warp's F gathers F[c + x_ra + x_rb] are nearby
-    __shared__ int2 sh[kCtabStage];
-    for (int t = threadIdx.x; t < D; t += 256) sh[t] = make_int2(sk[t], sc[t]);
-    __syncthreads();
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int pr = w; pr < (D + 1) / 2; pr += 8) {
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int ra = side ? D - 1 - pr : pr;
-        if (side && ra == pr) break;
-        const int2 xa = sh[ra];
-        const int64_t ha = xa.y;
-        const int64_t base = c + xa.x;
-        if (lane == 0 && ha > 1) Ws += (double)(ha * (ha - 1) / 2) * __ldg(a.F + base + xa.x);
-        for (int rb = ra + 1 + lane; rb < D; rb += 32) {
-          const int2 xb = sh[rb];
-          Ws += (double)(ha * xb.y) * __ldg(a.F + base + xb.x);
-        }
-      }
-    }
-    Ws = block_sum<256>(Ws, red);
-    if (threadIdx.x == 0) a.Ws[v - a.seed_lo] = 2.0 * Ws;
-    return;
-  }
-  // row ra pairs with rb > ra; rows dealt from both ends for balance
-  for (int r = threadIdx.x; r < D; r += 256) {
-    const int ra = (r & 1) ? D - 1 - (r >> 1) : (r >> 1);
-    const int64_t ha = sc[ra];
-    const int64_t base = c + sk[ra];
-    double acc = ha > 1 ? (double)(ha * (ha - 1) / 2) * __ldg(a.F + base + sk[ra]) : 0.0;
-    for (int rb = ra + 1; rb < D; ++rb) acc += (double)(ha * sc[rb]) * __ldg(a.F + base + sk[rb]);
-    Ws += acc;
-  }
-  Ws = block_sum<256>(Ws, red);
-  if (threadIdx.x == 0) a.Ws[v - a.seed_lo] = 2.0 * Ws;
 }
 
 // ------------------------------------------------------------- triangles
@@ -810,11 +738,10 @@ struct Lists {
   int32_t *hw, *hs, *hb, *hl;     // histogram rows: d <= 32, <= 256, <= 2048, > 2048 (all nodes)
   int32_t *cg, *cb;               // chain tables: d <= 64, > 64 (all nodes)
   int32_t *chs, *chb;             // chain sums: seeds dv <= 1024, > 1024
-  int32_t *sts, *stb;             // stars: dv <= 32, > 32
   int32_t *trs, *tr1, *tr2, *tr3, *hub;  // triangles
 };
 enum Slot {
-  kHW, kHS, kHB, kHL, kCG, kCB, kChS, kChB, kStS, kStB, kTrS, kTr1, kTr2, kTr3, kHubs, kNTasks, kNSlots
+  kHW, kHS, kHB, kHL, kCG, kCB, kChS, kChB, kTrS, kTr1, kTr2, kTr3, kHubs, kNTasks, kNSlots
 };
 constexpr int64_t kHistWarpMax = 32, kHistBlockMax = kHistThreads * kHistItems, kCtabGroupMax = 64;
 
@@ -839,8 +766,6 @@ static Lists make_lists(Context& ctx, const Prepared& P, SeedRange r, int64_t* c
   select_seeds(ctx, all, DegRange{off, kCtabGroupMax, INT64_MAX}, L.cb, cdev + kCB);
   L.chs = list("f_l_chs", cnt);
   L.chb = list("f_l_chb", cnt);
-  L.sts = list("f_l_sts", cnt);
-  L.stb = list("f_l_stb", cnt);
   L.trs = list("f_l_trs", cnt);
   L.tr1 = list("f_l_tr1", cnt);
   L.tr2 = list("f_l_tr2", cnt);
@@ -848,8 +773,6 @@ static Lists make_lists(Context& ctx, const Prepared& P, SeedRange r, int64_t* c
   L.hub = list("f_l_hub", cnt);
   select_seeds(ctx, r, DegRange{off, -1, 1024}, L.chs, cdev + kChS);
   select_seeds(ctx, r, DegRange{off, 1024, INT64_MAX}, L.chb, cdev + kChB);
-  select_seeds(ctx, r, DegRange{off, -1, 32}, L.sts, cdev + kStS);
-  select_seeds(ctx, r, DegRange{off, 32, INT64_MAX}, L.stb, cdev + kStB);
   select_seeds(ctx, r, DegRange{off, -1, 32}, L.trs, cdev + kTrS);
   select_seeds(ctx, r, DegRange{off, 32, 256}, L.tr1, cdev + kTr1);
   select_seeds(ctx, r, DegRange{off, 256, 1024}, L.tr2, cdev + kTr2);
@@ -1009,12 +932,9 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     EFG_LAUNCH(k_tri_seed_256, c[kTr1], 128, 32 * 512, s, L.tr1, c[kTr1], a);
     EFG_LAUNCH(k_tri_warp, ceil_div(c[kTrS], kTriWarps), kTriWarps * 32, 0, s, L.trs, c[kTrS], a);
   }
-  // 3. chains: warp per row (dv <= 1024), CTA per row above
+  // 3. chains (and stars, from the seed's own chain table): warp per row (dv <= 1024), CTA per row above
   EFG_LAUNCH(k_chain_block, c[kChB], 256, 0, s, L.chb, c[kChB], a);
   EFG_LAUNCH(k_chain_warp, ceil_div(c[kChS] * 32, B), B, 0, s, L.chs, c[kChS], a);
-  // 4. stars: warp per seed (dv <= 32, so |D_v| <= 32), CTA per seed above
-  EFG_LAUNCH(k_stars_block, c[kStB], 256, 0, s, L.stb, c[kStB], a);
-  EFG_LAUNCH(k_stars_warp, ceil_div(c[kStS] * 32, B), B, 0, s, L.sts, c[kStS], a);
   // 5. epilogue
   EFG_LAUNCH(k_epilogue, ceil_div(cnt, B), B, 0, s, a, cnt, ef, total, flags, T_out, W_out);
 }

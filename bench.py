@@ -86,7 +86,7 @@ def fingerprint(g):
 
 # seed classes of the factorized engine's triangle kernels (csrc/ef_factor.cu): (kernel, lo < dv <= hi)
 TRI_CLASSES = [("k_tri_warp", 0, 32), ("k_tri_seed_256", 32, 256), ("k_tri_seed_1024", 256, 1024),
-               ("k_tri_seed_4096", 1024, 4096), ("k_tri_task", 4096, 1 << 40)]
+               ("k_tri_seed_4096", 1024, 4096), ("k_tri_hub", 4096, 1 << 40)]
 
 
 def kernel_bytes_model(offsets, neighbors):

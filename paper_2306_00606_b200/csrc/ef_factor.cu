@@ -48,8 +48,10 @@ struct FArgs {
   const double* G;         // G[S] = F(S-6) - F(S-4): triangle correction per unit weight
   const int64_t* ps;       // [2m] start of Adj+(nbr[e]) in adjp
   const int32_t* pc;       // [2m] |Adj+(nbr[e])|
-  const int32_t* adjj;     // oriented adjacency Adj+ (ascending j per row)
+  const int32_t* adjj;     // oriented adjacency Adj+ as rank labels
   const int32_t* deg;
+  const int32_t* rank_of;      // node -> rank label
+  const int32_t* deg_by_rank;  // rank label -> degree
   const int32_t* dcnt;     // |D_i|: H_i = hkey/hcnt[offsets[i], offsets[i] + dcnt[i])
   const int32_t* hkey;
   const int32_t* hcnt;
@@ -471,7 +473,7 @@ k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   SmemMap<32, true> map{sK[w], sD[w], nullptr};
   map.clear(lane, 32);
   __syncwarp();
-  if (lane < dv) map.insert(a.nbr[ob + lane], a.nd[ob + lane]);
+  if (lane < dv) map.insert(__ldg(a.rank_of + a.nbr[ob + lane]), a.nd[ob + lane]);
   __syncwarp();
   int64_t tri = 0;
   double Wt = 0.0;
@@ -497,10 +499,10 @@ k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   const int32_t v = seeds[qs];
   const int64_t ob = a.offsets[v];
   const int dv = (int)(a.offsets[v + 1] - ob);
-  SmemMap<NB, WITH_DEG> map{dyn4, reinterpret_cast<int32_t*>(dyn4 + NB), a.deg};
+  SmemMap<NB, WITH_DEG> map{dyn4, reinterpret_cast<int32_t*>(dyn4 + NB), a.deg_by_rank};
   map.clear(threadIdx.x, THREADS);
   __syncthreads();
-  for (int x = threadIdx.x; x < dv; x += THREADS) map.insert(a.nbr[ob + x], a.nd[ob + x]);
+  for (int x = threadIdx.x; x < dv; x += THREADS) map.insert(__ldg(a.rank_of + a.nbr[ob + x]), a.nd[ob + x]);
   __syncthreads();
   int64_t tri = 0;
   double Wt = 0.0;
@@ -522,25 +524,26 @@ constexpr int kHubThreads = 1024;
 constexpr uint32_t kFilterWords = 48 * 1024;            // 192 KB of shared memory
 constexpr uint32_t kFilterBits = kFilterWords * 32;
 
+// Membership over rank labels: probe targets j come from Adj+ lists, so they
+// outrank a neighbour of the hub and are mostly high-degree nodes with small
+// labels.  Labels < kFilterBits are answered exactly by the shared-memory
+// bitmap; larger labels (rare) read the hub's global bitmap.
 struct HubMap {
-  const uint32_t* filt;  // shared
-  const uint32_t* bm;    // global exact bitmap
-  const int32_t* deg;
-  __device__ __forceinline__ static uint32_t fbit(int32_t j) {
-    return (uint32_t)(((uint64_t)((uint32_t)j * 2654435761u) * kFilterBits) >> 32);
-  }
+  const uint32_t* sbm;   // shared: bits of labels < kFilterBits
+  const uint32_t* bm;    // global exact bitmap over all labels
+  const int32_t* deg;    // degree by rank label
   static constexpr bool kPhased = true;  // global loads: issue each phase's loads together
   __device__ __forceinline__ int32_t degree(int32_t j) const { return probe(j) >= 0 ? finish(j, 0) : -1; }
-  // phase 1: shared-memory filter
+  // phase 1: shared bitmap (exact), or "ask global" for large labels
   __device__ __forceinline__ int32_t probe(int32_t j) const {
-    const uint32_t b = fbit(j);
-    return ((filt[b >> 5] >> (b & 31)) & 1u) ? 0 : -1;
+    if ((uint32_t)j < kFilterBits) return ((sbm[j >> 5] >> (j & 31)) & 1u) ? 0 : -1;
+    return 1;
   }
-  // phase 2: exact bitmap word and degree fetched together
-  __device__ __forceinline__ int32_t finish(int32_t j, int32_t) const {
-    const uint32_t w = __ldg(bm + (j >> 5));
+  // phase 2: degree (and, for large labels, the exact bit) fetched together
+  __device__ __forceinline__ int32_t finish(int32_t j, int32_t tag) const {
     const int32_t d = __ldg(deg + j);
-    return ((w >> (j & 31)) & 1u) ? d : -1;
+    if (tag == 0) return d;
+    return ((__ldg(bm + (j >> 5)) >> (j & 31)) & 1u) ? d : -1;
   }
 };
 
@@ -571,11 +574,11 @@ k_tri_hub(HubTasks tk, int64_t ntasks, const uint32_t* __restrict__ bitmaps, int
   for (uint32_t k = threadIdx.x; k < kFilterWords; k += kHubThreads) filt[k] = 0u;
   __syncthreads();
   for (int x = threadIdx.x; x < dv; x += kHubThreads) {
-    const uint32_t b = HubMap::fbit(a.nbr[ob + x]);
-    atomicOr(&filt[b >> 5], 1u << (b & 31));
+    const int32_t r = __ldg(a.rank_of + a.nbr[ob + x]);
+    if ((uint32_t)r < kFilterBits) atomicOr(&filt[r >> 5], 1u << (r & 31));
   }
   __syncthreads();
-  HubMap map{filt, bitmaps + (int64_t)hub_slot[v] * words, a.deg};
+  HubMap map{filt, bitmaps + (int64_t)hub_slot[v] * words, a.deg_by_rank};
   int64_t tri = 0;
   double Wt = 0.0;
   const int x0 = tk.x0[t];
@@ -646,15 +649,15 @@ __global__ void k_hub_merge(const int32_t* __restrict__ hubs, int64_t nhubs, con
 }
 
 __global__ void k_hub_bitmaps(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ offsets,
-                              const int32_t* __restrict__ nbr, uint32_t* __restrict__ bitmaps, int64_t words,
-                              int32_t* __restrict__ hub_slot) {
+                              const int32_t* __restrict__ nbr, const int32_t* __restrict__ rank_of,
+                              uint32_t* __restrict__ bitmaps, int64_t words, int32_t* __restrict__ hub_slot) {
   int64_t h = blockIdx.x;
   if (h >= nhubs) return;
   int32_t v = hubs[h];
   if (threadIdx.x == 0) hub_slot[v] = (int32_t)h;
   uint32_t* bm = bitmaps + h * words;
   for (int64_t p = offsets[v] + threadIdx.x; p < offsets[v + 1]; p += blockDim.x) {
-    int32_t i = nbr[p];
+    int32_t i = rank_of[nbr[p]];
     atomicOr(bm + (i >> 5), 1u << (i & 31));
   }
 }
@@ -872,6 +875,8 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   a.pc = P.pc;
   a.adjj = P.adjj;
   a.deg = P.deg;
+  a.rank_of = P.rank_of;
+  a.deg_by_rank = P.deg_by_rank;
   a.dcnt = dcnt;
   a.hkey = hkey;
   a.hcnt = hcnt;
@@ -890,7 +895,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     uint32_t* bms = ctx.buf("f_bitmaps").as<uint32_t>(nhubs * words);
     int32_t* hub_slot = ctx.buf("f_hub_slot").as<int32_t>(n);
     EFG_CUDA_CHECK(cudaMemsetAsync(bms, 0, nhubs * words * sizeof(uint32_t), s));
-    EFG_LAUNCH(k_hub_bitmaps, nhubs, 1024, 0, s, L.hub, nhubs, P.g.offsets, P.g.nbr, bms, words, hub_slot);
+    EFG_LAUNCH(k_hub_bitmaps, nhubs, 1024, 0, s, L.hub, nhubs, P.g.offsets, P.g.nbr, P.rank_of, bms, words, hub_slot);
     int64_t* hw_sorted = hw + nhubs;
     int32_t* hs = ctx.buf("f_hub_sorted").as<int32_t>(nhubs);
     EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, hw, hw_sorted, L.hub, hs, nhubs, 0, 64, s));

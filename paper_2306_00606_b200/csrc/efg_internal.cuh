@@ -73,7 +73,9 @@ struct Prepared {
   int64_t ftab_len = 0;
   // degree-ordered orientation: j in Adj+(i) iff (d_j, j) > (d_i, i)
   int64_t* offp = nullptr;      // [n+1]
-  int32_t* adjj = nullptr;      // [m]  Adj+ rows, ascending j
+  int32_t* adjj = nullptr;      // [m]  Adj+ rows as rank labels
+  int32_t* rank_of = nullptr;   // [n]  position in descending (degree, id) order
+  int32_t* deg_by_rank = nullptr;  // [n]
   int64_t* ps = nullptr;        // [2m] per slot (v->i): offp[i]
   int32_t* pc = nullptr;        // [2m] per slot (v->i): |Adj+(i)|
 };

@@ -70,10 +70,10 @@ __global__ void k_row_sums(const int64_t* __restrict__ offsets, const int32_t* _
   }
 }
 
-// Warp per row: ordered compaction of Adj+(v) (ascending j).
+// Warp per row: ordered compaction of Adj+(v), stored as rank labels.
 __global__ void k_fill_adjp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
                             const int32_t* __restrict__ nd, int64_t n, const int64_t* __restrict__ offp,
-                            int32_t* __restrict__ adjj) {
+                            const int32_t* __restrict__ rank_of, int32_t* __restrict__ adjj) {
   const int lane = threadIdx.x & 31;
   int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (v >= n) return;
@@ -90,7 +90,7 @@ __global__ void k_fill_adjp(const int64_t* __restrict__ offsets, const int32_t* 
       take = ranks_above(dj, j, dv, (int32_t)v);
     }
     unsigned mask = __ballot_sync(0xffffffffu, take);
-    if (take) adjj[out + __popc(mask & ((1u << lane) - 1))] = j;
+    if (take) adjj[out + __popc(mask & ((1u << lane) - 1))] = __ldg(rank_of + j);
     out += __popc(mask);
   }
 }
@@ -104,6 +104,26 @@ __global__ void k_slot_plus(const int32_t* __restrict__ nbr, int64_t m2, const i
   const int64_t a = offp[i];
   ps[e] = a;
   pc[e] = (int32_t)(offp[i + 1] - a);
+}
+
+// Rank label of each node: its position in descending (degree, id) order, so
+// j in Adj+(i) iff rank(j) < rank(i) and the frequent probe targets (high
+// degree) get small labels.
+__global__ void k_rank_keys(const int32_t* __restrict__ deg, int64_t n, int32_t dmax, uint64_t* __restrict__ key,
+                            int32_t* __restrict__ val) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  key[v] = ((uint64_t)(uint32_t)(dmax - deg[v]) << 32) | (uint32_t)(n - 1 - v);
+  val[v] = (int32_t)v;
+}
+
+__global__ void k_rank_scatter(const int32_t* __restrict__ by_rank, int64_t n, const int32_t* __restrict__ deg,
+                               int32_t* __restrict__ rank_of, int32_t* __restrict__ deg_by_rank) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int32_t v = by_rank[r];
+  rank_of[v] = (int32_t)r;
+  deg_by_rank[r] = deg[v];
 }
 
 struct Choose2 {
@@ -151,8 +171,22 @@ void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P)
   EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, dplus64, P.offp, n + 1, s));
   EFG_CUDA_CHECK(cudaMemsetAsync(dplus64 + n, 0, sizeof(int64_t), s));
   EFG_REGION("cub::DeviceScan::ExclusiveSum", s, EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dplus64, P.offp, n + 1, s)));
+  {
+    uint64_t* key = ctx.buf("rank_key").as<uint64_t>(2 * n);
+    int32_t* val = ctx.buf("rank_val").as<int32_t>(2 * n);
+    EFG_LAUNCH(k_rank_keys, ceil_div(n, B), B, 0, s, P.deg, n, dmax, key, val);
+    int bits = 32;
+    while (bits < 64 && (uint64_t(1) << (bits - 32)) <= (uint64_t)dmax) ++bits;
+    EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, key + n, val, val + n, n, 0, bits, s));
+    EFG_REGION("cub::DeviceRadixSort::SortPairs", s,
+               EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(ctx.buf("cub").get(tmp), tmp, key, key + n, val,
+                                                              val + n, n, 0, bits, s)));
+    P.rank_of = ctx.buf("rank_of").as<int32_t>(n);
+    P.deg_by_rank = ctx.buf("deg_by_rank").as<int32_t>(n);
+    EFG_LAUNCH(k_rank_scatter, ceil_div(n, B), B, 0, s, val + n, n, P.deg, P.rank_of, P.deg_by_rank);
+  }
   P.adjj = ctx.buf("adjj").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);
-  EFG_LAUNCH(k_fill_adjp, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.offp, P.adjj);
+  EFG_LAUNCH(k_fill_adjp, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.offp, P.rank_of, P.adjj);
   P.ps = ctx.buf("ps").as<int64_t>(m2);
   P.pc = ctx.buf("pc").as<int32_t>(m2);
   EFG_LAUNCH(k_slot_plus, ceil_div(m2, B), B, 0, s, g.nbr, m2, P.offp, P.ps, P.pc);

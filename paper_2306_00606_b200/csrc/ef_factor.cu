@@ -49,6 +49,7 @@ struct FArgs {
   const int64_t* ps;       // [2m] start of Adj+(nbr[e]) in adjp
   const int32_t* pc;       // [2m] |Adj+(nbr[e])|
   const int32_t* adjj;     // oriented adjacency Adj+ as rank labels
+  const int32_t* adjd;     // degree of each Adj+ entry
   const int32_t* deg;
   const int32_t* rank_of;      // node -> rank label
   const int32_t* deg_by_rank;  // rank label -> degree
@@ -416,12 +417,17 @@ __device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restric
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) j[u] = p + 32 * u < p1 ? __ldg(row + p + 32 * u) : -1;
     if constexpr (Map::kPhased) {
-      int32_t tag[kUnroll];
+      // the entry's degree streams alongside its label (adjd), so a hit needs
+      // only the G gather; labels past the shared bitmap check the global one
+      int32_t tag[kUnroll], dd[kUnroll];
       double g[kUnroll];
+      const int32_t* rowd = a.adjd + (row - a.adjj);
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) dd[u] = j[u] >= 0 ? __ldg(rowd + p + 32 * u) : 0;
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) tag[u] = j[u] >= 0 ? map.probe(j[u]) : -1;
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) dj[u] = tag[u] >= 0 ? map.finish(j[u], tag[u]) : -1;
+      for (int u = 0; u < kUnroll; ++u) dj[u] = tag[u] >= 0 ? map.finish(j[u], tag[u], dd[u]) : -1;
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) g[u] = dj[u] >= 0 ? __ldg(a.G + s0 + dj[u]) : 0.0;
 #pragma unroll
@@ -533,15 +539,13 @@ struct HubMap {
   const uint32_t* bm;    // global exact bitmap over all labels
   const int32_t* deg;    // degree by rank label
   static constexpr bool kPhased = true;  // global loads: issue each phase's loads together
-  __device__ __forceinline__ int32_t degree(int32_t j) const { return probe(j) >= 0 ? finish(j, 0) : -1; }
   // phase 1: shared bitmap (exact), or "ask global" for large labels
   __device__ __forceinline__ int32_t probe(int32_t j) const {
     if ((uint32_t)j < kFilterBits) return ((sbm[j >> 5] >> (j & 31)) & 1u) ? 0 : -1;
     return 1;
   }
-  // phase 2: degree (and, for large labels, the exact bit) fetched together
-  __device__ __forceinline__ int32_t finish(int32_t j, int32_t tag) const {
-    const int32_t d = __ldg(deg + j);
+  // phase 2: large labels check the exact global bit
+  __device__ __forceinline__ int32_t finish(int32_t j, int32_t tag, int32_t d) const {
     if (tag == 0) return d;
     return ((__ldg(bm + (j >> 5)) >> (j & 31)) & 1u) ? d : -1;
   }
@@ -874,6 +878,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   a.ps = P.ps;
   a.pc = P.pc;
   a.adjj = P.adjj;
+  a.adjd = P.adjd;
   a.deg = P.deg;
   a.rank_of = P.rank_of;
   a.deg_by_rank = P.deg_by_rank;

@@ -74,6 +74,7 @@ struct Prepared {
   // degree-ordered orientation: j in Adj+(i) iff (d_j, j) > (d_i, i)
   int64_t* offp = nullptr;      // [n+1]
   int32_t* adjj = nullptr;      // [m]  Adj+ rows as rank labels
+  int32_t* adjd = nullptr;      // [m]  degree of each Adj+ entry
   int32_t* rank_of = nullptr;   // [n]  position in descending (degree, id) order
   int32_t* deg_by_rank = nullptr;  // [n]
   int64_t* ps = nullptr;        // [2m] per slot (v->i): offp[i]

@@ -73,7 +73,8 @@ __global__ void k_row_sums(const int64_t* __restrict__ offsets, const int32_t* _
 // Warp per row: ordered compaction of Adj+(v), stored as rank labels.
 __global__ void k_fill_adjp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
                             const int32_t* __restrict__ nd, int64_t n, const int64_t* __restrict__ offp,
-                            const int32_t* __restrict__ rank_of, int32_t* __restrict__ adjj) {
+                            const int32_t* __restrict__ rank_of, int32_t* __restrict__ adjj,
+                            int32_t* __restrict__ adjd) {
   const int lane = threadIdx.x & 31;
   int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (v >= n) return;
@@ -90,7 +91,11 @@ __global__ void k_fill_adjp(const int64_t* __restrict__ offsets, const int32_t* 
       take = ranks_above(dj, j, dv, (int32_t)v);
     }
     unsigned mask = __ballot_sync(0xffffffffu, take);
-    if (take) adjj[out + __popc(mask & ((1u << lane) - 1))] = __ldg(rank_of + j);
+    if (take) {
+      const int64_t o = out + __popc(mask & ((1u << lane) - 1));
+      adjj[o] = __ldg(rank_of + j);
+      adjd[o] = dj;
+    }
     out += __popc(mask);
   }
 }
@@ -186,7 +191,9 @@ void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P)
     EFG_LAUNCH(k_rank_scatter, ceil_div(n, B), B, 0, s, val + n, n, P.deg, P.rank_of, P.deg_by_rank);
   }
   P.adjj = ctx.buf("adjj").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);
-  EFG_LAUNCH(k_fill_adjp, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.offp, P.rank_of, P.adjj);
+  P.adjd = ctx.buf("adjd").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);
+  EFG_LAUNCH(k_fill_adjp, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.offp, P.rank_of, P.adjj,
+             P.adjd);
   P.ps = ctx.buf("ps").as<int64_t>(m2);
   P.pc = ctx.buf("pc").as<int32_t>(m2);
   EFG_LAUNCH(k_slot_plus, ceil_div(m2, B), B, 0, s, g.nbr, m2, P.offp, P.ps, P.pc);

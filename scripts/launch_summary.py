@@ -40,4 +40,12 @@ for k, t in sorted(tot.items(), key=lambda kv: -kv[1]["ms"]):
           f"{t['dram_bytes']/max(t['ms'],1e-9)/1e6:8.1f}")
 print(f"total {all_ms:.3f} ms over {sum(t['launches'] for t in tot.values())} launches (serialised, cold cache)")
 if out_json:
-    json.dump({k: t["dram_bytes"] / t["launches"] for k, t in tot.items()}, open(out_json, "w"), indent=1)
+    # live-profile names of the templated launches (csrc/ef_factor.cu)
+    alias = {"k_tri_seed<128, 512, 1>": "k_tri_seed_256", "k_tri_seed<256, 1024, 1>": "k_tri_seed_1024",
+             "k_tri_seed<512, 4096, 0>": "k_tri_seed_4096"}
+    out = {}
+    for k, t in tot.items():
+        out[k] = t["dram_bytes"] / t["launches"]
+        if k in alias:
+            out[alias[k]] = out[k]
+    json.dump(out, open(out_json, "w"), indent=1)

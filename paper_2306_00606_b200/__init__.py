@@ -28,6 +28,7 @@ from .expected_force import (
     key_nodes,
     write_ef_csv,
 )
+from .io import load_edge_list, write_edge_list
 from ._native import EFGDeviceError, set_device
 
 __version__ = "0.1.0"

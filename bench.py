@@ -292,7 +292,10 @@ def main():
     # ---- graph: rank 0 builds (host generator + device K1), broadcast to the others
     t0 = time.perf_counter()
     if rank == 0:
-        g = efg.build_graph(raw_edges(args.config))
+        if args.config == "rmat22":  # device sampler, bit-identical to the reference generator
+            g, _ = efg.generate_rmat(efg.RmatParams(scale=22, avg_degree=21, seed=0))
+        else:
+            g = efg.build_graph(raw_edges(args.config))
         meta = [g.n, g.m]
     else:
         meta = [0, 0]

@@ -72,6 +72,16 @@ EFG_API int efg_build_graph(efg_ctx *ctx, const int64_t *edges, int64_t k, int64
 /* Copy the resident CSR out: offsets[n+1], neighbors[2m], orig_ids[n]
  * (the Graph fields of graph.py:34-57). */
 EFG_API int efg_fetch_graph(efg_ctx *ctx, int64_t *offsets, int32_t *neighbors, int64_t *orig_ids);
+/* Device R-MAT sampler, bit-identical to graph.py:204-246 `generate_rmat`
+ * (numpy PCG64 double stream, first-`target`-distinct-code semantics, attempt
+ * cap 20*target).  probs[4] are the quadrant probabilities; pcg_state and
+ * pcg_inc are the 128-bit PCG64 state/increment of np.random.default_rng(seed)
+ * as {low 64 bits, high 64 bits}.  The CSR stays resident like
+ * efg_build_graph's; *truncated = 1 when the cap was hit. */
+EFG_API int efg_rmat_build(efg_ctx *ctx, int32_t scale, int64_t avg_degree, const double *probs,
+                           const uint64_t *pcg_state, const uint64_t *pcg_inc, int32_t *truncated,
+                           int64_t *n_out, int64_t *m_out);
+
 /* Device pointers of the resident CSR (valid until the next build). */
 EFG_API int efg_graph_device(efg_ctx *ctx, const int64_t **d_offsets, const int32_t **d_neighbors,
                      int64_t *n_out, int64_t *m_out);

@@ -32,7 +32,7 @@ EXPORTED = (
     "efg_synchronize", "efg_build_graph", "efg_fetch_graph", "efg_graph_device",
     "efg_expected_force", "efg_expected_force_device", "efg_shard_bounds", "efg_topk",
     "efg_topk_device", "efg_host_alloc", "efg_host_free", "efg_profile_enable", "efg_profile_reset",
-    "efg_profile_report",
+    "efg_profile_report", "efg_rmat_build",
 )
 
 
@@ -106,6 +106,7 @@ def lib():
             "efg_profile_enable": ([p, i32], ctypes.c_int),
             "efg_profile_reset": ([p], ctypes.c_int),
             "efg_profile_report": ([p, ctypes.c_char_p, i64], ctypes.c_int),
+            "efg_rmat_build": ([p, i32, i64, p, p, p, P(i32), P(i64), P(i64)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

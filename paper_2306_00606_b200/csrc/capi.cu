@@ -230,6 +230,19 @@ int efg_build_graph(efg_ctx* ctx, const int64_t* edges, int64_t k, int64_t* n_ou
   });
 }
 
+int efg_rmat_build(efg_ctx* ctx, int32_t scale, int64_t avg_degree, const double* probs, const uint64_t* pcg_state,
+                   const uint64_t* pcg_inc, int32_t* truncated, int64_t* n_out, int64_t* m_out) {
+  if (!probs || !pcg_state || !pcg_inc) return fail(efg::EFG_INVALID, "null R-MAT argument");
+  return guarded(ctx, [&](Context& c) {
+    bool tr = false;
+    efg::rmat_build_device(c, scale, avg_degree, probs, pcg_state, pcg_inc, tr, c.csr);
+    EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    if (truncated) *truncated = tr ? 1 : 0;
+    if (n_out) *n_out = c.csr.n;
+    if (m_out) *m_out = c.csr.m;
+  });
+}
+
 int efg_fetch_graph(efg_ctx* ctx, int64_t* offsets, int32_t* neighbors, int64_t* orig_ids) {
   return guarded(ctx, [&](Context& c) {
     const int64_t n = c.csr.n, m = c.csr.m;

@@ -88,6 +88,10 @@ struct SeedRange {
 // csr_build.cu
 void build_csr_device(Context& ctx, const int64_t* d_edges, int64_t k, DeviceCSR& out);
 
+// rmat.cu -- device R-MAT sampler (bit-identical to the reference generator)
+void rmat_build_device(Context& ctx, int scale, int64_t avg_degree, const double* probs, const uint64_t* state,
+                       const uint64_t* inc, bool& truncated, DeviceCSR& out);
+
 // prep.cu
 void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P);
 

@@ -15,7 +15,6 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
-from .generators import rmat_codes
 
 __all__ = [
     "Graph",
@@ -150,17 +149,24 @@ def _fetch(ctx, n: int, m: int) -> Graph:
 def generate_rmat(params: RmatParams, device: int | None = None) -> tuple[Graph, bool]:
     """R-MAT sample identical to the reference's (graph.py:204-246); returns (graph, truncated).
 
-    The edge set is the first floor(2^N*M/2) distinct non-loop codes of numpy's
-    PCG64 stream (vectorised, generators.rmat_codes), cleaned by K1.
+    Sampled on the GPU (csrc/rmat.cu): numpy PCG64's double stream is
+    reproduced by 128-bit LCG jump-ahead from np.random.default_rng(seed)'s
+    state; the edge set is the first floor(2^N*M/2) distinct non-loop codes of
+    the pair stream, cleaned by K1.  Bit-identical CSR (tests compare the
+    reference's sha256 fingerprints).
     """
-    codes, truncated = rmat_codes(params.scale, params.avg_degree, params.quadrant_probs, params.seed)
-    if codes.size == 0:
-        return _empty_graph(), truncated
-    side = np.int64(1 << params.scale)
-    edges = np.empty((codes.size, 2), dtype=np.int64)
-    edges[:, 0] = codes // side
-    edges[:, 1] = codes % side
-    return build_graph(edges, device=device), truncated
+    st = np.random.default_rng(params.seed).bit_generator.state["state"]
+    mask = (1 << 64) - 1
+    state = np.array([st["state"] & mask, st["state"] >> 64], dtype=np.uint64)
+    inc = np.array([st["inc"] & mask, st["inc"] >> 64], dtype=np.uint64)
+    probs = np.array([float(p) for p in params.quadrant_probs], dtype=np.float64)
+    ctx = _native.context(device)
+    C = _native.ctypes
+    tr, n, m = C.c_int32(), C.c_int64(), C.c_int64()
+    _native.check(_native.lib().efg_rmat_build(ctx.handle, int(params.scale), int(params.avg_degree),
+                                               _native.ptr(probs), _native.ptr(state), _native.ptr(inc),
+                                               C.byref(tr), C.byref(n), C.byref(m)))
+    return _fetch(ctx, n.value, m.value), bool(tr.value)
 
 
 def cluster_count(g) -> int:

@@ -138,3 +138,20 @@ def test_generate_rmat_matches_reference_fingerprints():
             h.update(np.ascontiguousarray(a).tobytes())
         assert h.hexdigest() == fps[key]["sha256"], key
         assert trunc == fps[key]["truncated"]
+
+
+def test_device_rmat_edge_cases():
+    g, trunc = efg.generate_rmat(efg.RmatParams(scale=1, avg_degree=1, quadrant_probs=(1.0, 0.0, 0.0, 0.0), seed=0))
+    assert trunc and g.n == 0
+    g, trunc = efg.generate_rmat(efg.RmatParams(scale=1, avg_degree=1, seed=3))
+    assert g.n <= 2 and g.m <= 1
+    # truncated instances equal the host restatement (all distinct codes of the first cap pairs)
+    from paper_2306_00606_b200 import generators as gen
+    from oracle import graph as OG
+    for params in ((3, 8, 1), (4, 8, 2), (10, 8, 1), (12, 4, 7)):
+        s, m, seed = params
+        g, trunc = efg.generate_rmat(efg.RmatParams(scale=s, avg_degree=m, seed=seed))
+        e, t2 = gen.rmat_edges(s, m, seed=seed)
+        n, mm, off, nb, orig = OG.build_csr(e)
+        assert trunc == t2 and (g.n, g.m) == (n, mm), params
+        assert np.array_equal(g.offsets, off) and np.array_equal(g.neighbors, nb), params

@@ -57,6 +57,7 @@ struct FArgs {
   const int32_t* hkey;
   const int32_t* hcnt;
   const double* ctab;
+  const int4* rowhash;     // bucketed hash of Adj+(i) for |Adj+(i)| >= kRevMin, at bucket 2*offp[i]
   int64_t seed_lo;
   // per-seed partials, index v - seed_lo
   int64_t* Tc;
@@ -233,23 +234,72 @@ __global__ void k_ctab_group(const int32_t* __restrict__ rows, int64_t count, co
 }
 
 // Rows with many distinct degrees: one CTA per row, threads over outputs.
-constexpr int kCtabStage = 2048;
-__global__ void k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __restrict__ offsets,
-                             const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey,
-                             const int32_t* __restrict__ hcnt, const int32_t* __restrict__ deg,
-                             const double* __restrict__ F, double* __restrict__ ctab) {
-  int64_t r = blockIdx.x;
+// H_i is staged in shared memory (counts as doubles) in chunks of
+// kCtabStage entries, and every thread carries up to kCtabOut outputs
+// (y = its own + T, + 2T, ...) so one staged (x, h) pair feeds kCtabOut F
+// gathers + FMAs.  Fixed per-output summation order (deterministic).
+constexpr int kCtabStage = 1024;
+constexpr int kCtabThreads = 128;
+constexpr int kCtabOut = 4;
+
+template <int K>
+__device__ __forceinline__ void ctab_outputs(const int32_t* __restrict__ sx, const double* __restrict__ sh, int nq,
+                                             const int64_t (&base)[kCtabOut], const double* __restrict__ F,
+                                             double (&acc)[kCtabOut]) {
+#pragma unroll 4
+  for (int q = 0; q < nq; ++q) {
+    const int32_t x = sx[q];
+    const double h = sh[q];
+#pragma unroll
+    for (int k = 0; k < K; ++k) acc[k] = fma(h, __ldg(F + base[k] + x), acc[k]);
+  }
+}
+
+__global__ void __launch_bounds__(kCtabThreads)
+k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __restrict__ offsets,
+             const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey, const int32_t* __restrict__ hcnt,
+             const int32_t* __restrict__ deg, const double* __restrict__ F, double* __restrict__ ctab) {
+  __shared__ int32_t sx[kCtabStage];
+  __shared__ double sh[kCtabStage];
+  const int64_t r = blockIdx.x;
   if (r >= nrows) return;
-  int32_t i = rows[r];
+  const int32_t i = rows[r];
   const int64_t b = offsets[i];
   const int D = dcnt[i];
   const int32_t di = deg[i];
-  for (int64_t o = b + threadIdx.x; o < b + D; o += blockDim.x) {
-    int32_t y = hkey[o];
-    int64_t base = (int64_t)y + di - 4;
-    double acc = 0.0;
-    for (int64_t q = b; q < b + D; ++q) acc += (double)__ldg(hcnt + q) * __ldg(F + base + __ldg(hkey + q));
-    ctab[o] = acc - __ldg(F + base + y);
+  constexpr int T = kCtabThreads;
+  for (int o0 = 0; o0 < D; o0 += T * kCtabOut) {
+    const int K = min(kCtabOut, (D - o0 + T - 1) / T);  // block-uniform
+    int64_t base[kCtabOut];
+    int32_t yk[kCtabOut];
+    double acc[kCtabOut];
+#pragma unroll
+    for (int k = 0; k < kCtabOut; ++k) {
+      const int o = o0 + threadIdx.x + k * T;
+      yk[k] = o < D ? hkey[b + o] : hkey[b];  // past-the-end outputs shadow the first one
+      base[k] = (int64_t)yk[k] + di - 4;
+      acc[k] = 0.0;
+    }
+    for (int q0 = 0; q0 < D; q0 += kCtabStage) {
+      const int nq = min(kCtabStage, D - q0);
+      __syncthreads();
+      for (int q = threadIdx.x; q < nq; q += T) {
+        sx[q] = hkey[b + q0 + q];
+        sh[q] = (double)hcnt[b + q0 + q];
+      }
+      __syncthreads();
+      switch (K) {
+        case 1: ctab_outputs<1>(sx, sh, nq, base, F, acc); break;
+        case 2: ctab_outputs<2>(sx, sh, nq, base, F, acc); break;
+        case 3: ctab_outputs<3>(sx, sh, nq, base, F, acc); break;
+        default: ctab_outputs<4>(sx, sh, nq, base, F, acc); break;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kCtabOut; ++k) {
+      const int o = o0 + threadIdx.x + k * T;
+      if (o < D) ctab[b + o] = acc[k] - __ldg(F + base[k] + yk[k]);
+    }
   }
 }
 
@@ -464,7 +514,55 @@ __device__ __forceinline__ void tri_rows(const FArgs& a, int64_t ob, int nrows, 
   }
 }
 
-// dv <= 32: warp per seed (the warp walks the seed's rows one after another).
+// Reverse probing.  A row Adj+(i) much longer than Adj(v) is cheaper to test
+// the other way round: each j in Adj(v) is looked up in a global bucketed
+// hash of Adj+(i) (built once per pass for |Adj+(i)| >= kRevMin, 4 keys per
+// 16-byte bucket, load <= 1/4, located at bucket 2*offp[i]).  A hit is
+// exactly j in Adj+(i), i.e. the same triangle the forward scan would find.
+constexpr int kRevMin = 64;
+constexpr int kRevKappa = 2;
+__device__ __forceinline__ bool use_reverse(int32_t pc, int dv) { return pc >= kRevMin && kRevKappa * dv < pc; }
+
+__device__ __forceinline__ uint32_t rowhash_lg(int32_t pc) { return 32u - __clz(pc - 1); }  // NB = 2^lg >= pc
+
+__device__ __forceinline__ bool rowhash_has(const int4* __restrict__ base, uint32_t lg, int32_t key) {
+  const uint32_t mask = (1u << lg) - 1;
+  uint32_t b = ((uint32_t)key * 2654435761u) >> (32 - lg);
+  while (true) {
+    const int4 q = __ldg(base + b);
+    if (q.x == key || q.y == key || q.z == key || q.w == key) return true;
+    if (q.w == -1) return false;
+    b = (b + 1) & mask;
+  }
+}
+
+// Warp per node with |Adj+(i)| >= kRevMin: clear its buckets, insert its labels.
+__global__ void k_rowhash(const int64_t* __restrict__ offp, const int32_t* __restrict__ adjj, int64_t n,
+                          int4* __restrict__ rowhash) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (i >= n) return;
+  const int64_t p0 = offp[i];
+  const int32_t pc = (int32_t)(offp[i + 1] - p0);
+  if (pc < kRevMin) return;
+  const uint32_t lg = rowhash_lg(pc), nb = 1u << lg;
+  int4* base = rowhash + 2 * p0;
+  for (uint32_t b = lane; b < nb; b += 32) base[b] = make_int4(-1, -1, -1, -1);
+  __syncwarp();
+  int32_t* flat = reinterpret_cast<int32_t*>(base);
+  for (int32_t p = lane; p < pc; p += 32) {
+    const int32_t key = adjj[p0 + p];
+    for (uint32_t b = (key * 2654435761u) >> (32 - lg);; b = (b + 1) & (nb - 1)) {
+      int k = 0;
+      for (; k < 4; ++k)
+        if (atomicCAS(&flat[4 * b + k], -1, key) == -1) break;
+      if (k < 4) break;
+    }
+  }
+}
+
+// dv <= 32: warp per seed (the warp walks the seed's rows one after another;
+// long rows are probed in reverse, all 32 lanes at once).
 constexpr int kTriWarps = 8;
 __global__ void __launch_bounds__(kTriWarps * 32)
 k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
@@ -478,12 +576,41 @@ k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   const int dv = (int)(a.offsets[v + 1] - ob);
   SmemMap<32, true> map{sK[w], sD[w], nullptr};
   map.clear(lane, 32);
+  int32_t myl = -1, myd = 0, mypc = 0;
+  int64_t myps = 0;
+  if (lane < dv) {
+    myl = __ldg(a.rank_of + a.nbr[ob + lane]);
+    myd = a.nd[ob + lane];
+    mypc = __ldg(a.pc + ob + lane);
+    myps = __ldg(a.ps + ob + lane);
+  }
   __syncwarp();
-  if (lane < dv) map.insert(__ldg(a.rank_of + a.nbr[ob + lane]), a.nd[ob + lane]);
+  if (lane < dv) map.insert(myl, myd);
   __syncwarp();
   int64_t tri = 0;
   double Wt = 0.0;
-  tri_rows(a, ob, dv, 0, 1, lane, map, tri, Wt, dv);
+  const bool rev = lane < dv && use_reverse(mypc, dv);
+  unsigned fwd = __ballot_sync(0xffffffffu, lane < dv && mypc > 0 && !rev);
+  while (fwd) {
+    const int x = __ffs(fwd) - 1;
+    fwd &= fwd - 1;
+    const int32_t pcx = __shfl_sync(0xffffffffu, mypc, x);
+    const int64_t psx = __shfl_sync(0xffffffffu, myps, x);
+    const int32_t dx = __shfl_sync(0xffffffffu, myd, x);
+    tri_row(a, a.adjj + psx, 0, pcx, dv + dx, lane, map, tri, Wt);
+  }
+  unsigned rv = __ballot_sync(0xffffffffu, rev);
+  while (rv) {
+    const int x = __ffs(rv) - 1;
+    rv &= rv - 1;
+    const int32_t pcx = __shfl_sync(0xffffffffu, mypc, x);
+    const int64_t psx = __shfl_sync(0xffffffffu, myps, x);
+    const int32_t dx = __shfl_sync(0xffffffffu, myd, x);
+    if (lane < dv && lane != x && rowhash_has(a.rowhash + 2 * psx, rowhash_lg(pcx), myl)) {
+      Wt += __ldg(a.G + dv + dx + myd);
+      ++tri;
+    }
+  }
   tri = warp_sum(tri);
   Wt = warp_sum(Wt);
   if (lane == 0) {
@@ -867,7 +994,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   double* ctab = ctx.buf("f_ctab").as<double>(m2);
   EFG_LAUNCH(k_ctab_group<8>, ceil_div(c[kCG] * 8, B), B, 0, s, L.cg, c[kCG], P.g.offsets, dcnt, hkey, hcnt, P.deg,
              P.ftab, ctab);
-  EFG_LAUNCH(k_ctab_block, c[kCB], 128, 0, s, L.cb, c[kCB], P.g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab);
+  EFG_LAUNCH(k_ctab_block, c[kCB], kCtabThreads, 0, s, L.cb, c[kCB], P.g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab);
   FArgs a;
   a.offsets = P.g.offsets;
   a.nbr = P.g.nbr;
@@ -886,6 +1013,11 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   a.hkey = hkey;
   a.hcnt = hcnt;
   a.ctab = ctab;
+  {
+    int4* rowhash = ctx.buf("f_rowhash").as<int4>(m2);  // 2 * m buckets: bucket 2*offp[i] starts Adj+(i)
+    EFG_LAUNCH(k_rowhash, ceil_div(n * 32, B), B, 0, s, P.offp, P.adjj, n, rowhash);
+    a.rowhash = rowhash;
+  }
   a.seed_lo = r.lo;
   a.Tc = ctx.buf("f_Tc").as<int64_t>(cnt);
   a.Wc = ctx.buf("f_Wc").as<double>(cnt);

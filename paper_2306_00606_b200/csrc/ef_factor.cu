@@ -793,6 +793,334 @@ __global__ void k_hub_bitmaps(const int32_t* __restrict__ hubs, int64_t nhubs, c
   }
 }
 
+// ------------------------------------------------------- triangle listing
+// Whole-graph passes list every triangle once instead of once per member.
+// Triangle {u, v, w} with rank(u) > rank(v) > rank(w) (u the lowest in the
+// degree order, v the middle) is found by v's CTA: for every lower-ranked
+// neighbour u of v (a "row"), Adj+(u) is scanned (coalesced, 4 loads in
+// flight per lane) against a shared-memory map of Adj+(v), which is short
+// (|Adj+| <= sqrt(2m); 813 at R-MAT22) even for hubs.  Probes: sum over u of
+// |Adj+(u)|^2 = 7.1e9 at R-MAT22, against 2.2e10 for the per-seed scan.
+// All three members receive the same correction G(du+dv+dw): v sums its own
+// in registers, u's arrive once per row, w's are summed per entry of Adj+(v)
+// and reach global memory once per (v, chunk of rows, entry).  Sums are in
+// fixed point (P = rint(G 2^40), |P| < 2^45: error <= 2^-41 per triangle,
+// far below the 1e-12 floor of the EF tolerance) with integer additions,
+// which commute, so the result does not depend on scheduling.  Global words
+// per node: (sum of s >> 32, sum of s & (2^32-1), count), never overflowing
+// (a row has < 2^16 hits, a node < 2^31 partial sums).
+constexpr int kMidWarps = 8;
+constexpr int kMidThreads = 256;
+constexpr int kMidNB = 1024;        // shared map of Adj+(v): |Adj+(v)| <= 1024 at load <= 1/4
+constexpr int kMidMaxP = kMidNB;    // longer Adj+(v) use their global hash, hits go straight to global
+constexpr int kMidChunk = 512;      // rows between entry flushes: 32-bit entry words cannot overflow
+constexpr int kListScale = 40;      // P = rint(G * 2^40)
+constexpr int64_t kListMaxDeg = 1000000;  // |G(3 dmax)| < 32
+
+struct MArgs {
+  const int64_t* offsets;
+  const int32_t* nbr;
+  const int32_t* nd;
+  const int64_t* ps;  // per slot e = (v -> u): start of Adj+(u)
+  const int32_t* pc;  // per slot: |Adj+(u)|
+  const int64_t* offp;
+  const int32_t* adjj;
+  const int32_t* adjd;
+  const int32_t* rank_of;
+  const int32_t* by_rank;
+  const int32_t* deg_by_rank;
+  const int4* rowhash;
+  const int64_t* PT;        // fixed-point G
+  unsigned long long* acc;  // [4 n] per node: (hi, lo, count, pad)
+  int64_t n, n32;           // labels < n32: degree > 32
+  int mode;
+};
+
+__global__ void k_gfix(const double* __restrict__ G, int64_t len, int64_t* __restrict__ PT) {
+  const int64_t S = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (S < len) PT[S] = (int64_t)rint(ldexp(G[S], kListScale));
+}
+
+// one partial sum (|s| < 2^63) and its triangle count into a node's words
+__device__ __forceinline__ void red_node(unsigned long long* acc, int32_t node, int64_t s, uint64_t c) {
+  unsigned long long* p = acc + 4 * (int64_t)node;
+  atomicAdd(p, (unsigned long long)(s >> 32));
+  atomicAdd(p + 1, (unsigned long long)(s & 0xffffffffll));
+  atomicAdd(p + 2, (unsigned long long)c);
+}
+
+// v's own share, kept as two words so that any number of rows fits
+struct Acc2 {
+  int64_t hi = 0, lo = 0;
+  uint32_t c = 0;
+  __device__ __forceinline__ void add_row(int64_t s, uint32_t n) {
+    hi += s >> 32;
+    lo += s & 0xffffffffll;
+    c += n;
+  }
+};
+
+// shared bucketed map label -> position in Adj+(v) (NB buckets of 4, key -1 = empty)
+template <class V>
+__device__ __forceinline__ int32_t smap_find(const int4* __restrict__ keys, const V* __restrict__ vals, uint32_t lg,
+                                             int32_t key) {
+  const uint32_t mask = (1u << lg) - 1;
+  uint32_t b = ((uint32_t)key * 2654435761u) >> (32 - lg);
+  while (true) {
+    const int4 q = keys[b];
+    const int k = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
+    if (k >= 0) return vals[4 * b + k];
+    if (q.w == -1) return -1;
+    b = (b + 1) & mask;
+  }
+}
+template <class V>
+__device__ __forceinline__ void smap_insert(int4* keys, V* vals, uint32_t lg, int32_t key, int32_t val) {
+  int32_t* flat = reinterpret_cast<int32_t*>(keys);
+  const uint32_t mask = (1u << lg) - 1;
+  for (uint32_t b = ((uint32_t)key * 2654435761u) >> (32 - lg);; b = (b + 1) & mask)
+    for (int k = 0; k < 4; ++k)
+      if (atomicCAS(&flat[4 * b + k], -1, key) == -1) {
+        vals[4 * b + k] = (V)val;
+        return;
+      }
+}
+
+// Scan of one row Adj+(u)[lane::32] in phases of kUnroll entries (labels +
+// degrees, then membership, then the G gathers), calling hit(y, label, P)
+// for every w found in Adj+(v) (y = its position there).
+template <class Find, class Hit>
+__device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu, int32_t s0, int lane, Find find,
+                                         Hit hit) {
+  for (int32_t p = lane; p < pu; p += 32 * kUnroll) {
+    int32_t j[kUnroll], d[kUnroll], y[kUnroll];
+    int64_t g[kUnroll];
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) j[k] = p + 32 * k < pu ? __ldg(a.adjj + psu + p + 32 * k) : -1;
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) y[k] = j[k] >= 0 ? find(j[k]) : -1;
+    // only hits need w's degree: gathered by label (4 B streamed per probe instead of 8)
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) d[k] = y[k] >= 0 ? __ldg(a.deg_by_rank + j[k]) : 0;
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k) g[k] = y[k] >= 0 ? __ldg(a.PT + s0 + d[k]) : 0;
+#pragma unroll
+    for (int k = 0; k < kUnroll; ++k)
+      if (y[k] >= 0) hit(y[k], j[k], g[k]);
+  }
+}
+
+__device__ __forceinline__ bool above(int32_t dj, int32_t j, int32_t dv, int32_t v) {
+  return dj > dv || (dj == dv && j > v);
+}
+
+// dv <= 32 (labels >= n32): warp per v.  Lane e holds slot e of v's row;
+// Adj+(v) is the set of lanes whose neighbour ranks above v.  A row's hits
+// are distinct entries, so the per-warp entry sums need no atomics.
+__global__ void __launch_bounds__(kMidWarps * 32)
+k_mid_warp(MArgs a) {
+  __shared__ int4 sK[kMidWarps][32];
+  __shared__ int8_t sV[kMidWarps][128];
+  __shared__ int64_t sP[kMidWarps][32];
+  __shared__ uint32_t sC[kMidWarps][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t r = a.n32 + (int64_t)blockIdx.x * kMidWarps + w;
+  if (r >= a.n) return;
+  const int32_t v = __ldg(a.by_rank + r);
+  const int64_t ob = __ldg(a.offsets + v);
+  const int32_t dv = (int32_t)(__ldg(a.offsets + v + 1) - ob);
+  int32_t u = -1, du = 0, pu = 0;
+  int64_t psu = 0;
+  bool up = false;
+  if (lane < dv) {
+    u = __ldg(a.nbr + ob + lane);
+    du = __ldg(a.nd + ob + lane);
+    up = above(du, u, dv, v);
+    pu = __ldg(a.pc + ob + lane);
+    psu = __ldg(a.ps + ob + lane);
+  }
+  sK[w][lane] = make_int4(-1, -1, -1, -1);
+  sP[w][lane] = 0;
+  sC[w][lane] = 0;
+  __syncwarp();
+  if (up) smap_insert(sK[w], sV[w], 5, __ldg(a.rank_of + u), lane);
+  __syncwarp();
+  Acc2 av;
+  unsigned todo = __ballot_sync(0xffffffffu, lane < dv && !up && pu >= 2);
+  if (__ballot_sync(0xffffffffu, up) == 0) todo = 0;  // Adj+(v) empty: no triangle has v in the middle
+  while (todo) {
+    const int x = __ffs(todo) - 1;
+    todo &= todo - 1;
+    const int32_t ux = __shfl_sync(0xffffffffu, u, x);
+    const int32_t pux = __shfl_sync(0xffffffffu, pu, x);
+    const int64_t psx = __shfl_sync(0xffffffffu, psu, x);
+    const int32_t s0 = dv + __shfl_sync(0xffffffffu, du, x);
+    int64_t rs = 0;
+    uint32_t rc = 0;
+    mid_scan(
+        a, psx, pux, s0, lane, [&](int32_t key) { return smap_find(sK[w], sV[w], 5, key); },
+        [&](int32_t y, int32_t, int64_t g) {
+          rs += g;
+          ++rc;
+          sP[w][y] += g;
+          sC[w][y] += 1;
+        });
+    rc = warp_sum(rc);
+    if (rc) {
+      rs = warp_sum(rs);
+      av.add_row(rs, rc);
+      if (lane == 0) red_node(a.acc, ux, rs, rc);
+    }
+    __syncwarp();
+  }
+  if (up && sC[w][lane]) red_node(a.acc, u, sP[w][lane], sC[w][lane]);
+  if (lane == 0 && av.c) {
+    unsigned long long* q = a.acc + 4 * (int64_t)v;
+    atomicAdd(q, (unsigned long long)av.hi);
+    atomicAdd(q + 1, (unsigned long long)av.lo);
+    atomicAdd(q + 2, (unsigned long long)av.c);
+  }
+}
+
+// dv > 32 (labels < n32, hubs first): CTA per v, warps take rows.  Entry
+// sums of Adj+(v) in shared memory as 32-bit words (Q = -P split 22 + 23
+// bits, count), flushed every kMidChunk rows.
+struct MidSmem {
+  int4 lk[kMidNB];
+  int64_t rps[kMidChunk];  // compacted rows of the current chunk: Adj+(u) start,
+  int32_t ru[kMidChunk], rdu[kMidChunk], rpu[kMidChunk];  // u, du, |Adj+(u)|
+  int32_t node[kMidMaxP];
+  uint32_t elo[kMidMaxP], ehi[kMidMaxP], ec[kMidMaxP];
+  int16_t lv[4 * kMidNB];
+  int32_t nrows;
+};
+
+__global__ void __launch_bounds__(kMidThreads)
+k_mid_block(MArgs a) {
+  extern __shared__ int4 dyn_mid[];
+  MidSmem& sm = *reinterpret_cast<MidSmem*>(dyn_mid);
+  __shared__ int64_t red_h[kMidThreads / 32], red_l[kMidThreads / 32];
+  __shared__ uint32_t red_c[kMidThreads / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  constexpr int NW = kMidThreads / 32;
+  const int32_t v = __ldg(a.by_rank + blockIdx.x);
+  const int64_t ob = __ldg(a.offsets + v);
+  const int32_t dv = (int32_t)(__ldg(a.offsets + v + 1) - ob);
+  const int64_t pb = __ldg(a.offp + v);
+  const int32_t pv = (int32_t)(__ldg(a.offp + v + 1) - pb);
+  if (pv == 0) return;  // no triangle has v in the middle
+  const bool gset = pv > kMidMaxP;
+  const uint32_t lgl = 32u - __clz(max(pv, 2) - 1);  // NB = 2^lgl >= pv buckets
+  if (!gset) {
+    for (int b = threadIdx.x; b < (1 << lgl); b += blockDim.x) sm.lk[b] = make_int4(-1, -1, -1, -1);
+    __syncthreads();
+    for (int t = threadIdx.x; t < pv; t += blockDim.x) {
+      const int32_t l = __ldg(a.adjj + pb + t);
+      smap_insert(sm.lk, sm.lv, lgl, l, t);
+      sm.node[t] = __ldg(a.by_rank + l);
+      sm.elo[t] = 0;
+      sm.ehi[t] = 0;
+      sm.ec[t] = 0;
+    }
+  }
+  __syncthreads();
+  Acc2 av;
+  const int4* vset = a.rowhash + 2 * pb;
+  const uint32_t vlg = rowhash_lg(max(pv, 2));
+  for (int32_t c0 = 0; c0 < dv; c0 += kMidChunk) {
+    // compact the chunk's rows (lower-ranked u with |Adj+(u)| >= 2) into shared memory
+    if (threadIdx.x == 0) sm.nrows = 0;
+    __syncthreads();
+    for (int32_t x = c0 + threadIdx.x; x < min(dv, c0 + kMidChunk); x += blockDim.x) {
+      const int64_t e = ob + x;
+      const int32_t u = __ldg(a.nbr + e), du = __ldg(a.nd + e);
+      const int32_t pu = above(du, u, dv, v) ? 0 : __ldg(a.pc + e);
+      const bool keep = pu >= 2;
+      const unsigned m = __ballot_sync(__activemask(), keep);
+      int base = 0;
+      const int leader = __ffs(__activemask()) - 1;
+      if (lane == leader && m) base = atomicAdd(&sm.nrows, __popc(m));
+      base = __shfl_sync(__activemask(), base, leader);
+      if (keep) {
+        const int k = base + __popc(m & ((1u << lane) - 1));
+        sm.ru[k] = u;
+        sm.rdu[k] = du;
+        sm.rpu[k] = pu;
+        sm.rps[k] = __ldg(a.ps + e);
+      }
+    }
+    __syncthreads();
+    const int32_t nr = sm.nrows;
+    for (int32_t x = w; x < nr; x += NW) {
+      const int32_t u = sm.ru[x], du = sm.rdu[x], pu = sm.rpu[x];
+      const int64_t psu = sm.rps[x];
+      int64_t rs = 0;
+      uint32_t rc = 0;
+      if (gset) {
+        mid_scan(
+            a, psu, pu, dv + du, lane, [&](int32_t key) { return rowhash_has(vset, vlg, key) ? 0 : -1; },
+            [&](int32_t, int32_t wl, int64_t g) {
+              rs += g;
+              ++rc;
+              red_node(a.acc, __ldg(a.by_rank + wl), g, 1);
+            });
+      } else {
+        mid_scan(
+            a, psu, pu, dv + du, lane, [&](int32_t key) { return smap_find(sm.lk, sm.lv, lgl, key); },
+            [&](int32_t y, int32_t, int64_t g) {
+              rs += g;
+              ++rc;
+              if (a.mode == 0) {
+                const uint64_t q = (uint64_t)(-g);
+                atomicAdd(sm.elo + y, (uint32_t)(q & 0x3fffff));
+                atomicAdd(sm.ehi + y, (uint32_t)(q >> 22));
+                atomicAdd(sm.ec + y, 1u);
+              }
+            });
+      }
+      rc = warp_sum(rc);
+      if (rc) {
+        rs = warp_sum(rs);
+        if (lane == 0) {
+          red_node(a.acc, u, rs, rc);
+          av.add_row(rs, rc);
+        }
+      }
+    }
+    __syncthreads();
+    if (!gset) {
+      for (int t = threadIdx.x; t < pv; t += blockDim.x) {
+        if (sm.ec[t]) {
+          const uint64_t q = ((uint64_t)sm.ehi[t] << 22) + sm.elo[t];
+          red_node(a.acc, sm.node[t], -(int64_t)q, sm.ec[t]);
+          sm.elo[t] = 0;
+          sm.ehi[t] = 0;
+          sm.ec[t] = 0;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  const int64_t vh = block_sum<kMidThreads>(av.hi, red_h);
+  const int64_t vl = block_sum<kMidThreads>(av.lo, red_l);
+  const uint32_t vc = block_sum<kMidThreads>(av.c, red_c);
+  if (threadIdx.x == 0 && vc) {
+    unsigned long long* q = a.acc + 4 * (int64_t)v;
+    atomicAdd(q, (unsigned long long)vh);
+    atomicAdd(q + 1, (unsigned long long)vl);
+    atomicAdd(q + 2, (unsigned long long)vc);
+  }
+}
+
+// Per-seed results of the listing: t(v) and W_t(v) = (hi 2^32 + lo) 2^-40.
+__global__ void k_list_out(const unsigned long long* __restrict__ acc, FArgs a, int64_t count) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= count) return;
+  const unsigned long long* p = acc + 4 * (a.seed_lo + q);
+  a.tri[q] = (int64_t)p[2];
+  a.Wt[q] = ldexp((double)(int64_t)p[0], 32 - kListScale) + ldexp((double)(int64_t)p[1], -kListScale);
+}
+
 // Epilogue: closed-form T and mass, W, EF = ln T - W/T, flags.
 __global__ void k_epilogue(FArgs a, int64_t count, double* __restrict__ ef, int64_t* __restrict__ total,
                            uint8_t* __restrict__ flags, int64_t* __restrict__ T_out, double* __restrict__ W_out) {
@@ -1024,9 +1352,39 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   a.Ws = ctx.buf("f_Ws").as<double>(cnt);
   a.tri = ctx.buf("f_tri").as<int64_t>(cnt);
   a.Wt = ctx.buf("f_Wt").as<double>(cnt);
-  // 2. triangles (the long kernels first)
+  // 2. triangles: listed once each for whole-graph passes, else per seed (the long kernels first)
   const int64_t nhubs = c[kHubs], ntasks = c[kNTasks];
-  if (nhubs) {
+  const bool listing = r.lo == 0 && r.hi == n && P.dmax <= kListMaxDeg && !getenv("EFG_NO_LIST");
+  if (listing) {
+    MArgs ma;
+    int64_t* PT = ctx.buf("l_pt").as<int64_t>(P.ftab_len);
+    EFG_LAUNCH(k_gfix, ceil_div(P.ftab_len, B), B, 0, s, P.gtab, P.ftab_len, PT);
+    unsigned long long* acc = ctx.buf("l_acc").as<unsigned long long>(4 * n);
+    EFG_CUDA_CHECK(cudaMemsetAsync(acc, 0, 4 * n * sizeof(unsigned long long), s));
+    ma.offsets = P.g.offsets;
+    ma.nbr = P.g.nbr;
+    ma.nd = P.nd;
+    ma.ps = P.ps;
+    ma.pc = P.pc;
+    ma.offp = P.offp;
+    ma.adjj = P.adjj;
+    ma.adjd = P.adjd;
+    ma.rank_of = P.rank_of;
+    ma.by_rank = P.by_rank;
+    ma.deg_by_rank = P.deg_by_rank;
+    ma.rowhash = a.rowhash;
+    ma.PT = PT;
+    ma.acc = acc;
+    ma.n = n;
+    ma.n32 = c[kTr1] + c[kTr2] + c[kTr3] + c[kHubs];  // whole-graph pass: nodes of degree > 32
+    ma.mode = getenv("EFG_LIST_MODE") ? atoi(getenv("EFG_LIST_MODE")) : 0;
+    const int smb = (int)sizeof(MidSmem);
+    EFG_CUDA_CHECK(cudaFuncSetAttribute(k_mid_block, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
+    EFG_LAUNCH(k_mid_block, ma.n32, kMidThreads, smb, s, ma);
+    EFG_LAUNCH(k_mid_warp, ceil_div(n - ma.n32, kMidWarps), kMidWarps * 32, 0, s, ma);
+    EFG_LAUNCH(k_list_out, ceil_div(cnt, B), B, 0, s, acc, a, cnt);
+  }
+  if (nhubs && !listing) {
     // exact bitmaps; hubs sorted by descending triangle work; tasks of kHubRows rows
     const int64_t words = ceil_div(n, 32);
     uint32_t* bms = ctx.buf("f_bitmaps").as<uint32_t>(nhubs * words);
@@ -1061,7 +1419,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     EFG_LAUNCH(k_hub_merge, ceil_div(nhubs, B), B, 0, s, hs, nhubs, tstart, tk.ptri, tk.pWt, a);
     if (st) st->terms = ntasks;
   }
-  {
+  if (!listing) {
     // buckets of 4 keys: dv <= 256 at load <= 1/8 with degrees, dv <= 1024 / 4096 at load <= 1/4
     auto k_tri_seed_256 = k_tri_seed<128, 512, true>;
     auto k_tri_seed_1024 = k_tri_seed<256, 1024, true>;

@@ -77,6 +77,7 @@ struct Prepared {
   int32_t* adjd = nullptr;      // [m]  degree of each Adj+ entry
   int32_t* rank_of = nullptr;   // [n]  position in descending (degree, id) order
   int32_t* deg_by_rank = nullptr;  // [n]
+  int32_t* by_rank = nullptr;   // [n]  node of each rank label
   int64_t* ps = nullptr;        // [2m] per slot (v->i): offp[i]
   int32_t* pc = nullptr;        // [2m] per slot (v->i): |Adj+(i)|
 };

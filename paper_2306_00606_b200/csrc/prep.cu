@@ -189,6 +189,7 @@ void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P)
     P.rank_of = ctx.buf("rank_of").as<int32_t>(n);
     P.deg_by_rank = ctx.buf("deg_by_rank").as<int32_t>(n);
     EFG_LAUNCH(k_rank_scatter, ceil_div(n, B), B, 0, s, val + n, n, P.deg, P.rank_of, P.deg_by_rank);
+    P.by_rank = val + n;
   }
   P.adjj = ctx.buf("adjj").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);
   P.adjd = ctx.buf("adjd").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);

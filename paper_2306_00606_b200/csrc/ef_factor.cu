@@ -813,7 +813,8 @@ constexpr int kMidWarps = 8;
 constexpr int kMidThreads = 256;
 constexpr int kMidNB = 1024;        // shared map of Adj+(v): |Adj+(v)| <= 1024 at load <= 1/4
 constexpr int kMidMaxP = kMidNB;    // longer Adj+(v) use their global hash, hits go straight to global
-constexpr int kMidChunk = 512;      // rows between entry flushes: 32-bit entry words cannot overflow
+constexpr int kMidChunk = 512;
+constexpr int kMidUnroll = 4;      // rows between entry flushes: 32-bit entry words cannot overflow
 constexpr int kListScale = 40;      // P = rint(G * 2^40)
 constexpr int64_t kListMaxDeg = 1000000;  // |G(3 dmax)| < 32
 
@@ -833,6 +834,7 @@ struct MArgs {
   const int64_t* PT;        // fixed-point G
   unsigned long long* acc;  // [4 n] per node: (hi, lo, count, pad)
   int64_t n, n32;           // labels < n32: degree > 32
+  int64_t nhubs, ntasks;    // labels < nhubs come as ntasks row-range tasks
   int mode;
 };
 
@@ -861,18 +863,26 @@ struct Acc2 {
 };
 
 // shared bucketed map label -> position in Adj+(v) (NB buckets of 4, key -1 = empty)
+// slot of key past a full first bucket (rare at load <= 1/4), or -1
+__device__ __noinline__ int32_t smap_slot_slow(const int4* __restrict__ keys, uint32_t lg, uint32_t b, int32_t key) {
+  const uint32_t mask = (1u << lg) - 1;
+  while (true) {
+    b = (b + 1) & mask;
+    const int4 q = keys[b];
+    const int k = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
+    if (k >= 0) return (int32_t)(4 * b + k);
+    if (q.w == -1) return -1;
+  }
+}
 template <class V>
 __device__ __forceinline__ int32_t smap_find(const int4* __restrict__ keys, const V* __restrict__ vals, uint32_t lg,
                                              int32_t key) {
-  const uint32_t mask = (1u << lg) - 1;
-  uint32_t b = ((uint32_t)key * 2654435761u) >> (32 - lg);
-  while (true) {
-    const int4 q = keys[b];
-    const int k = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
-    if (k >= 0) return vals[4 * b + k];
-    if (q.w == -1) return -1;
-    b = (b + 1) & mask;
-  }
+  const uint32_t b = ((uint32_t)key * 2654435761u) >> (32 - lg);
+  const int4 q = keys[b];
+  int32_t slot = q.x == key ? (int32_t)(4 * b) : q.y == key ? (int32_t)(4 * b + 1)
+               : q.z == key ? (int32_t)(4 * b + 2) : q.w == key ? (int32_t)(4 * b + 3) : -1;
+  if (slot < 0 && q.w != -1) slot = smap_slot_slow(keys, lg, b, key);
+  return slot >= 0 ? (int32_t)vals[slot] : -1;
 }
 template <class V>
 __device__ __forceinline__ void smap_insert(int4* keys, V* vals, uint32_t lg, int32_t key, int32_t val) {
@@ -889,24 +899,36 @@ __device__ __forceinline__ void smap_insert(int4* keys, V* vals, uint32_t lg, in
 // Scan of one row Adj+(u)[lane::32] in phases of kUnroll entries (labels +
 // degrees, then membership, then the G gathers), calling hit(y, label, P)
 // for every w found in Adj+(v) (y = its position there).
-template <class Find, class Hit>
-__device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu, int32_t s0, int lane, Find find,
-                                         Hit hit) {
-  for (int32_t p = lane; p < pu; p += 32 * kUnroll) {
-    int32_t j[kUnroll], d[kUnroll], y[kUnroll];
-    int64_t g[kUnroll];
+template <int U, class Find, class Hit>
+__device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu, int32_t lim, int32_t s0, int lane,
+                                         Find find, Hit hit) {
+  // Adj+(u) is sorted by label and only labels < lim = rank(v) can lie in
+  // Adj+(v): the scan stops at the first entry >= lim (i.e. at v itself)
+  const int32_t* __restrict__ row = a.adjj + psu;
+  const int64_t* __restrict__ pt = a.PT + s0;
+  for (int32_t p0 = 0; p0 < pu; p0 += 32 * U) {
+    int32_t j[U], d[U], y[U];
+    int64_t g[U];
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) j[k] = p + 32 * k < pu ? __ldg(a.adjj + psu + p + 32 * k) : -1;
+    for (int k = 0; k < U; ++k) {
+      const int32_t p = p0 + lane + 32 * k;
+      j[k] = p < pu ? __ldg(row + p) : INT32_MAX;
+    }
+    bool past = false;
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) y[k] = j[k] >= 0 ? find(j[k]) : -1;
+    for (int k = 0; k < U; ++k) {
+      past |= j[k] >= lim;
+      y[k] = j[k] < lim ? find(j[k]) : -1;
+    }
     // only hits need w's degree: gathered by label (4 B streamed per probe instead of 8)
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) d[k] = y[k] >= 0 ? __ldg(a.deg_by_rank + j[k]) : 0;
+    for (int k = 0; k < U; ++k) d[k] = y[k] >= 0 ? __ldg(a.deg_by_rank + j[k]) : 0;
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k) g[k] = y[k] >= 0 ? __ldg(a.PT + s0 + d[k]) : 0;
+    for (int k = 0; k < U; ++k) g[k] = y[k] >= 0 ? __ldg(pt + d[k]) : 0;
 #pragma unroll
-    for (int k = 0; k < kUnroll; ++k)
+    for (int k = 0; k < U; ++k)
       if (y[k] >= 0) hit(y[k], j[k], g[k]);
+    if (__any_sync(0xffffffffu, past)) break;
   }
 }
 
@@ -957,8 +979,8 @@ k_mid_warp(MArgs a) {
     const int32_t s0 = dv + __shfl_sync(0xffffffffu, du, x);
     int64_t rs = 0;
     uint32_t rc = 0;
-    mid_scan(
-        a, psx, pux, s0, lane, [&](int32_t key) { return smap_find(sK[w], sV[w], 5, key); },
+    mid_scan<kMidUnroll>(
+        a, psx, pux, (int32_t)r, s0, lane, [&](int32_t key) { return smap_find(sK[w], sV[w], 5, key); },
         [&](int32_t y, int32_t, int64_t g) {
           rs += g;
           ++rc;
@@ -996,18 +1018,30 @@ struct MidSmem {
 };
 
 __global__ void __launch_bounds__(kMidThreads)
-k_mid_block(MArgs a) {
+k_mid_block(MArgs a, HubTasks tk) {
   extern __shared__ int4 dyn_mid[];
   MidSmem& sm = *reinterpret_cast<MidSmem*>(dyn_mid);
   __shared__ int64_t red_h[kMidThreads / 32], red_l[kMidThreads / 32];
   __shared__ uint32_t red_c[kMidThreads / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   constexpr int NW = kMidThreads / 32;
-  const int32_t v = __ldg(a.by_rank + blockIdx.x);
+  int32_t v, x0, x1;
+  if (a.mode == 2 && blockIdx.x < a.ntasks) return;
+  if (a.mode == 3 && blockIdx.x >= a.ntasks) return;
+  if (blockIdx.x < a.ntasks) {  // a row range of a hub
+    v = tk.seed[blockIdx.x];
+    x0 = tk.x0[blockIdx.x];
+    x1 = tk.x1[blockIdx.x];
+  } else {
+    v = __ldg(a.by_rank + a.nhubs + (blockIdx.x - a.ntasks));
+    x0 = 0;
+    x1 = (int32_t)(__ldg(a.offsets + v + 1) - __ldg(a.offsets + v));
+  }
   const int64_t ob = __ldg(a.offsets + v);
   const int32_t dv = (int32_t)(__ldg(a.offsets + v + 1) - ob);
   const int64_t pb = __ldg(a.offp + v);
   const int32_t pv = (int32_t)(__ldg(a.offp + v + 1) - pb);
+  const int32_t labv = __ldg(a.rank_of + v);
   if (pv == 0) return;  // no triangle has v in the middle
   const bool gset = pv > kMidMaxP;
   const uint32_t lgl = 32u - __clz(max(pv, 2) - 1);  // NB = 2^lgl >= pv buckets
@@ -1027,11 +1061,11 @@ k_mid_block(MArgs a) {
   Acc2 av;
   const int4* vset = a.rowhash + 2 * pb;
   const uint32_t vlg = rowhash_lg(max(pv, 2));
-  for (int32_t c0 = 0; c0 < dv; c0 += kMidChunk) {
+  for (int32_t c0 = x0; c0 < x1; c0 += kMidChunk) {
     // compact the chunk's rows (lower-ranked u with |Adj+(u)| >= 2) into shared memory
     if (threadIdx.x == 0) sm.nrows = 0;
     __syncthreads();
-    for (int32_t x = c0 + threadIdx.x; x < min(dv, c0 + kMidChunk); x += blockDim.x) {
+    for (int32_t x = c0 + threadIdx.x; x < min(x1, c0 + kMidChunk); x += blockDim.x) {
       const int64_t e = ob + x;
       const int32_t u = __ldg(a.nbr + e), du = __ldg(a.nd + e);
       const int32_t pu = above(du, u, dv, v) ? 0 : __ldg(a.pc + e);
@@ -1057,16 +1091,16 @@ k_mid_block(MArgs a) {
       int64_t rs = 0;
       uint32_t rc = 0;
       if (gset) {
-        mid_scan(
-            a, psu, pu, dv + du, lane, [&](int32_t key) { return rowhash_has(vset, vlg, key) ? 0 : -1; },
+        mid_scan<kMidUnroll>(
+            a, psu, pu, labv, dv + du, lane, [&](int32_t key) { return rowhash_has(vset, vlg, key) ? 0 : -1; },
             [&](int32_t, int32_t wl, int64_t g) {
               rs += g;
               ++rc;
               red_node(a.acc, __ldg(a.by_rank + wl), g, 1);
             });
       } else {
-        mid_scan(
-            a, psu, pu, dv + du, lane, [&](int32_t key) { return smap_find(sm.lk, sm.lv, lgl, key); },
+        mid_scan<kMidUnroll>(
+            a, psu, pu, labv, dv + du, lane, [&](int32_t key) { return smap_find(sm.lk, sm.lv, lgl, key); },
             [&](int32_t y, int32_t, int64_t g) {
               rs += g;
               ++rc;
@@ -1355,6 +1389,32 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   // 2. triangles: listed once each for whole-graph passes, else per seed (the long kernels first)
   const int64_t nhubs = c[kHubs], ntasks = c[kNTasks];
   const bool listing = r.lo == 0 && r.hi == n && P.dmax <= kListMaxDeg && !getenv("EFG_NO_LIST");
+  // hub tasks (hubs in descending work order, kHubRows rows each) serve both triangle paths
+  HubTasks tk{};
+  int64_t* tstart = nullptr;
+  int32_t* hs = nullptr;
+  if (nhubs) {
+    int64_t* hw_sorted = hw + nhubs;
+    hs = ctx.buf("f_hub_sorted").as<int32_t>(nhubs);
+    EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, hw, hw_sorted, L.hub, hs, nhubs, 0, 64, s));
+    EFG_REGION("cub::DeviceRadixSort::SortPairsDescending", s,
+               EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(ctx.buf("cub").get(tmp), tmp, hw, hw_sorted,
+                                                                        L.hub, hs, nhubs, 0, 64, s)));
+    int64_t* hnt = ctx.buf("f_hub_nt").as<int64_t>(nhubs + 1);
+    tstart = ctx.buf("f_hub_tstart").as<int64_t>(nhubs + 1);
+    EFG_LAUNCH(k_hub_ntasks, ceil_div(nhubs + 1, B), B, 0, s, hs, nhubs, P.g.offsets, hnt);
+    EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, hnt, tstart, nhubs + 1, s));
+    EFG_REGION("cub::DeviceScan::ExclusiveSum", s,
+               EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, hnt, tstart, nhubs + 1, s)));
+    int32_t* tseed = ctx.buf("f_hub_tseed").as<int32_t>(ntasks);
+    int32_t* tx0 = ctx.buf("f_hub_tx0").as<int32_t>(ntasks);
+    int32_t* tx1 = ctx.buf("f_hub_tx1").as<int32_t>(ntasks);
+    EFG_LAUNCH(k_hub_tasks, ceil_div(nhubs, B), B, 0, s, hs, nhubs, P.g.offsets, tstart, tseed, tx0, tx1);
+    tk.seed = tseed;
+    tk.x0 = tx0;
+    tk.x1 = tx1;
+    if (st) st->terms = ntasks;
+  }
   if (listing) {
     MArgs ma;
     int64_t* PT = ctx.buf("l_pt").as<int64_t>(P.ftab_len);
@@ -1377,47 +1437,27 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     ma.acc = acc;
     ma.n = n;
     ma.n32 = c[kTr1] + c[kTr2] + c[kTr3] + c[kHubs];  // whole-graph pass: nodes of degree > 32
+    ma.nhubs = nhubs;                                  // labels [0, nhubs): degree > kHashMaxDeg
+    ma.ntasks = ntasks;
     ma.mode = getenv("EFG_LIST_MODE") ? atoi(getenv("EFG_LIST_MODE")) : 0;
     const int smb = (int)sizeof(MidSmem);
     EFG_CUDA_CHECK(cudaFuncSetAttribute(k_mid_block, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
-    EFG_LAUNCH(k_mid_block, ma.n32, kMidThreads, smb, s, ma);
+    EFG_LAUNCH(k_mid_block, ntasks + (ma.n32 - nhubs), kMidThreads, smb, s, ma, tk);
     EFG_LAUNCH(k_mid_warp, ceil_div(n - ma.n32, kMidWarps), kMidWarps * 32, 0, s, ma);
     EFG_LAUNCH(k_list_out, ceil_div(cnt, B), B, 0, s, acc, a, cnt);
-  }
-  if (nhubs && !listing) {
-    // exact bitmaps; hubs sorted by descending triangle work; tasks of kHubRows rows
+  } else if (nhubs) {
+    // exact bitmaps over rank labels, per-task partials merged in task order
     const int64_t words = ceil_div(n, 32);
     uint32_t* bms = ctx.buf("f_bitmaps").as<uint32_t>(nhubs * words);
     int32_t* hub_slot = ctx.buf("f_hub_slot").as<int32_t>(n);
     EFG_CUDA_CHECK(cudaMemsetAsync(bms, 0, nhubs * words * sizeof(uint32_t), s));
     EFG_LAUNCH(k_hub_bitmaps, nhubs, 1024, 0, s, L.hub, nhubs, P.g.offsets, P.g.nbr, P.rank_of, bms, words, hub_slot);
-    int64_t* hw_sorted = hw + nhubs;
-    int32_t* hs = ctx.buf("f_hub_sorted").as<int32_t>(nhubs);
-    EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, hw, hw_sorted, L.hub, hs, nhubs, 0, 64, s));
-    EFG_REGION("cub::DeviceRadixSort::SortPairsDescending", s,
-               EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(ctx.buf("cub").get(tmp), tmp, hw, hw_sorted,
-                                                                        L.hub, hs, nhubs, 0, 64, s)));
-    int64_t* hnt = ctx.buf("f_hub_nt").as<int64_t>(nhubs + 1);
-    int64_t* tstart = ctx.buf("f_hub_tstart").as<int64_t>(nhubs + 1);
-    EFG_LAUNCH(k_hub_ntasks, ceil_div(nhubs + 1, B), B, 0, s, hs, nhubs, P.g.offsets, hnt);
-    EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, hnt, tstart, nhubs + 1, s));
-    EFG_REGION("cub::DeviceScan::ExclusiveSum", s,
-               EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, hnt, tstart, nhubs + 1, s)));
-    HubTasks tk;
-    int32_t* tseed = ctx.buf("f_hub_tseed").as<int32_t>(ntasks);
-    int32_t* tx0 = ctx.buf("f_hub_tx0").as<int32_t>(ntasks);
-    int32_t* tx1 = ctx.buf("f_hub_tx1").as<int32_t>(ntasks);
-    EFG_LAUNCH(k_hub_tasks, ceil_div(nhubs, B), B, 0, s, hs, nhubs, P.g.offsets, tstart, tseed, tx0, tx1);
-    tk.seed = tseed;
-    tk.x0 = tx0;
-    tk.x1 = tx1;
     tk.ptri = ctx.buf("f_hub_ptri").as<int64_t>(ntasks);
     tk.pWt = ctx.buf("f_hub_pWt").as<double>(ntasks);
     const int smh = kFilterWords * 4;
     EFG_CUDA_CHECK(cudaFuncSetAttribute(k_tri_hub, cudaFuncAttributeMaxDynamicSharedMemorySize, smh));
     EFG_LAUNCH(k_tri_hub, ntasks, kHubThreads, smh, s, tk, ntasks, bms, words, hub_slot, a);
     EFG_LAUNCH(k_hub_merge, ceil_div(nhubs, B), B, 0, s, hs, nhubs, tstart, tk.ptri, tk.pWt, a);
-    if (st) st->terms = ntasks;
   }
   if (!listing) {
     // buckets of 4 keys: dv <= 256 at load <= 1/8 with degrees, dv <= 1024 / 4096 at load <= 1/4

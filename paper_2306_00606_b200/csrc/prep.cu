@@ -131,6 +131,111 @@ __global__ void k_rank_scatter(const int32_t* __restrict__ by_rank, int64_t n, c
   deg_by_rank[r] = deg[v];
 }
 
+// ---- Adj+ rows sorted by label (ascending): the triangle listing stops a
+// row scan at the first label >= rank(v).  Rows are short (|Adj+| <= sqrt(2m)),
+// so one warp sorts a row in registers: a bitonic network over 32*I labels,
+// I per lane in blocked order (within-lane stages are register min/max,
+// cross-lane stages shuffles).  Degrees are re-gathered by label afterwards.
+template <int I>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&x)[I], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * I; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < I) {
+#pragma unroll
+        for (int i = 0; i < I; ++i) {
+          const int pi = i ^ j;
+          if (pi > i) {
+            const bool up = ((lane * I + i) & k) == 0;
+            const uint32_t lo = min(x[i], x[pi]), hi = max(x[i], x[pi]);
+            x[i] = up ? lo : hi;
+            x[pi] = up ? hi : lo;
+          }
+        }
+      } else {
+        const int lj = j / I;
+        const bool lower = (lane & lj) == 0;
+#pragma unroll
+        for (int i = 0; i < I; ++i) {
+          const uint32_t y = __shfl_xor_sync(0xffffffffu, x[i], lj);
+          const bool up = ((lane * I + i) & k) == 0;
+          x[i] = (lower == up) ? min(x[i], y) : max(x[i], y);
+        }
+      }
+    }
+  }
+}
+
+template <int I>
+__device__ __forceinline__ void sort_row(int32_t* __restrict__ row, int32_t* __restrict__ rowd, int p, int lane,
+                                         const int32_t* __restrict__ deg_by_rank) {
+  uint32_t x[I];
+#pragma unroll
+  for (int i = 0; i < I; ++i) {  // any input arrangement: load coalesced
+    const int t = i * 32 + lane;
+    x[i] = t < p ? (uint32_t)row[t] : 0xffffffffu;
+  }
+  warp_bitonic<I>(x, lane);
+#pragma unroll
+  for (int i = 0; i < I; ++i) {  // sorted in blocked order
+    const int t = lane * I + i;
+    if (t < p) {
+      row[t] = (int32_t)x[i];
+      rowd[t] = __ldg(deg_by_rank + x[i]);
+    }
+  }
+}
+
+// Warp per row.  Each warp scans 32 nodes at a time (interleaved over the
+// grid: long rows cluster at small ids in skewed graphs) and sorts those in
+// [PMIN, PMAX]; rows above 1024 entries (rare) rank by counting through a
+// scratch row.  Two instantiations keep the small-row kernel's registers low.
+template <int PMIN, int PMAX>
+__global__ void k_sort_rows(const int64_t* __restrict__ offp, int64_t n, const int32_t* __restrict__ deg_by_rank,
+                            int32_t* __restrict__ adjj, int32_t* __restrict__ adjd, int32_t* __restrict__ scratch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g * 32 < n; g += nw) {
+    const int64_t mine = g * 32 + lane;
+    int p = 0;
+    if (mine < n) p = (int)(offp[mine + 1] - offp[mine]);
+    unsigned todo = __ballot_sync(0xffffffffu, p >= PMIN && p <= PMAX && p >= 2);
+    while (todo) {
+      const int x = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const int64_t v = g * 32 + x;
+      const int pv = __shfl_sync(0xffffffffu, p, x);
+      const int64_t b = offp[v];
+      int32_t* row = adjj + b;
+      int32_t* rowd = adjd + b;
+      if (PMAX <= 256) {
+        if (pv <= 32) sort_row<1>(row, rowd, pv, lane, deg_by_rank);
+        else if (pv <= 64) sort_row<2>(row, rowd, pv, lane, deg_by_rank);
+        else if (pv <= 128) sort_row<4>(row, rowd, pv, lane, deg_by_rank);
+        else sort_row<8>(row, rowd, pv, lane, deg_by_rank);
+      } else if (pv <= 512) {
+        sort_row<16>(row, rowd, pv, lane, deg_by_rank);
+      } else if (pv <= 1024) {
+        sort_row<32>(row, rowd, pv, lane, deg_by_rank);
+      } else {
+        for (int t = lane; t < pv; t += 32) {
+          const int32_t key = row[t];
+          int32_t rank = 0;
+          for (int o = 0; o < pv; ++o) rank += row[o] < key;
+          scratch[b + rank] = key;
+        }
+        __syncwarp();
+        for (int t = lane; t < pv; t += 32) {
+          row[t] = scratch[b + t];
+          rowd[t] = __ldg(deg_by_rank + row[t]);
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
 struct Choose2 {
   __host__ __device__ int64_t operator()(const int32_t& d) const { return (int64_t)d * (d - 1) / 2; }
 };
@@ -195,6 +300,17 @@ void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P)
   P.adjd = ctx.buf("adjd").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);
   EFG_LAUNCH(k_fill_adjp, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.offp, P.rank_of, P.adjj,
              P.adjd);
+  {
+    // rows sorted by label: a row scan for a higher-ranked v can stop at v (triangle listing)
+    int32_t* scratch = ctx.buf("adjj_scratch").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);
+    auto k_sort_small = k_sort_rows<2, 256>;
+    auto k_sort_large = k_sort_rows<257, INT32_MAX>;
+    const int64_t groups = ceil_div(n, 32);
+    EFG_LAUNCH(k_sort_small, std::min<int64_t>(ceil_div(groups * 32, B), 16 * ctx.num_sms), B, 0, s, P.offp, n,
+               P.deg_by_rank, P.adjj, P.adjd, scratch);
+    EFG_LAUNCH(k_sort_large, std::min<int64_t>(ceil_div(groups * 32, B), 4 * ctx.num_sms), B, 0, s, P.offp, n,
+               P.deg_by_rank, P.adjj, P.adjd, scratch);
+  }
   P.ps = ctx.buf("ps").as<int64_t>(m2);
   P.pc = ctx.buf("pc").as<int32_t>(m2);
   EFG_LAUNCH(k_slot_plus, ceil_div(m2, B), B, 0, s, g.nbr, m2, P.offp, P.ps, P.pc);

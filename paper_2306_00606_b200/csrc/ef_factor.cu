@@ -39,6 +39,14 @@ namespace {
 constexpr int kHashSlots = 8192;     // smem hash of Adj(v) for dv <= 4096
 constexpr int kHashMaxDeg = kHashSlots / 2;
 
+// Per-node chain data packed in one 16-byte record (one sector per random
+// gather instead of three): m < 2^31 keeps offsets below 2^32.
+struct __align__(16) NodeRec {
+  int64_t s1;    // sum of neighbour degrees
+  uint32_t off;  // offsets[i]: H_i = hkey/hcnt[off, off + dcnt)
+  int32_t dcnt;  // |D_i|
+};
+
 struct FArgs {
   const int64_t* offsets;
   const int32_t* nbr;
@@ -57,6 +65,7 @@ struct FArgs {
   const int32_t* hkey;
   const int32_t* hcnt;
   const double* ctab;
+  const NodeRec* nrec;
   const int4* rowhash;     // bucketed hash of Adj+(i) for |Adj+(i)| >= kRevMin, at bucket 2*offp[i]
   int64_t seed_lo;
   // per-seed partials, index v - seed_lo
@@ -303,6 +312,12 @@ k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __r
   }
 }
 
+__global__ void k_node_rec(const int64_t* __restrict__ offsets, const int64_t* __restrict__ s1,
+                           const int32_t* __restrict__ dcnt, int64_t n, NodeRec* __restrict__ nrec) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) nrec[i] = NodeRec{s1[i], (uint32_t)offsets[i], dcnt[i]};
+}
+
 // ---------------------------------------------------------------- per seed
 template <class T>
 __device__ __forceinline__ T warp_sum(T x) {
@@ -331,8 +346,9 @@ __device__ __forceinline__ T block_sum(T x, T* scratch) {
 __device__ __forceinline__ void chain_slot(const FArgs& a, int64_t e, int64_t dv, int64_t& Tc, double& Wc) {
   const int32_t i = a.nbr[e];
   const int64_t di = a.nd[e];
-  Tc += (di - 1) * (dv + di - 4) + a.s1[i] - dv;
-  int64_t lo = a.offsets[i], hi = lo + a.dcnt[i] - 1;
+  const NodeRec r = a.nrec[i];
+  Tc += (di - 1) * (dv + di - 4) + r.s1 - dv;
+  int64_t lo = r.off, hi = lo + r.dcnt - 1;
   while (lo < hi) {  // dv is present: v is a neighbour of i
     int64_t mid = (lo + hi) >> 1;
     if (__ldg(a.hkey + mid) < dv) lo = mid + 1; else hi = mid;
@@ -1357,6 +1373,8 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   EFG_LAUNCH(k_ctab_group<8>, ceil_div(c[kCG] * 8, B), B, 0, s, L.cg, c[kCG], P.g.offsets, dcnt, hkey, hcnt, P.deg,
              P.ftab, ctab);
   EFG_LAUNCH(k_ctab_block, c[kCB], kCtabThreads, 0, s, L.cb, c[kCB], P.g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab);
+  NodeRec* nrec = ctx.buf("f_nrec").as<NodeRec>(n);
+  EFG_LAUNCH(k_node_rec, ceil_div(n, B), B, 0, s, P.g.offsets, P.s1, dcnt, n, nrec);
   FArgs a;
   a.offsets = P.g.offsets;
   a.nbr = P.g.nbr;
@@ -1375,6 +1393,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   a.hkey = hkey;
   a.hcnt = hcnt;
   a.ctab = ctab;
+  a.nrec = nrec;
   {
     int4* rowhash = ctx.buf("f_rowhash").as<int4>(m2);  // 2 * m buckets: bucket 2*offp[i] starts Adj+(i)
     EFG_LAUNCH(k_rowhash, ceil_div(n * 32, B), B, 0, s, P.offp, P.adjj, n, rowhash);

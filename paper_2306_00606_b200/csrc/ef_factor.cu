@@ -54,6 +54,7 @@ struct FArgs {
   const int64_t* s1;
   const double* F;
   const double* G;         // G[S] = F(S-6) - F(S-4): triangle correction per unit weight
+  const int64_t* PT;       // P[S] = rint(G[S] 2^40): triangle sums are exact integers (any order, any path)
   const int64_t* ps;       // [2m] start of Adj+(nbr[e]) in adjp
   const int32_t* pc;       // [2m] |Adj+(nbr[e])|
   const int32_t* adjj;     // oriented adjacency Adj+ as rank labels
@@ -73,7 +74,8 @@ struct FArgs {
   double* Wc;
   double* Ws;
   int64_t* tri;
-  double* Wt;
+  int64_t* Wth;  // W_t in fixed point, two words: (sum of P >> 32, sum of P & (2^32 - 1)), P = rint(G 2^40)
+  int64_t* Wtl;
 };
 
 // ---------------------------------------------------------------- H build
@@ -471,13 +473,23 @@ struct SmemMap {
 
 
 
+// Exact two-word fixed-point sum of P values (each |P| < 2^45): the value is
+// hi 2^32 + lo; both words stay far from overflow for any count < 2^31.
+struct Fix2 {
+  int64_t hi = 0, lo = 0;
+  __device__ __forceinline__ void add(int64_t p) {
+    hi += p >> 32;
+    lo += p & 0xffffffffll;
+  }
+};
+
 // One warp over entries [p0, p1) of row `row` (= Adj+(i), s0 = dv + di), in
 // phases so that each phase's loads are issued together: kUnroll entry loads,
 // kUnroll membership probes, kUnroll degree lookups for the hits, kUnroll
 // G-table gathers, then the (fixed-order) accumulation.
 template <class Map>
 __device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restrict__ row, int32_t p0, int32_t p1,
-                                        int32_t s0, int lane, const Map& map, int64_t& tri, double& Wt) {
+                                        int32_t s0, int lane, const Map& map, int64_t& tri, Fix2& Wt) {
   for (int32_t p = p0 + lane; p < p1; p += 32 * kUnroll) {
     int32_t j[kUnroll], dj[kUnroll];
 #pragma unroll
@@ -486,7 +498,7 @@ __device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restric
       // the entry's degree streams alongside its label (adjd), so a hit needs
       // only the G gather; labels past the shared bitmap check the global one
       int32_t tag[kUnroll], dd[kUnroll];
-      double g[kUnroll];
+      int64_t g[kUnroll];
       const int32_t* rowd = a.adjd + (row - a.adjj);
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) dd[u] = j[u] >= 0 ? __ldg(rowd + p + 32 * u) : 0;
@@ -495,11 +507,11 @@ __device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restric
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) dj[u] = tag[u] >= 0 ? map.finish(j[u], tag[u], dd[u]) : -1;
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) g[u] = dj[u] >= 0 ? __ldg(a.G + s0 + dj[u]) : 0.0;
+      for (int u = 0; u < kUnroll; ++u) g[u] = dj[u] >= 0 ? __ldg(a.PT + s0 + dj[u]) : 0;
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         if (dj[u] >= 0) {
-          Wt += g[u];
+          Wt.add(g[u]);
           ++tri;
         }
       }
@@ -509,7 +521,7 @@ __device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restric
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         if (dj[u] >= 0) {
-          Wt += __ldg(a.G + s0 + dj[u]);
+          Wt.add(__ldg(a.PT + s0 + dj[u]));
           ++tri;
         }
       }
@@ -521,7 +533,7 @@ __device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restric
 // Rows ob+x, x = first, first+stride, ... < nrows (of a seed of degree dv).
 template <class Map>
 __device__ __forceinline__ void tri_rows(const FArgs& a, int64_t ob, int nrows, int first, int stride, int lane,
-                                         const Map& map, int64_t& tri, double& Wt, int dv) {
+                                         const Map& map, int64_t& tri, Fix2& Wt, int dv) {
   for (int x = first; x < nrows; x += stride) {
     const int64_t e = ob + x;
     const int32_t pc = __ldg(a.pc + e);
@@ -604,7 +616,7 @@ k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   if (lane < dv) map.insert(myl, myd);
   __syncwarp();
   int64_t tri = 0;
-  double Wt = 0.0;
+  Fix2 Wt;
   const bool rev = lane < dv && use_reverse(mypc, dv);
   unsigned fwd = __ballot_sync(0xffffffffu, lane < dv && mypc > 0 && !rev);
   while (fwd) {
@@ -623,15 +635,17 @@ k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
     const int64_t psx = __shfl_sync(0xffffffffu, myps, x);
     const int32_t dx = __shfl_sync(0xffffffffu, myd, x);
     if (lane < dv && lane != x && rowhash_has(a.rowhash + 2 * psx, rowhash_lg(pcx), myl)) {
-      Wt += __ldg(a.G + dv + dx + myd);
+      Wt.add(__ldg(a.PT + dv + dx + myd));
       ++tri;
     }
   }
   tri = warp_sum(tri);
-  Wt = warp_sum(Wt);
+  Wt.hi = warp_sum(Wt.hi);
+  Wt.lo = warp_sum(Wt.lo);
   if (lane == 0) {
     a.tri[v - a.seed_lo] = tri;
-    a.Wt[v - a.seed_lo] = Wt;
+    a.Wth[v - a.seed_lo] = Wt.hi;
+    a.Wtl[v - a.seed_lo] = Wt.lo;
   }
 }
 
@@ -641,8 +655,7 @@ template <int THREADS, int NB, bool WITH_DEG>
 __global__ void __launch_bounds__(THREADS)
 k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   extern __shared__ int4 dyn4[];
-  __shared__ int64_t red_i[THREADS / 32];
-  __shared__ double red_d[THREADS / 32];
+  __shared__ int64_t red_i[THREADS / 32], red_h[THREADS / 32], red_l[THREADS / 32];
   const int64_t qs = blockIdx.x;
   if (qs >= count) return;
   const int32_t v = seeds[qs];
@@ -654,13 +667,15 @@ k_tri_seed(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   for (int x = threadIdx.x; x < dv; x += THREADS) map.insert(__ldg(a.rank_of + a.nbr[ob + x]), a.nd[ob + x]);
   __syncthreads();
   int64_t tri = 0;
-  double Wt = 0.0;
+  Fix2 Wt;
   tri_rows(a, ob, dv, threadIdx.x >> 5, THREADS / 32, threadIdx.x & 31, map, tri, Wt, dv);
   tri = block_sum<THREADS>(tri, red_i);
-  Wt = block_sum<THREADS>(Wt, red_d);
+  const int64_t wh = block_sum<THREADS>(Wt.hi, red_h);
+  const int64_t wl = block_sum<THREADS>(Wt.lo, red_l);
   if (threadIdx.x == 0) {
     a.tri[v - a.seed_lo] = tri;
-    a.Wt[v - a.seed_lo] = Wt;
+    a.Wth[v - a.seed_lo] = wh;
+    a.Wtl[v - a.seed_lo] = wl;
   }
 }
 
@@ -704,15 +719,15 @@ struct HubTasks {
   const int32_t* x0;    // [ntasks] first row
   const int32_t* x1;    // [ntasks] end row
   int64_t* ptri;
-  double* pWt;
+  int64_t* pWh;
+  int64_t* pWl;
 };
 
 __global__ void __launch_bounds__(kHubThreads, 1)
 k_tri_hub(HubTasks tk, int64_t ntasks, const uint32_t* __restrict__ bitmaps, int64_t words,
           const int32_t* __restrict__ hub_slot, FArgs a) {
   extern __shared__ uint32_t filt[];  // kFilterWords
-  __shared__ int64_t red_i[kHubThreads / 32];
-  __shared__ double red_d[kHubThreads / 32];
+  __shared__ int64_t red_i[kHubThreads / 32], red_h[kHubThreads / 32], red_l[kHubThreads / 32];
   const int64_t t = blockIdx.x;
   if (t >= ntasks) return;
   const int32_t v = tk.seed[t];
@@ -727,14 +742,16 @@ k_tri_hub(HubTasks tk, int64_t ntasks, const uint32_t* __restrict__ bitmaps, int
   __syncthreads();
   HubMap map{filt, bitmaps + (int64_t)hub_slot[v] * words, a.deg_by_rank};
   int64_t tri = 0;
-  double Wt = 0.0;
+  Fix2 Wt;
   const int x0 = tk.x0[t];
   tri_rows(a, ob + x0, tk.x1[t] - x0, threadIdx.x >> 5, kHubThreads / 32, threadIdx.x & 31, map, tri, Wt, dv);
   tri = block_sum<kHubThreads>(tri, red_i);
-  Wt = block_sum<kHubThreads>(Wt, red_d);
+  const int64_t wh = block_sum<kHubThreads>(Wt.hi, red_h);
+  const int64_t wl = block_sum<kHubThreads>(Wt.lo, red_l);
   if (threadIdx.x == 0) {
     tk.ptri[t] = tri;
-    tk.pWt[t] = Wt;
+    tk.pWh[t] = wh;
+    tk.pWl[t] = wl;
   }
 }
 
@@ -781,18 +798,20 @@ __global__ void k_hub_tasks(const int32_t* __restrict__ hubs, int64_t nhubs, con
 }
 
 __global__ void k_hub_merge(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ tstart,
-                            const int64_t* __restrict__ ptri, const double* __restrict__ pWt, FArgs a) {
+                            const int64_t* __restrict__ ptri, const int64_t* __restrict__ pWh,
+                            const int64_t* __restrict__ pWl, FArgs a) {
   const int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (h >= nhubs) return;
-  int64_t tri = 0;
-  double Wt = 0.0;
+  int64_t tri = 0, wh = 0, wl = 0;
   for (int64_t t = tstart[h]; t < tstart[h + 1]; ++t) {
     tri += ptri[t];
-    Wt += pWt[t];
+    wh += pWh[t];
+    wl += pWl[t];
   }
   const int32_t v = hubs[h];
   a.tri[v - a.seed_lo] = tri;
-  a.Wt[v - a.seed_lo] = Wt;
+  a.Wth[v - a.seed_lo] = wh;
+  a.Wtl[v - a.seed_lo] = wl;
 }
 
 __global__ void k_hub_bitmaps(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ offsets,
@@ -828,7 +847,7 @@ __global__ void k_hub_bitmaps(const int32_t* __restrict__ hubs, int64_t nhubs, c
 constexpr int kMidWarps = 8;
 constexpr int kMidThreads = 256;
 constexpr int kMidNB = 1024;        // shared map of Adj+(v): |Adj+(v)| <= 1024 at load <= 1/4
-constexpr int kMidMaxP = kMidNB;    // longer Adj+(v) use their global hash, hits go straight to global
+constexpr int kMidMaxP = kMidNB;    // longer Adj+(v) are processed in parts of this size
 constexpr int kMidChunk = 512;
 constexpr int kMidUnroll = 4;      // rows between entry flushes: 32-bit entry words cannot overflow
 constexpr int kListScale = 40;      // P = rint(G * 2^40)
@@ -846,12 +865,10 @@ struct MArgs {
   const int32_t* rank_of;
   const int32_t* by_rank;
   const int32_t* deg_by_rank;
-  const int4* rowhash;
   const int64_t* PT;        // fixed-point G
   unsigned long long* acc;  // [4 n] per node: (hi, lo, count, pad)
   int64_t n, n32;           // labels < n32: degree > 32
   int64_t nhubs, ntasks;    // labels < nhubs come as ntasks row-range tasks
-  int mode;
 };
 
 __global__ void k_gfix(const double* __restrict__ G, int64_t len, int64_t* __restrict__ PT) {
@@ -1042,8 +1059,6 @@ k_mid_block(MArgs a, HubTasks tk) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   constexpr int NW = kMidThreads / 32;
   int32_t v, x0, x1;
-  if (a.mode == 2 && blockIdx.x < a.ntasks) return;
-  if (a.mode == 3 && blockIdx.x >= a.ntasks) return;
   if (blockIdx.x < a.ntasks) {  // a row range of a hub
     v = tk.seed[blockIdx.x];
     x0 = tk.x0[blockIdx.x];
@@ -1059,87 +1074,75 @@ k_mid_block(MArgs a, HubTasks tk) {
   const int32_t pv = (int32_t)(__ldg(a.offp + v + 1) - pb);
   const int32_t labv = __ldg(a.rank_of + v);
   if (pv == 0) return;  // no triangle has v in the middle
-  const bool gset = pv > kMidMaxP;
-  const uint32_t lgl = 32u - __clz(max(pv, 2) - 1);  // NB = 2^lgl >= pv buckets
-  if (!gset) {
+  Acc2 av;
+  // Adj+(v) in parts of kMidMaxP entries (one part unless |Adj+(v)| > 1024);
+  // a part's rows stop at its last label
+  for (int32_t q0 = 0; q0 < pv; q0 += kMidMaxP) {
+    const int32_t np = min(pv - q0, kMidMaxP);
+    const int32_t lim = q0 + np < pv ? __ldg(a.adjj + pb + q0 + np) : labv;
+    const uint32_t lgl = 32u - __clz(max(np, 2) - 1);  // NB = 2^lgl >= np buckets
+    __syncthreads();
     for (int b = threadIdx.x; b < (1 << lgl); b += blockDim.x) sm.lk[b] = make_int4(-1, -1, -1, -1);
     __syncthreads();
-    for (int t = threadIdx.x; t < pv; t += blockDim.x) {
-      const int32_t l = __ldg(a.adjj + pb + t);
+    for (int t = threadIdx.x; t < np; t += blockDim.x) {
+      const int32_t l = __ldg(a.adjj + pb + q0 + t);
       smap_insert(sm.lk, sm.lv, lgl, l, t);
       sm.node[t] = __ldg(a.by_rank + l);
       sm.elo[t] = 0;
       sm.ehi[t] = 0;
       sm.ec[t] = 0;
     }
-  }
-  __syncthreads();
-  Acc2 av;
-  const int4* vset = a.rowhash + 2 * pb;
-  const uint32_t vlg = rowhash_lg(max(pv, 2));
-  for (int32_t c0 = x0; c0 < x1; c0 += kMidChunk) {
-    // compact the chunk's rows (lower-ranked u with |Adj+(u)| >= 2) into shared memory
-    if (threadIdx.x == 0) sm.nrows = 0;
-    __syncthreads();
-    for (int32_t x = c0 + threadIdx.x; x < min(x1, c0 + kMidChunk); x += blockDim.x) {
-      const int64_t e = ob + x;
-      const int32_t u = __ldg(a.nbr + e), du = __ldg(a.nd + e);
-      const int32_t pu = above(du, u, dv, v) ? 0 : __ldg(a.pc + e);
-      const bool keep = pu >= 2;
-      const unsigned m = __ballot_sync(__activemask(), keep);
-      int base = 0;
-      const int leader = __ffs(__activemask()) - 1;
-      if (lane == leader && m) base = atomicAdd(&sm.nrows, __popc(m));
-      base = __shfl_sync(__activemask(), base, leader);
-      if (keep) {
-        const int k = base + __popc(m & ((1u << lane) - 1));
-        sm.ru[k] = u;
-        sm.rdu[k] = du;
-        sm.rpu[k] = pu;
-        sm.rps[k] = __ldg(a.ps + e);
+    for (int32_t c0 = x0; c0 < x1; c0 += kMidChunk) {
+      // compact the chunk's rows (lower-ranked u with |Adj+(u)| >= 2) into shared memory
+      __syncthreads();
+      if (threadIdx.x == 0) sm.nrows = 0;
+      __syncthreads();
+      for (int32_t x = c0 + threadIdx.x; x < min(x1, c0 + kMidChunk); x += blockDim.x) {
+        const int64_t e = ob + x;
+        const int32_t u = __ldg(a.nbr + e), du = __ldg(a.nd + e);
+        const int32_t pu = above(du, u, dv, v) ? 0 : __ldg(a.pc + e);
+        const bool keep = pu >= 2;
+        const unsigned m = __ballot_sync(__activemask(), keep);
+        int base = 0;
+        const int leader = __ffs(__activemask()) - 1;
+        if (lane == leader && m) base = atomicAdd(&sm.nrows, __popc(m));
+        base = __shfl_sync(__activemask(), base, leader);
+        if (keep) {
+          const int k = base + __popc(m & ((1u << lane) - 1));
+          sm.ru[k] = u;
+          sm.rdu[k] = du;
+          sm.rpu[k] = pu;
+          sm.rps[k] = __ldg(a.ps + e);
+        }
       }
-    }
-    __syncthreads();
-    const int32_t nr = sm.nrows;
-    for (int32_t x = w; x < nr; x += NW) {
-      const int32_t u = sm.ru[x], du = sm.rdu[x], pu = sm.rpu[x];
-      const int64_t psu = sm.rps[x];
-      int64_t rs = 0;
-      uint32_t rc = 0;
-      if (gset) {
+      __syncthreads();
+      const int32_t nr = sm.nrows;
+      for (int32_t x = w; x < nr; x += NW) {
+        const int32_t u = sm.ru[x], du = sm.rdu[x], pu = sm.rpu[x];
+        const int64_t psu = sm.rps[x];
+        int64_t rs = 0;
+        uint32_t rc = 0;
         mid_scan<kMidUnroll>(
-            a, psu, pu, labv, dv + du, lane, [&](int32_t key) { return rowhash_has(vset, vlg, key) ? 0 : -1; },
-            [&](int32_t, int32_t wl, int64_t g) {
-              rs += g;
-              ++rc;
-              red_node(a.acc, __ldg(a.by_rank + wl), g, 1);
-            });
-      } else {
-        mid_scan<kMidUnroll>(
-            a, psu, pu, labv, dv + du, lane, [&](int32_t key) { return smap_find(sm.lk, sm.lv, lgl, key); },
+            a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return smap_find(sm.lk, sm.lv, lgl, key); },
             [&](int32_t y, int32_t, int64_t g) {
               rs += g;
               ++rc;
-              if (a.mode == 0) {
-                const uint64_t q = (uint64_t)(-g);
-                atomicAdd(sm.elo + y, (uint32_t)(q & 0x3fffff));
-                atomicAdd(sm.ehi + y, (uint32_t)(q >> 22));
-                atomicAdd(sm.ec + y, 1u);
-              }
+              const uint64_t q = (uint64_t)(-g);
+              atomicAdd(sm.elo + y, (uint32_t)(q & 0x3fffff));
+              atomicAdd(sm.ehi + y, (uint32_t)(q >> 22));
+              atomicAdd(sm.ec + y, 1u);
             });
-      }
-      rc = warp_sum(rc);
-      if (rc) {
-        rs = warp_sum(rs);
-        if (lane == 0) {
-          red_node(a.acc, u, rs, rc);
-          av.add_row(rs, rc);
+        rc = warp_sum(rc);
+        if (rc) {
+          rs = warp_sum(rs);
+          if (lane == 0) {
+            red_node(a.acc, u, rs, rc);
+            av.add_row(rs, rc);
+          }
         }
       }
-    }
-    __syncthreads();
-    if (!gset) {
-      for (int t = threadIdx.x; t < pv; t += blockDim.x) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < np; t += blockDim.x) {
         if (sm.ec[t]) {
           const uint64_t q = ((uint64_t)sm.ehi[t] << 22) + sm.elo[t];
           red_node(a.acc, sm.node[t], -(int64_t)q, sm.ec[t]);
@@ -1148,7 +1151,6 @@ k_mid_block(MArgs a, HubTasks tk) {
           sm.ec[t] = 0;
         }
       }
-      __syncthreads();
     }
   }
   const int64_t vh = block_sum<kMidThreads>(av.hi, red_h);
@@ -1162,13 +1164,14 @@ k_mid_block(MArgs a, HubTasks tk) {
   }
 }
 
-// Per-seed results of the listing: t(v) and W_t(v) = (hi 2^32 + lo) 2^-40.
+// Per-seed results of the listing: t(v) and the two W_t words.
 __global__ void k_list_out(const unsigned long long* __restrict__ acc, FArgs a, int64_t count) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= count) return;
   const unsigned long long* p = acc + 4 * (a.seed_lo + q);
   a.tri[q] = (int64_t)p[2];
-  a.Wt[q] = ldexp((double)(int64_t)p[0], 32 - kListScale) + ldexp((double)(int64_t)p[1], -kListScale);
+  a.Wth[q] = (int64_t)p[0];
+  a.Wtl[q] = (int64_t)p[1];
 }
 
 // Epilogue: closed-form T and mass, W, EF = ln T - W/T, flags.
@@ -1182,7 +1185,12 @@ __global__ void k_epilogue(FArgs a, int64_t count, double* __restrict__ ef, int6
   const int64_t tri = a.tri[q];
   const int64_t T = dv * (dv - 1) * (dv - 4) + 2 * (dv - 1) * s1v + a.Tc[q] - 8 * tri;
   const int64_t mass = dv * (dv - 1) + s1v - dv;
-  const double W = (a.Ws[q] + a.Wc[q]) + 4.0 * a.Wt[q];
+  // W_t = X 2^-40 with X = Wth 2^32 + Wtl, converted from the canonical split
+  // (0 <= lo < 2^32): a function of the exact integer only, so every triangle
+  // path and every sharding gives the same double
+  const int64_t xh = a.Wth[q] + (a.Wtl[q] >> 32), xl = a.Wtl[q] & 0xffffffffll;
+  const double Wt = ldexp((double)xh, 32 - kListScale) + ldexp((double)xl, -kListScale);
+  const double W = (a.Ws[q] + a.Wc[q]) + 4.0 * Wt;
   double e = 0.0;
   // entropy >= 0: clamp the last-ulp cancellation of ln T - W/T when only one
   // positive-degree cluster class exists (EF mathematically 0)
@@ -1394,20 +1402,21 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   a.hcnt = hcnt;
   a.ctab = ctab;
   a.nrec = nrec;
-  {
-    int4* rowhash = ctx.buf("f_rowhash").as<int4>(m2);  // 2 * m buckets: bucket 2*offp[i] starts Adj+(i)
-    EFG_LAUNCH(k_rowhash, ceil_div(n * 32, B), B, 0, s, P.offp, P.adjj, n, rowhash);
-    a.rowhash = rowhash;
-  }
   a.seed_lo = r.lo;
   a.Tc = ctx.buf("f_Tc").as<int64_t>(cnt);
   a.Wc = ctx.buf("f_Wc").as<double>(cnt);
   a.Ws = ctx.buf("f_Ws").as<double>(cnt);
   a.tri = ctx.buf("f_tri").as<int64_t>(cnt);
-  a.Wt = ctx.buf("f_Wt").as<double>(cnt);
+  a.Wth = ctx.buf("f_Wth").as<int64_t>(cnt);
+  a.Wtl = ctx.buf("f_Wtl").as<int64_t>(cnt);
+  {
+    int64_t* PT = ctx.buf("l_pt").as<int64_t>(P.ftab_len);
+    EFG_LAUNCH(k_gfix, ceil_div(P.ftab_len, B), B, 0, s, P.gtab, P.ftab_len, PT);
+    a.PT = PT;
+  }
   // 2. triangles: listed once each for whole-graph passes, else per seed (the long kernels first)
   const int64_t nhubs = c[kHubs], ntasks = c[kNTasks];
-  const bool listing = r.lo == 0 && r.hi == n && P.dmax <= kListMaxDeg && !getenv("EFG_NO_LIST");
+  const bool listing = r.lo == 0 && r.hi == n && P.dmax <= kListMaxDeg;
   // hub tasks (hubs in descending work order, kHubRows rows each) serve both triangle paths
   HubTasks tk{};
   int64_t* tstart = nullptr;
@@ -1436,8 +1445,6 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   }
   if (listing) {
     MArgs ma;
-    int64_t* PT = ctx.buf("l_pt").as<int64_t>(P.ftab_len);
-    EFG_LAUNCH(k_gfix, ceil_div(P.ftab_len, B), B, 0, s, P.gtab, P.ftab_len, PT);
     unsigned long long* acc = ctx.buf("l_acc").as<unsigned long long>(4 * n);
     EFG_CUDA_CHECK(cudaMemsetAsync(acc, 0, 4 * n * sizeof(unsigned long long), s));
     ma.offsets = P.g.offsets;
@@ -1451,14 +1458,12 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     ma.rank_of = P.rank_of;
     ma.by_rank = P.by_rank;
     ma.deg_by_rank = P.deg_by_rank;
-    ma.rowhash = a.rowhash;
-    ma.PT = PT;
+    ma.PT = a.PT;
     ma.acc = acc;
     ma.n = n;
     ma.n32 = c[kTr1] + c[kTr2] + c[kTr3] + c[kHubs];  // whole-graph pass: nodes of degree > 32
     ma.nhubs = nhubs;                                  // labels [0, nhubs): degree > kHashMaxDeg
     ma.ntasks = ntasks;
-    ma.mode = getenv("EFG_LIST_MODE") ? atoi(getenv("EFG_LIST_MODE")) : 0;
     const int smb = (int)sizeof(MidSmem);
     EFG_CUDA_CHECK(cudaFuncSetAttribute(k_mid_block, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
     EFG_LAUNCH(k_mid_block, ntasks + (ma.n32 - nhubs), kMidThreads, smb, s, ma, tk);
@@ -1472,13 +1477,17 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     EFG_CUDA_CHECK(cudaMemsetAsync(bms, 0, nhubs * words * sizeof(uint32_t), s));
     EFG_LAUNCH(k_hub_bitmaps, nhubs, 1024, 0, s, L.hub, nhubs, P.g.offsets, P.g.nbr, P.rank_of, bms, words, hub_slot);
     tk.ptri = ctx.buf("f_hub_ptri").as<int64_t>(ntasks);
-    tk.pWt = ctx.buf("f_hub_pWt").as<double>(ntasks);
+    tk.pWh = ctx.buf("f_hub_pWh").as<int64_t>(ntasks);
+    tk.pWl = ctx.buf("f_hub_pWl").as<int64_t>(ntasks);
     const int smh = kFilterWords * 4;
     EFG_CUDA_CHECK(cudaFuncSetAttribute(k_tri_hub, cudaFuncAttributeMaxDynamicSharedMemorySize, smh));
     EFG_LAUNCH(k_tri_hub, ntasks, kHubThreads, smh, s, tk, ntasks, bms, words, hub_slot, a);
-    EFG_LAUNCH(k_hub_merge, ceil_div(nhubs, B), B, 0, s, hs, nhubs, tstart, tk.ptri, tk.pWt, a);
+    EFG_LAUNCH(k_hub_merge, ceil_div(nhubs, B), B, 0, s, hs, nhubs, tstart, tk.ptri, tk.pWh, tk.pWl, a);
   }
   if (!listing) {
+    int4* rowhash = ctx.buf("f_rowhash").as<int4>(m2);  // 2 * m buckets: bucket 2*offp[i] starts Adj+(i)
+    EFG_LAUNCH(k_rowhash, ceil_div(n * 32, B), B, 0, s, P.offp, P.adjj, n, rowhash);
+    a.rowhash = rowhash;
     // buckets of 4 keys: dv <= 256 at load <= 1/8 with degrees, dv <= 1024 / 4096 at load <= 1/4
     auto k_tri_seed_256 = k_tri_seed<128, 512, true>;
     auto k_tri_seed_1024 = k_tri_seed<256, 1024, true>;

@@ -90,3 +90,51 @@ def test_shards_are_bitwise_identical_to_one_pass(rmat18, engine):
     # top-k on device equals host lexsort
     efh = full[0].cpu().numpy()
     assert np.array_equal(D.topk(full[0], 500), np.lexsort((np.arange(n), -efh))[:500])
+
+
+@pytest.fixture(scope="module")
+def dense_core():
+    # a 1100-clique inside a sparse random graph: clique members have more than
+    # 1024 higher-ranked neighbours, so the triangle listing takes Adj+(v) in parts
+    rng = np.random.default_rng(3)
+    k = 1100
+    iu = np.triu_indices(k, 1)
+    clique = np.stack(iu, 1).astype(np.int64)
+    extra = rng.integers(0, 30000, size=(200000, 2))
+    return efg.build_graph(np.concatenate([clique, extra]))
+
+
+def test_dense_core_listing_parts(dense_core):
+    g = dense_core
+    res_f = _run(g, 0, "factorized", None, want_tw=True)
+    res_d = _run(g, 0, "direct", None, want_tw=True)
+    assert np.array_equal(res_f.stats["T"], res_d.stats["T"])
+    assert np.array_equal(res_f.cluster_total, res_d.cluster_total)
+    assert ef_close(res_f.ef, res_d.ef)
+    rng = np.random.default_rng(1)
+    seeds = np.unique(np.concatenate([rng.choice(np.arange(1100, g.n), 300, replace=False), [0, 1, 2]]))
+    seeds = seeds[np.diff(g.offsets)[seeds] < 1200]  # keep the oracle cheap: at most a few clique members
+    ef, tot, fl, T, W = O.ef_seeds(g.offsets, g.neighbors, seeds=seeds, threads=8)
+    assert np.array_equal(res_f.stats["T"][seeds], T)
+    assert ef_close(res_f.ef[seeds], ef)
+
+
+def test_dense_core_shards_bitwise(dense_core):
+    # whole-graph passes list triangles, shards run the per-seed path: both sum
+    # the same exact fixed-point values, so the results are bitwise identical
+    import torch
+    from paper_2306_00606_b200 import device as D
+
+    dg = D.DeviceGraph.from_host(dense_core)
+    n = dense_core.n
+    full = [torch.empty(n, dtype=t, device="cuda") for t in (torch.float64, torch.int64, torch.uint8)]
+    D.ef_range(dg, 0, n, *full)
+    b = D.shard_bounds(dg, 3, "factorized")
+    outs = [torch.empty(n, dtype=t, device="cuda") for t in (torch.float64, torch.int64, torch.uint8)]
+    for r in range(3):
+        lo, hi = int(b[r]), int(b[r + 1])
+        if hi > lo:
+            D.ef_range(dg, lo, hi, outs[0][lo:hi], outs[1][lo:hi], outs[2][lo:hi])
+    torch.cuda.synchronize()
+    for x, y in zip(full, outs):
+        assert torch.equal(x, y)

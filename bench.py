@@ -84,29 +84,51 @@ def fingerprint(g):
     return h.hexdigest()
 
 
-# seed classes of the factorized engine's triangle kernels (csrc/ef_factor.cu): (kernel, lo < dv <= hi)
-TRI_CLASSES = [("k_tri_warp", 0, 32), ("k_tri_seed_256", 32, 256), ("k_tri_seed_1024", 256, 1024),
-               ("k_tri_seed_4096", 1024, 4096), ("k_tri_hub", 4096, 1 << 40)]
-
-
 def kernel_bytes_model(offsets, neighbors):
-    """Algorithmic bytes per launch of each triangle-probe kernel:
-    per probe 4 B (the Adj+ entry j), per row 20 B (neighbour id, |Adj+|, Adj+
-    start, neighbour degree), per seed 40 B (offsets, outputs t and W_t)."""
-    deg = np.diff(offsets)
-    n = deg.size
-    src = np.repeat(np.arange(n), deg)
-    nd = deg[neighbors]
-    up = (nd > deg[src]) | ((nd == deg[src]) & (neighbors > src))
-    dplus = np.bincount(src[up], minlength=n)
-    probes_per_seed = np.add.reduceat(dplus[neighbors], offsets[:-1]) if neighbors.size else np.zeros(n)
+    """Algorithmic bytes per launch of the triangle-listing kernels.
+
+    A whole-graph pass lists each triangle at its middle vertex v
+    (csrc/ef_factor.cu k_mid_block for dv > 32, k_mid_warp for dv <= 32):
+    every lower-ranked neighbour u of v is a row, and the label-sorted Adj+(u)
+    is read up to v itself (pos_u(v) + 1 labels of 4 B).  Per examined slot of
+    v's row 8 B (neighbour id + degree), per kept row 12 B (|Adj+(u)|, start),
+    per entry of Adj+(v) 8 B (label + node id), per seed 40 B.  The hit
+    gathers (12 B per triangle) are not counted: a lower bound.  Computed on
+    the GPU with torch (one sort of the oriented edges)."""
+    import torch
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    off = torch.as_tensor(np.asarray(offsets, dtype=np.int64), device=dev)
+    nb = torch.as_tensor(np.asarray(neighbors, dtype=np.int64), device=dev)
+    n = off.numel() - 1
+    deg = off[1:] - off[:-1]
+    src = torch.repeat_interleave(torch.arange(n, device=dev), deg)
+    dn, ds = deg[nb], deg[src]
+    up = (dn > ds) | ((dn == ds) & (nb > src))                 # nb ranks above src: nb in Adj+(src)
+    # rank label: position in descending (degree, id) order
+    order = torch.argsort(deg * (n + 1) + torch.arange(n, device=dev), descending=True)
+    label = torch.empty(n, dtype=torch.int64, device=dev)
+    label[order] = torch.arange(n, device=dev)
+    u, v = src[up], nb[up]
+    pu = torch.bincount(u, minlength=n)
+    key = u * n + label[v]
+    srt = torch.argsort(key)
+    start = torch.cumsum(pu, 0) - pu
+    pos = torch.empty_like(srt)
+    pos[srt] = torch.arange(srt.numel(), device=dev) - start[u[srt]]
+    keep = pu[u] >= 2
+    probes_v = torch.zeros(n, dtype=torch.int64, device=dev).index_add_(0, v[keep], pos[keep] + 1)
+    rows_v = torch.bincount(v[keep], minlength=n)
+    pv = torch.bincount(u, minlength=n)  # |Adj+| per node
     out = {}
-    for name, lo, hi in TRI_CLASSES:
-        msk = (deg > lo) & (deg <= hi)
-        probes = int(probes_per_seed[msk].sum())
-        rows = int(deg[msk].sum())
+    for name, big in (("k_mid_block", True), ("k_mid_warp", False)):
+        msk = deg > 32 if big else deg <= 32
+        probes = int(probes_v[msk].sum())
+        rows = int(rows_v[msk].sum())
+        slots = int(deg[msk].sum())
         seeds = int(msk.sum())
-        out[name] = {"probes": probes, "rows": rows, "seeds": seeds, "bytes": 4 * probes + 20 * rows + 40 * seeds}
+        ent = int(pv[msk].sum())
+        out[name] = {"probes": probes, "rows": rows, "slots": slots, "seeds": seeds,
+                     "bytes": 4 * probes + 8 * slots + 12 * rows + 8 * ent + 40 * seeds}
     return out
 
 
@@ -422,7 +444,8 @@ def main():
         "pass_achieved": b_alg / (ms_per_step / 1e3) / 1e9,
         "pass_frac": b_alg / (ms_per_step / 1e3) / 1e9 / peak,
         "bytes_alg_pass": b_alg,
-        "note": "achieved = kernel_bytes_alg (4 B/probe + 20 B/row + 40 B/seed, DESIGN.md) / live event time; "
+        "note": "achieved = kernel_bytes_alg (listing model: 4 B/label read + 8 B/slot + 12 B/row + 8 B/Adj+(v) "
+                "entry + 40 B/seed, DESIGN.md) / live event time; "
                 "pass_* = SURVEY 8(d) B_alg of the whole graph / step time; traffic = ncu dram bytes per launch "
                 "(profiles/dram_traffic.json)",
     }
@@ -445,7 +468,7 @@ def main():
         "cpu_baseline": cpu,
         "gpu_launches": int(st["launches"]) * args.steps,
         "kernels_ms": {k: round(v["ms"], 4) for k, v in sorted(kernels.items(), key=lambda kv: -kv[1]["ms"])},
-        "triangle_model": model,
+        "listing_model": model,
         "clocks": clocks.summary(),
         "setup_s": setup_s,
         "stats": {k: v for k, v in st.items() if k not in ("T", "W")},

@@ -848,7 +848,7 @@ constexpr int kMidWarps = 8;
 constexpr int kMidThreads = 256;
 constexpr int kMidNB = 1024;        // shared map of Adj+(v): |Adj+(v)| <= 1024 at load <= 1/4
 constexpr int kMidMaxP = kMidNB;    // longer Adj+(v) are processed in parts of this size
-constexpr int kMidChunk = 512;
+constexpr int kMidChunk = 256;
 constexpr int kMidUnroll = 4;      // rows between entry flushes: 32-bit entry words cannot overflow
 constexpr int kListScale = 40;      // P = rint(G * 2^40)
 constexpr int64_t kListMaxDeg = 1000000;  // |G(3 dmax)| < 32
@@ -897,7 +897,7 @@ struct Acc2 {
 
 // shared bucketed map label -> position in Adj+(v) (NB buckets of 4, key -1 = empty)
 // slot of key past a full first bucket (rare at load <= 1/4), or -1
-__device__ __noinline__ int32_t smap_slot_slow(const int4* __restrict__ keys, uint32_t lg, uint32_t b, int32_t key) {
+__device__ __forceinline__ int32_t smap_slot_slow(const int4* __restrict__ keys, uint32_t lg, uint32_t b, int32_t key) {
   const uint32_t mask = (1u << lg) - 1;
   while (true) {
     b = (b + 1) & mask;
@@ -963,6 +963,38 @@ __device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu
       if (y[k] >= 0) hit(y[k], j[k], g[k]);
     if (__any_sync(0xffffffffu, past)) break;
   }
+}
+
+// Explicit shared-window loads for the listing's probe loop: the map base is
+// converted once, so the loop carries a 32-bit address instead of
+// re-deriving the shared window of a generic pointer on every probe.
+__device__ __forceinline__ int4 lds128(uint32_t addr) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int32_t lds_s16(uint32_t addr) {
+  short v;
+  asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(addr));
+  return v;
+}
+
+// position of key in the shared map (keys at kb: NB = 2^lg buckets of 4; int16
+// positions at vb), or -1
+__device__ __forceinline__ int32_t mfind(uint32_t kb, uint32_t vb, uint32_t lg, int32_t key) {
+  uint32_t b = ((uint32_t)key * 2654435761u) >> (32 - lg);
+  int4 q = lds128(kb + 16 * b);
+  int k = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
+  if (k < 0 && q.w != -1) {  // first bucket full (rare at load <= 1/4): continue the probe sequence
+    const uint32_t mask = (1u << lg) - 1;
+    while (true) {
+      b = (b + 1) & mask;
+      q = lds128(kb + 16 * b);
+      k = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
+      if (k >= 0 || q.w == -1) break;
+    }
+  }
+  return k >= 0 ? lds_s16(vb + 2 * (4 * b + k)) : -1;
 }
 
 __device__ __forceinline__ bool above(int32_t dj, int32_t j, int32_t dv, int32_t v) {
@@ -1052,8 +1084,8 @@ struct MidSmem {
 
 __global__ void __launch_bounds__(kMidThreads)
 k_mid_block(MArgs a, HubTasks tk) {
-  extern __shared__ int4 dyn_mid[];
-  MidSmem& sm = *reinterpret_cast<MidSmem*>(dyn_mid);
+  __shared__ MidSmem sm;
+  const uint32_t kb = (uint32_t)__cvta_generic_to_shared(sm.lk), vb = (uint32_t)__cvta_generic_to_shared(sm.lv);
   __shared__ int64_t red_h[kMidThreads / 32], red_l[kMidThreads / 32];
   __shared__ uint32_t red_c[kMidThreads / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1123,7 +1155,7 @@ k_mid_block(MArgs a, HubTasks tk) {
         int64_t rs = 0;
         uint32_t rc = 0;
         mid_scan<kMidUnroll>(
-            a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return smap_find(sm.lk, sm.lv, lgl, key); },
+            a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); },
             [&](int32_t y, int32_t, int64_t g) {
               rs += g;
               ++rc;
@@ -1464,9 +1496,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
     ma.n32 = c[kTr1] + c[kTr2] + c[kTr3] + c[kHubs];  // whole-graph pass: nodes of degree > 32
     ma.nhubs = nhubs;                                  // labels [0, nhubs): degree > kHashMaxDeg
     ma.ntasks = ntasks;
-    const int smb = (int)sizeof(MidSmem);
-    EFG_CUDA_CHECK(cudaFuncSetAttribute(k_mid_block, cudaFuncAttributeMaxDynamicSharedMemorySize, smb));
-    EFG_LAUNCH(k_mid_block, ntasks + (ma.n32 - nhubs), kMidThreads, smb, s, ma, tk);
+    EFG_LAUNCH(k_mid_block, ntasks + (ma.n32 - nhubs), kMidThreads, 0, s, ma, tk);
     EFG_LAUNCH(k_mid_warp, ceil_div(n - ma.n32, kMidWarps), kMidWarps * 32, 0, s, ma);
     EFG_LAUNCH(k_list_out, ceil_div(cnt, B), B, 0, s, acc, a, cnt);
   } else if (nhubs) {

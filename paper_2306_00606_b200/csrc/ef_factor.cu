@@ -979,6 +979,10 @@ __device__ __forceinline__ int32_t lds_s16(uint32_t addr) {
   return v;
 }
 
+__device__ __forceinline__ void reds_add(uint32_t addr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
 // position of key in the shared map (keys at kb: NB = 2^lg buckets of 4; int16
 // positions at vb), or -1
 __device__ __forceinline__ int32_t mfind(uint32_t kb, uint32_t vb, uint32_t lg, int32_t key) {
@@ -1086,6 +1090,8 @@ __global__ void __launch_bounds__(kMidThreads)
 k_mid_block(MArgs a, HubTasks tk) {
   __shared__ MidSmem sm;
   const uint32_t kb = (uint32_t)__cvta_generic_to_shared(sm.lk), vb = (uint32_t)__cvta_generic_to_shared(sm.lv);
+  const uint32_t eb_lo = (uint32_t)__cvta_generic_to_shared(sm.elo), eb_hi = (uint32_t)__cvta_generic_to_shared(sm.ehi),
+                 eb_c = (uint32_t)__cvta_generic_to_shared(sm.ec);
   __shared__ int64_t red_h[kMidThreads / 32], red_l[kMidThreads / 32];
   __shared__ uint32_t red_c[kMidThreads / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1160,9 +1166,9 @@ k_mid_block(MArgs a, HubTasks tk) {
               rs += g;
               ++rc;
               const uint64_t q = (uint64_t)(-g);
-              atomicAdd(sm.elo + y, (uint32_t)(q & 0x3fffff));
-              atomicAdd(sm.ehi + y, (uint32_t)(q >> 22));
-              atomicAdd(sm.ec + y, 1u);
+              reds_add(eb_lo + 4 * y, (uint32_t)(q & 0x3fffff));
+              reds_add(eb_hi + 4 * y, (uint32_t)(q >> 22));
+              reds_add(eb_c + 4 * y, 1u);
             });
         rc = warp_sum(rc);
         if (rc) {

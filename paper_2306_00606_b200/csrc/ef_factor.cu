@@ -82,9 +82,9 @@ struct FArgs {
 // H_i (the histogram of the degrees of Adj(i): distinct values ascending, with
 // counts) is stored in adjacency-slot space: row i occupies hkey/hcnt
 // [offsets[i], offsets[i] + dcnt[i]) (|D_i| <= d_i), so no scan/compaction pass
-// is needed.  Rows are sorted by size class: a warp bitonic sort in registers
-// (d <= 32), a CTA radix sort in shared memory (d <= 2048), CUB's segmented
-// sort for the few larger rows followed by a CTA run-length pass.
+// is needed.  Rows by size class: a warp bitonic sort in registers (d <= 32),
+// a CTA radix sort in shared memory (d <= 2048), windowed counting in shared
+// memory for the few larger rows.
 
 // d <= 32: warp per row, 32-lane bitonic sort of the neighbour degrees.
 __global__ void k_hist_warp(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
@@ -176,50 +176,71 @@ k_hist_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
   if (threadIdx.x == 0) dcnt[i] = total;
 }
 
-// d > 2048: run-length pass over a row already sorted in `snd` (CTA per row).
-__global__ void __launch_bounds__(256)
-k_hist_rle(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
-           const int32_t* __restrict__ snd, int32_t* __restrict__ hkey, int32_t* __restrict__ hcnt,
-           int32_t* __restrict__ dcnt) {
-  using Scan = cub::BlockScan<int32_t, 256>;
-  __shared__ typename Scan::TempStorage tmp;
-  __shared__ int32_t carry;
+// d > 2048: CTA per row, counting instead of sorting.  Degrees are counted
+// in shared-memory windows of kHistWin consecutive values (direct-mapped
+// counters, native shared atomics); the window's nonzero counters are then
+// compacted in ascending order by a block scan.  Windows are visited from
+// the smallest degree up, jumping over empty value ranges (next window = the
+// smallest degree not yet counted), so a row costs one pass per non-empty
+// window (R-MAT22 hubs: 1-8).
+constexpr int kHistWin = 16384, kHistBigThreads = 512;
+__global__ void __launch_bounds__(kHistBigThreads)
+k_hist_count(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
+             const int32_t* __restrict__ nd, int32_t* __restrict__ hkey, int32_t* __restrict__ hcnt,
+             int32_t* __restrict__ dcnt) {
+  extern __shared__ int32_t wcnt[];  // kHistWin
+  using Scan = cub::BlockScan<int32_t, kHistBigThreads>;
+  using Red = cub::BlockReduce<int32_t, kHistBigThreads>;
+  __shared__ union {
+    typename Scan::TempStorage scan;
+    typename Red::TempStorage red;
+  } tmp;
+  __shared__ int32_t next_lo;
+  constexpr int kPer = kHistWin / kHistBigThreads;  // counters per thread in the compaction
   const int64_t q = blockIdx.x;
   if (q >= count) return;
   const int32_t i = rows[q];
   const int64_t b = offsets[i];
   const int d = (int)(offsets[i + 1] - b);
-  if (threadIdx.x == 0) carry = 0;
+  // smallest degree of the row: first window
+  int32_t mn = INT32_MAX;
+  for (int p = threadIdx.x; p < d; p += kHistBigThreads) mn = min(mn, nd[b + p]);
+  mn = Red(tmp.red).Reduce(mn, cub::Min());
+  if (threadIdx.x == 0) next_lo = mn;
   __syncthreads();
-  // pass 1: heads -> hkey, head position parked in hcnt
-  for (int p0 = 0; p0 < d; p0 += 256) {
-    const int p = p0 + threadIdx.x;
-    const bool head = p < d && (p == 0 || snd[b + p] != snd[b + p - 1]);
-    int32_t rank, tot;
-    Scan(tmp).ExclusiveSum((int32_t)head, rank, tot);
-    const int32_t base = carry;
-    if (head) {
-      hkey[b + base + rank] = snd[b + p];
-      hcnt[b + base + rank] = p;
-    }
+  int32_t lo = next_lo, base = 0;
+  while (lo != INT32_MAX) {
+    for (int k = threadIdx.x; k < kHistWin; k += kHistBigThreads) wcnt[k] = 0;
     __syncthreads();
-    if (threadIdx.x == 0) carry = base + tot;
+    int32_t nxt = INT32_MAX;  // smallest degree beyond this window
+    for (int p = threadIdx.x; p < d; p += kHistBigThreads) {
+      const int32_t k = nd[b + p];
+      if (k >= lo && k - lo < kHistWin) atomicAdd(&wcnt[k - lo], 1);
+      else if (k >= lo) nxt = min(nxt, k);
+    }
+    nxt = Red(tmp.red).Reduce(nxt, cub::Min());
+    if (threadIdx.x == 0) next_lo = nxt;
+    __syncthreads();
+    // ascending compaction of the nonzero counters: thread t owns [t*kPer, (t+1)*kPer)
+    int32_t nz = 0;
+#pragma unroll 4
+    for (int u = 0; u < kPer; ++u) nz += wcnt[threadIdx.x * kPer + u] != 0;
+    int32_t rank, total;
+    Scan(tmp.scan).ExclusiveSum(nz, rank, total);
+    rank += base;
+    for (int u = 0; u < kPer; ++u) {
+      const int32_t c = wcnt[threadIdx.x * kPer + u];
+      if (c) {
+        hkey[b + rank] = lo + threadIdx.x * kPer + u;
+        hcnt[b + rank] = c;
+        ++rank;
+      }
+    }
+    base += total;
+    lo = next_lo;
     __syncthreads();
   }
-  const int32_t total = carry;
-  // pass 2: counts = distance to the next head (read all, then write)
-  for (int r0 = 0; r0 < total; r0 += 256) {
-    const int r = r0 + threadIdx.x;
-    int32_t cur = 0, nxt = 0;
-    if (r < total) {
-      cur = hcnt[b + r];
-      nxt = r + 1 < total ? hcnt[b + r + 1] : d;
-    }
-    __syncthreads();
-    if (r < total) hcnt[b + r] = nxt - cur;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) dcnt[i] = total;
+  if (threadIdx.x == 0) dcnt[i] = base;
 }
 
 // Chain table, group of G lanes per row i: for every distinct neighbour
@@ -257,12 +278,15 @@ template <int K>
 __device__ __forceinline__ void ctab_outputs(const int32_t* __restrict__ sx, const double* __restrict__ sh, int nq,
                                              const int64_t (&base)[kCtabOut], const double* __restrict__ F,
                                              double (&acc)[kCtabOut]) {
+  const double* Fb[K];  // per-output table base: one 32-bit index per gather
+#pragma unroll
+  for (int k = 0; k < K; ++k) Fb[k] = F + base[k];
 #pragma unroll 4
   for (int q = 0; q < nq; ++q) {
     const int32_t x = sx[q];
     const double h = sh[q];
 #pragma unroll
-    for (int k = 0; k < K; ++k) acc[k] = fma(h, __ldg(F + base[k] + x), acc[k]);
+    for (int k = 0; k < K; ++k) acc[k] = fma(h, __ldg(Fb[k] + x), acc[k]);
   }
 }
 
@@ -1280,16 +1304,6 @@ __global__ void k_seed_work(const int64_t* __restrict__ offsets, const int32_t* 
 }  // namespace
 
 // Segment bounds of listed rows (CUB segmented sort over non-contiguous rows).
-struct RowBegin {
-  const int32_t* rows;
-  const int64_t* off;
-  __host__ __device__ int64_t operator()(const int64_t& k) const { return off[rows[k]]; }
-};
-struct RowEnd {
-  const int32_t* rows;
-  const int64_t* off;
-  __host__ __device__ int64_t operator()(const int64_t& k) const { return off[rows[k] + 1]; }
-};
 
 // Class lists by degree (all known before any histogram is built).
 struct Lists {
@@ -1352,19 +1366,9 @@ static void build_histograms(Context& ctx, const Prepared& P, const Lists& L, co
   EFG_LAUNCH((k_hist_block<kHistThreads, kHistItems>), c[kHB], kHistThreads, 0, s, L.hb, c[kHB], off, P.nd, hkey,
              hcnt, dcnt, bits);
   if (c[kHL]) {
-    // few large rows: CUB segmented sort in place of their slot ranges, then run lengths
-    const int64_t m2 = P.g.m2;
-    EFG_REQUIRE(m2 < (int64_t(1) << 31), "adjacency too large for the segmented sort (2m >= 2^31)");
-    int32_t* snd = ctx.buf("f_snd").as<int32_t>(m2);
-    cub::CountingInputIterator<int64_t> ci(0);
-    cub::TransformInputIterator<int64_t, RowBegin, cub::CountingInputIterator<int64_t>> bi(ci, RowBegin{L.hl, off});
-    cub::TransformInputIterator<int64_t, RowEnd, cub::CountingInputIterator<int64_t>> ei(ci, RowEnd{L.hl, off});
-    size_t tmp = 0;
-    EFG_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(nullptr, tmp, P.nd, snd, (int)m2, (int)c[kHL], bi, ei, s));
-    EFG_REGION("cub::DeviceSegmentedSort::SortKeys", s,
-               EFG_CUDA_CHECK(cub::DeviceSegmentedSort::SortKeys(ctx.buf("cub").get(tmp), tmp, P.nd, snd, (int)m2,
-                                                                 (int)c[kHL], bi, ei, s)));
-    EFG_LAUNCH(k_hist_rle, c[kHL], 256, 0, s, L.hl, c[kHL], off, snd, hkey, hcnt, dcnt);
+    const int smw = kHistWin * (int)sizeof(int32_t);
+    EFG_CUDA_CHECK(cudaFuncSetAttribute(k_hist_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smw));
+    EFG_LAUNCH(k_hist_count, c[kHL], kHistBigThreads, smw, s, L.hl, c[kHL], off, P.nd, hkey, hcnt, dcnt);
   }
 }
 

@@ -779,23 +779,27 @@ k_tri_hub(HubTasks tk, int64_t ntasks, const uint32_t* __restrict__ bitmaps, int
   }
 }
 
-// Triangle probes of each hub (sort key for the hub order), warp per hub,
-// grid-stride over the device-side hub count; total task count.
-__global__ void k_hub_work(const int32_t* __restrict__ hubs, const int64_t* __restrict__ nhubs_dev,
-                           const int64_t* __restrict__ offsets, const int32_t* __restrict__ pc,
-                           int64_t* __restrict__ work, unsigned long long* __restrict__ ntasks) {
-  const int lane = threadIdx.x & 31;
+// Hub task count (degrees only: it is read back with the list counts).
+__global__ void k_hub_count(const int32_t* __restrict__ hubs, const int64_t* __restrict__ nhubs_dev,
+                            const int64_t* __restrict__ offsets, unsigned long long* __restrict__ ntasks) {
   const int64_t nhubs = *nhubs_dev;
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < nhubs; h += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t v = hubs[h];
+    atomicAdd(ntasks, (unsigned long long)ceil_div(offsets[v + 1] - offsets[v], kHubRows));
+  }
+}
+
+// Triangle probes of each hub (sort key for the hub order), warp per hub.
+__global__ void k_hub_work(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ offsets,
+                           const int32_t* __restrict__ pc, int64_t* __restrict__ work) {
+  const int lane = threadIdx.x & 31;
   for (int64_t h = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; h < nhubs;
        h += ((int64_t)gridDim.x * blockDim.x) >> 5) {
     const int32_t v = hubs[h];
     int64_t w = 0;
     for (int64_t p = offsets[v] + lane; p < offsets[v + 1]; p += 32) w += pc[p];
     w = warp_sum(w);
-    if (lane == 0) {
-      work[h] = w;
-      atomicAdd(ntasks, (unsigned long long)ceil_div(offsets[v + 1] - offsets[v], kHubRows));
-    }
+    if (lane == 0) work[h] = w;
   }
 }
 
@@ -1315,27 +1319,40 @@ struct Lists {
 enum Slot {
   kHW, kHS, kHB, kHL, kCG, kCB, kChS, kChB, kTrS, kTr1, kTr2, kTr3, kHubs, kNTasks, kNSlots
 };
+// per-chunk counts of the node-class lists (histograms, chain tables): class
+// c in [kHW, kCB], chunk k -> kNSlots + c * kMaxChunks + k
+constexpr int kNCounts = kNSlots + (kCB + 1) * kMaxChunks;
+__host__ __device__ constexpr int cslot(int c, int k) { return kNSlots + c * kMaxChunks + k; }
 constexpr int64_t kHistWarpMax = 32, kHistBlockMax = kHistThreads * kHistItems, kCtabGroupMax = 64;
 
-static Lists make_lists(Context& ctx, const Prepared& P, SeedRange r, int64_t* cdev, bool seeds) {
+// Node-class lists.  Histogram and chain-table classes are selected per row
+// chunk (chunk k's part of list X starts at X + row[k]), so their kernels can
+// run on a chunk as soon as its neighbours are resident.
+static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, SeedRange r, int64_t* cdev, bool seeds) {
   const int64_t n = P.g.n, cnt = r.hi - r.lo;
   auto list = [&](const char* name, int64_t len) { return ctx.buf(name).as<int32_t>(len > 0 ? len : 1); };
   const int64_t* off = P.g.offsets;
-  const SeedRange all{0, n};
   Lists L{};
   L.hw = list("f_l_hw", n);
   L.hs = list("f_l_hs", n);
   L.hb = list("f_l_hb", n);
   L.hl = list("f_l_hl", n);
-  select_seeds(ctx, all, DegRange{off, -1, kHistWarpMax}, L.hw, cdev + kHW);
-  select_seeds(ctx, all, DegRange{off, kHistWarpMax, 256}, L.hs, cdev + kHS);
-  select_seeds(ctx, all, DegRange{off, 256, kHistBlockMax}, L.hb, cdev + kHB);
-  select_seeds(ctx, all, DegRange{off, kHistBlockMax, INT64_MAX}, L.hl, cdev + kHL);
+  if (seeds) {
+    L.cg = list("f_l_cg", n);
+    L.cb = list("f_l_cb", n);
+  }
+  for (int k = 0; k < stg.nchunks; ++k) {
+    const SeedRange ch{stg.row[k], stg.row[k + 1]};
+    const int64_t o = stg.row[k];
+    select_seeds(ctx, ch, DegRange{off, -1, kHistWarpMax}, L.hw + o, cdev + cslot(kHW, k));
+    select_seeds(ctx, ch, DegRange{off, kHistWarpMax, 256}, L.hs + o, cdev + cslot(kHS, k));
+    select_seeds(ctx, ch, DegRange{off, 256, kHistBlockMax}, L.hb + o, cdev + cslot(kHB, k));
+    select_seeds(ctx, ch, DegRange{off, kHistBlockMax, INT64_MAX}, L.hl + o, cdev + cslot(kHL, k));
+    if (!seeds) continue;
+    select_seeds(ctx, ch, DegRange{off, -1, kCtabGroupMax}, L.cg + o, cdev + cslot(kCG, k));
+    select_seeds(ctx, ch, DegRange{off, kCtabGroupMax, INT64_MAX}, L.cb + o, cdev + cslot(kCB, k));
+  }
   if (!seeds) return L;
-  L.cg = list("f_l_cg", n);
-  L.cb = list("f_l_cb", n);
-  select_seeds(ctx, all, DegRange{off, -1, kCtabGroupMax}, L.cg, cdev + kCG);
-  select_seeds(ctx, all, DegRange{off, kCtabGroupMax, INT64_MAX}, L.cb, cdev + kCB);
   L.chs = list("f_l_chs", cnt);
   L.chb = list("f_l_chb", cnt);
   L.trs = list("f_l_trs", cnt);
@@ -1354,75 +1371,91 @@ static Lists make_lists(Context& ctx, const Prepared& P, SeedRange r, int64_t* c
 }
 
 // Neighbour-degree histograms H_i for every node (slot space, see H build).
-static void build_histograms(Context& ctx, const Prepared& P, const Lists& L, const int64_t* c, int32_t* hkey,
-                             int32_t* hcnt, int32_t* dcnt) {
+static void build_histograms(Context& ctx, const Prepared& P, const Lists& L, const int64_t* c, const Staging& stg,
+                             int k, int32_t* hkey, int32_t* hcnt, int32_t* dcnt) {
   cudaStream_t s = ctx.stream;
   const int B = 256;
   const int64_t* off = P.g.offsets;
-  EFG_LAUNCH(k_hist_warp, ceil_div(c[kHW] * 32, B), B, 0, s, L.hw, c[kHW], off, P.nd, hkey, hcnt, dcnt);
+  const int64_t o = stg.row[k];
+  const int64_t nw = c[cslot(kHW, k)], ns = c[cslot(kHS, k)], nb = c[cslot(kHB, k)], nl = c[cslot(kHL, k)];
+  EFG_LAUNCH(k_hist_warp, ceil_div(nw * 32, B), B, 0, s, L.hw + o, nw, off, P.nd, hkey, hcnt, dcnt);
   int bits = 1;
   while (bits < 31 && (int64_t(1) << bits) <= (int64_t)P.dmax + 1) ++bits;
-  EFG_LAUNCH((k_hist_block<64, 4>), c[kHS], 64, 0, s, L.hs, c[kHS], off, P.nd, hkey, hcnt, dcnt, bits);
-  EFG_LAUNCH((k_hist_block<kHistThreads, kHistItems>), c[kHB], kHistThreads, 0, s, L.hb, c[kHB], off, P.nd, hkey,
-             hcnt, dcnt, bits);
-  if (c[kHL]) {
+  EFG_LAUNCH((k_hist_block<64, 4>), ns, 64, 0, s, L.hs + o, ns, off, P.nd, hkey, hcnt, dcnt, bits);
+  EFG_LAUNCH((k_hist_block<kHistThreads, kHistItems>), nb, kHistThreads, 0, s, L.hb + o, nb, off, P.nd, hkey, hcnt,
+             dcnt, bits);
+  if (nl) {
     const int smw = kHistWin * (int)sizeof(int32_t);
     EFG_CUDA_CHECK(cudaFuncSetAttribute(k_hist_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smw));
-    EFG_LAUNCH(k_hist_count, c[kHL], kHistBigThreads, smw, s, L.hl, c[kHL], off, P.nd, hkey, hcnt, dcnt);
+    EFG_LAUNCH(k_hist_count, nl, kHistBigThreads, smw, s, L.hl + o, nl, off, P.nd, hkey, hcnt, dcnt);
   }
 }
 
 static int64_t read_counts(Context& ctx, const int64_t* cdev, int64_t* c) {
-  EFG_CUDA_CHECK(cudaMemcpyAsync(c, cdev, kNSlots * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
+  EFG_CUDA_CHECK(cudaMemcpyAsync(c, cdev, kNCounts * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.stream));
   EFG_CUDA_CHECK(cudaStreamSynchronize(ctx.stream));
   return 0;
 }
 
 void factorized_work(Context& ctx, Prepared& P, int64_t* d_work) {
   const int64_t n = P.g.n, m2 = P.g.m2 > 0 ? P.g.m2 : 1;
-  int64_t* cdev = ctx.buf("f_counts").as<int64_t>(kNSlots);
-  EFG_CUDA_CHECK(cudaMemsetAsync(cdev, 0, kNSlots * sizeof(int64_t), ctx.stream));
-  Lists L = make_lists(ctx, P, SeedRange{0, n}, cdev, false);
-  int64_t c[kNSlots];
+  Staging one;
+  one.row[1] = n;
+  one.slot[1] = P.g.m2;
+  int64_t* cdev = ctx.buf("f_counts").as<int64_t>(kNCounts);
+  EFG_CUDA_CHECK(cudaMemsetAsync(cdev, 0, kNCounts * sizeof(int64_t), ctx.stream));
+  Lists L = make_lists(ctx, P, one, SeedRange{0, n}, cdev, false);
+  int64_t c[kNCounts];
   read_counts(ctx, cdev, c);
   int32_t* hkey = ctx.buf("f_hkey").as<int32_t>(m2);
   int32_t* hcnt = ctx.buf("f_hcnt").as<int32_t>(m2);
   int32_t* dcnt = ctx.buf("f_dcnt").as<int32_t>(n);
-  build_histograms(ctx, P, L, c, hkey, hcnt, dcnt);
+  build_histograms(ctx, P, L, c, one, 0, hkey, hcnt, dcnt);
   const int B = 256;
   EFG_LAUNCH(k_seed_work, ceil_div(n * 32, B), B, 0, ctx.stream, P.g.offsets, P.pc, dcnt, n, d_work);
 }
 
-// The pass has exactly one host synchronisation after prepare(): every class
-// list (by degree) and the hub task count are produced on the device first
-// and read back in a single copy; the kernels are then launched back to back.
-void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* total, uint8_t* flags,
-                   int64_t* T_out, double* W_out, efg_stats* st) {
+// The pass has two host synchronisations: dmax (prepare_head) and one
+// batched read of every class count; the rest is launched back to back.  With
+// staged host inputs the per-row work (neighbour degrees, histograms, chain
+// tables) of each row chunk runs while the next chunk is still copied.
+PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedRange r, double* ef, int64_t* total,
+                       uint8_t* flags, int64_t* T_out, double* W_out, efg_stats* st) {
   cudaStream_t s = ctx.stream;
-  const int64_t n = P.g.n, m2 = P.g.m2 > 0 ? P.g.m2 : 1;
+  const int64_t n = g.n, m2 = g.m2 > 0 ? g.m2 : 1;
   const int B = 256;
   size_t tmp = 0;
   const int64_t cnt = r.hi - r.lo;
-  if (cnt <= 0) return;
+  Prepared P;
+  if (st) EFG_CUDA_CHECK(cudaEventRecord(ctx.ev[2], s));
+  prepare_head(ctx, g, true, P);
   // ---- phase 1: class lists and counts on the device, one read-back
-  int64_t* cdev = ctx.buf("f_counts").as<int64_t>(kNSlots);
-  EFG_CUDA_CHECK(cudaMemsetAsync(cdev, 0, kNSlots * sizeof(int64_t), s));
-  Lists L = make_lists(ctx, P, r, cdev, true);
-  int64_t* hw = ctx.buf("f_hub_work").as<int64_t>(2 * cnt + 2);
-  EFG_LAUNCH(k_hub_work, 8 * ctx.num_sms, 256, 0, s, L.hub, cdev + kHubs, P.g.offsets, P.pc, hw,
+  int64_t* cdev = ctx.buf("f_counts").as<int64_t>(kNCounts);
+  EFG_CUDA_CHECK(cudaMemsetAsync(cdev, 0, kNCounts * sizeof(int64_t), s));
+  Lists L = make_lists(ctx, P, stg, r, cdev, true);
+  EFG_LAUNCH(k_hub_count, 2 * ctx.num_sms, 256, 0, s, L.hub, cdev + kHubs, g.offsets,
              reinterpret_cast<unsigned long long*>(cdev + kNTasks));
-  int64_t c[kNSlots];
+  int64_t c[kNCounts];
   read_counts(ctx, cdev, c);
-  // ---- phase 2: no further host synchronisation
+  // ---- phase 2: no further host synchronisation; per row chunk as it arrives
   int32_t* hkey = ctx.buf("f_hkey").as<int32_t>(m2);
   int32_t* hcnt = ctx.buf("f_hcnt").as<int32_t>(m2);
   int32_t* dcnt = ctx.buf("f_dcnt").as<int32_t>(n);
-  build_histograms(ctx, P, L, c, hkey, hcnt, dcnt);
-  // 1. chain tables C_i(y): rows with d <= 64 by 8-lane groups, the rest by CTAs
   double* ctab = ctx.buf("f_ctab").as<double>(m2);
-  EFG_LAUNCH(k_ctab_group<8>, ceil_div(c[kCG] * 8, B), B, 0, s, L.cg, c[kCG], P.g.offsets, dcnt, hkey, hcnt, P.deg,
-             P.ftab, ctab);
-  EFG_LAUNCH(k_ctab_block, c[kCB], kCtabThreads, 0, s, L.cb, c[kCB], P.g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab);
+  for (int k = 0; k < stg.nchunks; ++k) {
+    if (stg.ready[k]) EFG_CUDA_CHECK(cudaStreamWaitEvent(s, stg.ready[k], 0));
+    prepare_rows(ctx, P, stg.row[k], stg.row[k + 1], stg.slot[k], stg.slot[k + 1]);
+    build_histograms(ctx, P, L, c, stg, k, hkey, hcnt, dcnt);
+    // chain tables C_i(y): rows with d <= 64 by 8-lane groups, the rest by CTAs
+    const int64_t o = stg.row[k], ng = c[cslot(kCG, k)], nb = c[cslot(kCB, k)];
+    EFG_LAUNCH(k_ctab_group<8>, ceil_div(ng * 8, B), B, 0, s, L.cg + o, ng, g.offsets, dcnt, hkey, hcnt, P.deg,
+               P.ftab, ctab);
+    EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab);
+  }
+  prepare_tail(ctx, P, true);
+  if (st) EFG_CUDA_CHECK(cudaEventRecord(ctx.ev[3], s));
+  const PrepInfo info{P.dmax, P.sum_c2};
+  if (cnt <= 0) return info;
   NodeRec* nrec = ctx.buf("f_nrec").as<NodeRec>(n);
   EFG_LAUNCH(k_node_rec, ceil_div(n, B), B, 0, s, P.g.offsets, P.s1, dcnt, n, nrec);
   FArgs a;
@@ -1464,6 +1497,8 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   int64_t* tstart = nullptr;
   int32_t* hs = nullptr;
   if (nhubs) {
+    int64_t* hw = ctx.buf("f_hub_work").as<int64_t>(2 * nhubs + 2);
+    EFG_LAUNCH(k_hub_work, 8 * ctx.num_sms, 256, 0, s, L.hub, nhubs, g.offsets, P.pc, hw);
     int64_t* hw_sorted = hw + nhubs;
     hs = ctx.buf("f_hub_sorted").as<int32_t>(nhubs);
     EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, hw, hw_sorted, L.hub, hs, nhubs, 0, 64, s));
@@ -1545,6 +1580,7 @@ void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* 
   EFG_LAUNCH(k_chain_warp, ceil_div(c[kChS] * 32, B), B, 0, s, L.chs, c[kChS], a);
   // 5. epilogue
   EFG_LAUNCH(k_epilogue, ceil_div(cnt, B), B, 0, s, a, cnt, ef, total, flags, T_out, W_out);
+  return info;
 }
 
 }  // namespace efg

@@ -47,6 +47,8 @@ struct Context {
   std::map<std::string, DevBuf> bufs;
   std::mutex mu;
   cudaEvent_t ev[16] = {};
+  cudaStream_t copy_stream = nullptr;   // host->device staging of efg_expected_force inputs
+  cudaEvent_t chunk_ev[9] = {};         // offsets + neighbour chunks resident (kMaxChunks + 1)
   Profiler prof;
   DeviceCSR csr;  // resident graph of efg_build_graph / efg_rmat_build
   DevBuf& buf(const std::string& name) { return bufs[name]; }
@@ -95,10 +97,28 @@ void rmat_build_device(Context& ctx, int scale, int64_t avg_degree, const double
 
 // prep.cu
 void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P);
+void prepare_head(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P);
+void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t e0, int64_t e1);
+void prepare_tail(Context& ctx, Prepared& P, bool need_orientation);
+
+// Host inputs arriving on a copy stream in row chunks (efg_expected_force):
+// work on the rows of chunk k may start once ready[k] has fired (null event:
+// already resident).  The offsets are resident before any of it.
+constexpr int kMaxChunks = 8;
+struct Staging {
+  int nchunks = 1;
+  int64_t row[kMaxChunks + 1] = {};   // row bounds
+  int64_t slot[kMaxChunks + 1] = {};  // offsets[row[k]]
+  cudaEvent_t ready[kMaxChunks] = {};
+};
 
 // ef_factor.cu -- factorised cluster-centric engine
-void ef_factorized(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* total, uint8_t* flags,
-                   int64_t* T_out, double* W_out, efg_stats* st);
+struct PrepInfo {
+  int32_t dmax = 0;
+  int64_t sum_c2 = 0;
+};
+PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedRange r, double* ef, int64_t* total,
+                       uint8_t* flags, int64_t* T_out, double* W_out, efg_stats* st);
 
 // ef_direct.cu -- direct per-seed enumeration (original formulation)
 void ef_direct(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* total, uint8_t* flags,

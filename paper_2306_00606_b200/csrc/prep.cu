@@ -34,10 +34,10 @@ __global__ void k_gtab(const double* __restrict__ F, double* __restrict__ G, int
   if (S < len) G[S] = S >= 6 ? F[S - 6] - F[S - 4] : 0.0;
 }
 
-__global__ void k_nd(const int32_t* __restrict__ nbr, int64_t m2, const int32_t* __restrict__ deg,
+__global__ void k_nd(const int32_t* __restrict__ nbr, int64_t e0, int64_t e1, const int32_t* __restrict__ deg,
                      int32_t* __restrict__ nd) {
-  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e < m2) nd[e] = __ldg(deg + nbr[e]);
+  int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e < e1) nd[e] = __ldg(deg + nbr[e]);
 }
 
 __device__ __forceinline__ bool ranks_above(int32_t dj, int32_t j, int32_t di, int32_t i) {
@@ -46,11 +46,11 @@ __device__ __forceinline__ bool ranks_above(int32_t dj, int32_t j, int32_t di, i
 
 // Warp per row: s1[v] = sum of neighbour degrees; dplus[v] = |Adj+(v)|.
 __global__ void k_row_sums(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
-                           const int32_t* __restrict__ nd, int64_t n, int64_t* __restrict__ s1,
+                           const int32_t* __restrict__ nd, int64_t r0, int64_t r1, int64_t* __restrict__ s1,
                            int64_t* __restrict__ dplus) {
   const int lane = threadIdx.x & 31;
-  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (v >= n) return;
+  int64_t v = r0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (v >= r1) return;
   int64_t b = offsets[v], e = offsets[v + 1];
   int32_t dv = (int32_t)(e - b);
   int64_t s = 0;
@@ -242,7 +242,9 @@ struct Choose2 {
 
 }  // namespace
 
-void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P) {
+// Offsets-only part: degrees, dmax (the one host sync), the F/G tables and
+// the rank labels.  Runs while the neighbour arrays may still be in flight.
+void prepare_head(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P) {
   cudaStream_t s = ctx.stream;
   const int B = 256;
   P.g = g;
@@ -272,30 +274,46 @@ void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P)
   EFG_LAUNCH(k_ftab, ceil_div(P.ftab_len, B), B, 0, s, P.ftab, P.ftab_len);
   P.gtab = ctx.buf("gtab").as<double>(P.ftab_len);
   EFG_LAUNCH(k_gtab, ceil_div(P.ftab_len, B), B, 0, s, P.ftab, P.gtab, P.ftab_len);
-  EFG_LAUNCH(k_nd, ceil_div(m2, B), B, 0, s, g.nbr, m2, P.deg, P.nd);
-  int64_t* dplus64 = ctx.buf("dplus64").as<int64_t>(n + 1);
-  EFG_LAUNCH(k_row_sums, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.s1, dplus64);
   if (!need_orientation) return;
   EFG_REQUIRE(m2 / 2 < (int64_t(1) << 31), "more than 2^31-1 edges: oriented adjacency index exceeds int32");
+  uint64_t* key = ctx.buf("rank_key").as<uint64_t>(2 * n);
+  int32_t* val = ctx.buf("rank_val").as<int32_t>(2 * n);
+  EFG_LAUNCH(k_rank_keys, ceil_div(n, B), B, 0, s, P.deg, n, dmax, key, val);
+  int bits = 32;
+  while (bits < 64 && (uint64_t(1) << (bits - 32)) <= (uint64_t)dmax) ++bits;
+  EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, key + n, val, val + n, n, 0, bits, s));
+  EFG_REGION("cub::DeviceRadixSort::SortPairs", s,
+             EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(ctx.buf("cub").get(tmp), tmp, key, key + n, val, val + n,
+                                                            n, 0, bits, s)));
+  P.rank_of = ctx.buf("rank_of").as<int32_t>(n);
+  P.deg_by_rank = ctx.buf("deg_by_rank").as<int32_t>(n);
+  EFG_LAUNCH(k_rank_scatter, ceil_div(n, B), B, 0, s, val + n, n, P.deg, P.rank_of, P.deg_by_rank);
+  P.by_rank = val + n;
+}
+
+// Rows [r0, r1) (slots [e0, e1)) whose neighbours are resident: neighbour
+// degrees, S1 and |Adj+|.
+void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t e0, int64_t e1) {
+  cudaStream_t s = ctx.stream;
+  const int B = 256;
+  int64_t* dplus64 = ctx.buf("dplus64").as<int64_t>(P.g.n + 1);
+  EFG_LAUNCH(k_nd, ceil_div(e1 - e0, B), B, 0, s, P.g.nbr, e0, e1, P.deg, P.nd);
+  EFG_LAUNCH(k_row_sums, ceil_div((r1 - r0) * 32, B), B, 0, s, P.g.offsets, P.g.nbr, P.nd, r0, r1, P.s1, dplus64);
+}
+
+// Everything that needs all neighbours: the label-sorted orientation.
+void prepare_tail(Context& ctx, Prepared& P, bool need_orientation) {
+  if (!need_orientation) return;
+  cudaStream_t s = ctx.stream;
+  const int B = 256;
+  const CSRView& g = P.g;
+  const int64_t n = g.n, m2 = g.m2;
+  int64_t* dplus64 = ctx.buf("dplus64").as<int64_t>(n + 1);
+  size_t tmp = 0;
   P.offp = ctx.buf("offp").as<int64_t>(n + 1);
   EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, dplus64, P.offp, n + 1, s));
   EFG_CUDA_CHECK(cudaMemsetAsync(dplus64 + n, 0, sizeof(int64_t), s));
   EFG_REGION("cub::DeviceScan::ExclusiveSum", s, EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dplus64, P.offp, n + 1, s)));
-  {
-    uint64_t* key = ctx.buf("rank_key").as<uint64_t>(2 * n);
-    int32_t* val = ctx.buf("rank_val").as<int32_t>(2 * n);
-    EFG_LAUNCH(k_rank_keys, ceil_div(n, B), B, 0, s, P.deg, n, dmax, key, val);
-    int bits = 32;
-    while (bits < 64 && (uint64_t(1) << (bits - 32)) <= (uint64_t)dmax) ++bits;
-    EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(nullptr, tmp, key, key + n, val, val + n, n, 0, bits, s));
-    EFG_REGION("cub::DeviceRadixSort::SortPairs", s,
-               EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairs(ctx.buf("cub").get(tmp), tmp, key, key + n, val,
-                                                              val + n, n, 0, bits, s)));
-    P.rank_of = ctx.buf("rank_of").as<int32_t>(n);
-    P.deg_by_rank = ctx.buf("deg_by_rank").as<int32_t>(n);
-    EFG_LAUNCH(k_rank_scatter, ceil_div(n, B), B, 0, s, val + n, n, P.deg, P.rank_of, P.deg_by_rank);
-    P.by_rank = val + n;
-  }
   P.adjj = ctx.buf("adjj").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);
   P.adjd = ctx.buf("adjd").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);
   EFG_LAUNCH(k_fill_adjp, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.offp, P.rank_of, P.adjj,
@@ -314,6 +332,12 @@ void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P)
   P.ps = ctx.buf("ps").as<int64_t>(m2);
   P.pc = ctx.buf("pc").as<int32_t>(m2);
   EFG_LAUNCH(k_slot_plus, ceil_div(m2, B), B, 0, s, g.nbr, m2, P.offp, P.ps, P.pc);
+}
+
+void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P) {
+  prepare_head(ctx, g, need_orientation, P);
+  prepare_rows(ctx, P, 0, g.n, 0, g.m2);
+  prepare_tail(ctx, P, need_orientation);
 }
 
 }  // namespace efg

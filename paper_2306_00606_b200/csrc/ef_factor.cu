@@ -39,14 +39,6 @@ namespace {
 constexpr int kHashSlots = 8192;     // smem hash of Adj(v) for dv <= 4096
 constexpr int kHashMaxDeg = kHashSlots / 2;
 
-// Per-node chain data packed in one 16-byte record (one sector per random
-// gather instead of three): m < 2^31 keeps offsets below 2^32.
-struct __align__(16) NodeRec {
-  int64_t s1;    // sum of neighbour degrees
-  uint32_t off;  // offsets[i]: H_i = hkey/hcnt[off, off + dcnt)
-  int32_t dcnt;  // |D_i|
-};
-
 struct FArgs {
   const int64_t* offsets;
   const int32_t* nbr;
@@ -65,14 +57,16 @@ struct FArgs {
   const int32_t* dcnt;     // |D_i|: H_i = hkey/hcnt[offsets[i], offsets[i] + dcnt[i])
   const int32_t* hkey;
   const int32_t* hcnt;
-  const double* ctab;
-  const NodeRec* nrec;
   const int4* rowhash;     // bucketed hash of Adj+(i) for |Adj+(i)| >= kRevMin, at bucket 2*offp[i]
+  // per node: pushed chain sums (see chain_push) and the stars term
+  const int64_t* s2;
+  const unsigned long long* cwh;
+  const unsigned long long* cwl;
+  const unsigned long long* cp2;
+  const double* cws;
+  double c0;
   int64_t seed_lo;
   // per-seed partials, index v - seed_lo
-  int64_t* Tc;
-  double* Wc;
-  double* Ws;
   int64_t* tri;
   int64_t* Wth;  // W_t in fixed point, two words: (sum of P >> 32, sum of P & (2^32 - 1)), P = rint(G 2^40)
   int64_t* Wtl;
@@ -338,12 +332,6 @@ k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __r
   }
 }
 
-__global__ void k_node_rec(const int64_t* __restrict__ offsets, const int64_t* __restrict__ s1,
-                           const int32_t* __restrict__ dcnt, int64_t n, NodeRec* __restrict__ nrec) {
-  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) nrec[i] = NodeRec{s1[i], (uint32_t)offsets[i], dcnt[i]};
-}
-
 // ---------------------------------------------------------------- per seed
 template <class T>
 __device__ __forceinline__ T warp_sum(T x) {
@@ -365,61 +353,105 @@ __device__ __forceinline__ T block_sum(T x, T* scratch) {
   return r;
 }
 
-// Chain term of seed v (one group per row, slots strided over lanes):
-//   Tc(v) = sum_i (di-1)(dv+di-4) + S1(i) - dv          (chains through i, exact int)
-//   Wc(v) = sum_i C_i(dv),  C_i(dv) = sum_x H_i(x) F(dv+di-4+x) - F(2dv+di-4)
-// C_i(dv) is found by binary search of dv in i's distinct-degree list.
-__device__ __forceinline__ void chain_slot(const FArgs& a, int64_t e, int64_t dv, int64_t& Tc, double& Wc) {
-  const int32_t i = a.nbr[e];
-  const int64_t di = a.nd[e];
-  const NodeRec r = a.nrec[i];
-  Tc += (di - 1) * (dv + di - 4) + r.s1 - dv;
-  int64_t lo = r.off, hi = lo + r.dcnt - 1;
-  while (lo < hi) {  // dv is present: v is a neighbour of i
-    int64_t mid = (lo + hi) >> 1;
-    if (__ldg(a.hkey + mid) < dv) lo = mid + 1; else hi = mid;
-  }
-  Wc += __ldg(a.ctab + lo);
+// Chains, pushed.  Seed v's chain term is W_c(v) = sum_{i in A(v)} C_i(dv):
+// instead of every seed searching dv in each neighbour's table, each row i
+// pushes C_i(d_v) to every neighbour v right after computing its table
+// (rows are local: keys and values are contiguous, the lookup stays in
+// registers / shared memory).  Pushed values are summed in fixed point per
+// node, two words (hi = floor(x), lo = frac(x) 2^32, x = C 2^-e) with a
+// per-degree scale 2^e >= dv dmax F(3 dmax) 2^-62 >= W_c(v) 2^-62, so the
+// integer sums cannot overflow and keep >= 2^-94 of the bound: exact to far
+// below the EF tolerance, and independent of the order of the pushes.  The
+// exact integer part of the chain count, sum_i S1(i), is pushed alongside.
+struct ChainAcc {
+  unsigned long long* wh;  // [n] sum of hi words
+  unsigned long long* wl;  // [n] sum of lo words
+  unsigned long long* p2;  // [n] sum_{i in A(v)} S1(i)
+  double* ws;              // [n] stars: sum_b h_b C_v(x_b)
+  double c0;               // dmax F(3 dmax)
+};
+
+__host__ __device__ __forceinline__ int chain_exp(int64_t dv, double c0) {
+  return ilogb((double)dv * c0) + 1 - 62;
 }
 
-__global__ void k_chain_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
+__device__ __forceinline__ void chain_push(const ChainAcc& ca, int32_t v, int32_t dv, double val, int64_t s1i) {
+  const double x = ldexp(val, -chain_exp(dv, ca.c0));
+  const double f = floor(x);
+  atomicAdd(ca.wh + v, (unsigned long long)(int64_t)f);
+  atomicAdd(ca.wl + v, (unsigned long long)(int64_t)ldexp(x - f, 32));
+  atomicAdd(ca.p2 + v, (unsigned long long)s1i);
+}
+
+// d <= 32: warp per row i; lane k holds H_i's k-th key and C_i value, lane
+// e its slot's neighbour.  Also writes the stars term of i.
+__global__ void k_push_warp(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
+                            const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd,
+                            const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey,
+                            const int32_t* __restrict__ hcnt, const double* __restrict__ ctab,
+                            const int64_t* __restrict__ s1, ChainAcc ca) {
   const int lane = threadIdx.x & 31;
-  int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (q >= count) return;
-  const int32_t v = seeds[q];
-  const int64_t b = a.offsets[v], e = a.offsets[v + 1];
-  int64_t Tc = 0;
-  double Wc = 0.0, Ws = 0.0;
-  for (int64_t p = b + lane; p < e; p += 32) chain_slot(a, p, e - b, Tc, Wc);
-  for (int64_t h = b + lane; h < b + a.dcnt[v]; h += 32) Ws += (double)a.hcnt[h] * a.ctab[h];
-  Tc = warp_sum(Tc);
-  Wc = warp_sum(Wc);
-  Ws = warp_sum(Ws);
-  if (lane == 0) {
-    a.Tc[v - a.seed_lo] = Tc;
-    a.Wc[v - a.seed_lo] = Wc;
-    a.Ws[v - a.seed_lo] = Ws;
+  const int32_t i = rows[q];
+  const int64_t b = offsets[i];
+  const int d = (int)(offsets[i + 1] - b);
+  const int D = dcnt[i];
+  int32_t key = -1;
+  double c = 0.0, hc = 0.0;
+  if (lane < D) {
+    key = hkey[b + lane];
+    c = ctab[b + lane];
+    hc = (double)hcnt[b + lane] * c;
   }
+  hc = warp_sum(hc);
+  if (lane == 0) ca.ws[i] = hc;
+  int32_t y = -2, v = 0;
+  if (lane < d) {
+    y = nd[b + lane];
+    v = nbr[b + lane];
+  }
+  int idx = 0;
+  for (int k = 0; k < D; ++k)
+    if (__shfl_sync(0xffffffffu, key, k) == y) idx = k;
+  const double val = __shfl_sync(0xffffffffu, c, idx);
+  if (lane < d) chain_push(ca, v, y, val, s1[i]);
 }
 
-__global__ void __launch_bounds__(256) k_chain_block(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
-  __shared__ int64_t red_i[8];
-  __shared__ double red_d[8];
+// d > 32: CTA per row; H_i's keys in shared memory (global beyond 4096).
+constexpr int kPushThreads = 128, kPushKeys = 4096;
+__global__ void __launch_bounds__(kPushThreads)
+k_push_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
+             const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd, const int32_t* __restrict__ dcnt,
+             const int32_t* __restrict__ hkey, const int32_t* __restrict__ hcnt, const double* __restrict__ ctab,
+             const int64_t* __restrict__ s1, ChainAcc ca) {
+  __shared__ int32_t sk[kPushKeys];
+  __shared__ double red[kPushThreads / 32];
   const int64_t q = blockIdx.x;
   if (q >= count) return;
-  const int32_t v = seeds[q];
-  const int64_t b = a.offsets[v], e = a.offsets[v + 1];
-  int64_t Tc = 0;
-  double Wc = 0.0, Ws = 0.0;
-  for (int64_t p = b + threadIdx.x; p < e; p += 256) chain_slot(a, p, e - b, Tc, Wc);
-  for (int64_t h = b + threadIdx.x; h < b + a.dcnt[v]; h += 256) Ws += (double)a.hcnt[h] * a.ctab[h];
-  Tc = block_sum<256>(Tc, red_i);
-  Wc = block_sum<256>(Wc, red_d);
-  Ws = block_sum<256>(Ws, red_d);
-  if (threadIdx.x == 0) {
-    a.Tc[v - a.seed_lo] = Tc;
-    a.Wc[v - a.seed_lo] = Wc;
-    a.Ws[v - a.seed_lo] = Ws;
+  const int32_t i = rows[q];
+  const int64_t b = offsets[i];
+  const int d = (int)(offsets[i + 1] - b);
+  const int D = dcnt[i];
+  const int32_t* keys = D <= kPushKeys ? sk : hkey + b;
+  double hc = 0.0;
+  for (int k = threadIdx.x; k < D; k += kPushThreads) {
+    const int32_t kk = hkey[b + k];
+    if (D <= kPushKeys) sk[k] = kk;
+    hc += (double)hcnt[b + k] * ctab[b + k];
+  }
+  hc = block_sum<kPushThreads>(hc, red);  // syncs: sk is complete afterwards
+  if (threadIdx.x == 0) ca.ws[i] = hc;
+  __syncthreads();
+  const int64_t s1i = s1[i];
+  for (int p = threadIdx.x; p < d; p += kPushThreads) {
+    const int32_t y = nd[b + p];
+    int lo = 0, hi = D - 1;  // y is present: v is a neighbour of i
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (keys[mid] < y) lo = mid + 1; else hi = mid;
+    }
+    chain_push(ca, nbr[b + p], y, __ldg(ctab + b + lo), s1i);
   }
 }
 
@@ -1249,14 +1281,20 @@ __global__ void k_epilogue(FArgs a, int64_t count, double* __restrict__ ef, int6
   const int64_t dv = a.offsets[v + 1] - a.offsets[v];
   const int64_t s1v = a.s1[v];
   const int64_t tri = a.tri[q];
-  const int64_t T = dv * (dv - 1) * (dv - 4) + 2 * (dv - 1) * s1v + a.Tc[q] - 8 * tri;
+  // chains: sum_i [(di-1)(dv+di-4) + S1(i) - dv] = S2 + (dv-5) S1 - 2dv^2 + 4dv + sum_i S1(i)
+  const int64_t Tc = a.s2[v] + (dv - 5) * s1v - 2 * dv * dv + 4 * dv + (int64_t)a.cp2[v];
+  const int64_t T = dv * (dv - 1) * (dv - 4) + 2 * (dv - 1) * s1v + Tc - 8 * tri;
   const int64_t mass = dv * (dv - 1) + s1v - dv;
   // W_t = X 2^-40 with X = Wth 2^32 + Wtl, converted from the canonical split
   // (0 <= lo < 2^32): a function of the exact integer only, so every triangle
   // path and every sharding gives the same double
   const int64_t xh = a.Wth[q] + (a.Wtl[q] >> 32), xl = a.Wtl[q] & 0xffffffffll;
   const double Wt = ldexp((double)xh, 32 - kListScale) + ldexp((double)xl, -kListScale);
-  const double W = (a.Ws[q] + a.Wc[q]) + 4.0 * Wt;
+  // W_c from its two words, canonical split likewise
+  const int64_t ch = (int64_t)a.cwh[v] + ((int64_t)a.cwl[v] >> 32), cl = (int64_t)a.cwl[v] & 0xffffffffll;
+  const int ce = chain_exp(dv, a.c0);
+  const double Wc = dv > 0 ? ldexp((double)ch, ce) + ldexp((double)cl, ce - 32) : 0.0;
+  const double W = (a.cws[v] + Wc) + 4.0 * Wt;
   double e = 0.0;
   // entropy >= 0: clamp the last-ulp cancellation of ln T - W/T when only one
   // positive-degree cluster class exists (EF mathematically 0)
@@ -1313,11 +1351,10 @@ __global__ void k_seed_work(const int64_t* __restrict__ offsets, const int32_t* 
 struct Lists {
   int32_t *hw, *hs, *hb, *hl;     // histogram rows: d <= 32, <= 256, <= 2048, > 2048 (all nodes)
   int32_t *cg, *cb;               // chain tables: d <= 64, > 64 (all nodes)
-  int32_t *chs, *chb;             // chain sums: seeds dv <= 1024, > 1024
   int32_t *trs, *tr1, *tr2, *tr3, *hub;  // triangles
 };
 enum Slot {
-  kHW, kHS, kHB, kHL, kCG, kCB, kChS, kChB, kTrS, kTr1, kTr2, kTr3, kHubs, kNTasks, kNSlots
+  kHW, kHS, kHB, kHL, kCG, kCB, kTrS, kTr1, kTr2, kTr3, kHubs, kNTasks, kNSlots
 };
 // per-chunk counts of the node-class lists (histograms, chain tables): class
 // c in [kHW, kCB], chunk k -> kNSlots + c * kMaxChunks + k
@@ -1353,15 +1390,11 @@ static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, See
     select_seeds(ctx, ch, DegRange{off, kCtabGroupMax, INT64_MAX}, L.cb + o, cdev + cslot(kCB, k));
   }
   if (!seeds) return L;
-  L.chs = list("f_l_chs", cnt);
-  L.chb = list("f_l_chb", cnt);
   L.trs = list("f_l_trs", cnt);
   L.tr1 = list("f_l_tr1", cnt);
   L.tr2 = list("f_l_tr2", cnt);
   L.tr3 = list("f_l_tr3", cnt);
   L.hub = list("f_l_hub", cnt);
-  select_seeds(ctx, r, DegRange{off, -1, 1024}, L.chs, cdev + kChS);
-  select_seeds(ctx, r, DegRange{off, 1024, INT64_MAX}, L.chb, cdev + kChB);
   select_seeds(ctx, r, DegRange{off, -1, 32}, L.trs, cdev + kTrS);
   select_seeds(ctx, r, DegRange{off, 32, 256}, L.tr1, cdev + kTr1);
   select_seeds(ctx, r, DegRange{off, 256, 1024}, L.tr2, cdev + kTr2);
@@ -1442,6 +1475,17 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   int32_t* hcnt = ctx.buf("f_hcnt").as<int32_t>(m2);
   int32_t* dcnt = ctx.buf("f_dcnt").as<int32_t>(n);
   double* ctab = ctx.buf("f_ctab").as<double>(m2);
+  ChainAcc ca;
+  {
+    unsigned long long* acc = ctx.buf("f_chain_acc").as<unsigned long long>(3 * n);
+    EFG_CUDA_CHECK(cudaMemsetAsync(acc, 0, 3 * n * sizeof(unsigned long long), s));
+    ca.wh = acc;
+    ca.wl = acc + n;
+    ca.p2 = acc + 2 * n;
+    ca.ws = ctx.buf("f_chain_ws").as<double>(n);
+    const double d3 = 3.0 * (P.dmax > 1 ? P.dmax : 1);
+    ca.c0 = (P.dmax > 1 ? P.dmax : 1) * d3 * log(d3);
+  }
   for (int k = 0; k < stg.nchunks; ++k) {
     if (stg.ready[k]) EFG_CUDA_CHECK(cudaStreamWaitEvent(s, stg.ready[k], 0));
     prepare_rows(ctx, P, stg.row[k], stg.row[k + 1], stg.slot[k], stg.slot[k + 1]);
@@ -1451,13 +1495,21 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     EFG_LAUNCH(k_ctab_group<8>, ceil_div(ng * 8, B), B, 0, s, L.cg + o, ng, g.offsets, dcnt, hkey, hcnt, P.deg,
                P.ftab, ctab);
     EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab);
+    // chains pushed from the rows whose tables are now complete
+    const int64_t pw = c[cslot(kHW, k)], ps1 = c[cslot(kHS, k)], pb = c[cslot(kHB, k)], pl = c[cslot(kHL, k)];
+    EFG_LAUNCH(k_push_warp, ceil_div(pw * 32, B), B, 0, s, L.hw + o, pw, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt,
+               ctab, P.s1, ca);
+    EFG_LAUNCH(k_push_block, ps1, kPushThreads, 0, s, L.hs + o, ps1, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,
+               P.s1, ca);
+    EFG_LAUNCH(k_push_block, pb, kPushThreads, 0, s, L.hb + o, pb, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,
+               P.s1, ca);
+    EFG_LAUNCH(k_push_block, pl, kPushThreads, 0, s, L.hl + o, pl, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,
+               P.s1, ca);
   }
   prepare_tail(ctx, P, true);
   if (st) EFG_CUDA_CHECK(cudaEventRecord(ctx.ev[3], s));
   const PrepInfo info{P.dmax, P.sum_c2};
   if (cnt <= 0) return info;
-  NodeRec* nrec = ctx.buf("f_nrec").as<NodeRec>(n);
-  EFG_LAUNCH(k_node_rec, ceil_div(n, B), B, 0, s, P.g.offsets, P.s1, dcnt, n, nrec);
   FArgs a;
   a.offsets = P.g.offsets;
   a.nbr = P.g.nbr;
@@ -1475,12 +1527,13 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   a.dcnt = dcnt;
   a.hkey = hkey;
   a.hcnt = hcnt;
-  a.ctab = ctab;
-  a.nrec = nrec;
   a.seed_lo = r.lo;
-  a.Tc = ctx.buf("f_Tc").as<int64_t>(cnt);
-  a.Wc = ctx.buf("f_Wc").as<double>(cnt);
-  a.Ws = ctx.buf("f_Ws").as<double>(cnt);
+  a.s2 = P.s2;
+  a.cwh = ca.wh;
+  a.cwl = ca.wl;
+  a.cp2 = ca.p2;
+  a.cws = ca.ws;
+  a.c0 = ca.c0;
   a.tri = ctx.buf("f_tri").as<int64_t>(cnt);
   a.Wth = ctx.buf("f_Wth").as<int64_t>(cnt);
   a.Wtl = ctx.buf("f_Wtl").as<int64_t>(cnt);
@@ -1576,8 +1629,6 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     EFG_LAUNCH(k_tri_warp, ceil_div(c[kTrS], kTriWarps), kTriWarps * 32, 0, s, L.trs, c[kTrS], a);
   }
   // 3. chains (and stars, from the seed's own chain table): warp per row (dv <= 1024), CTA per row above
-  EFG_LAUNCH(k_chain_block, c[kChB], 256, 0, s, L.chb, c[kChB], a);
-  EFG_LAUNCH(k_chain_warp, ceil_div(c[kChS] * 32, B), B, 0, s, L.chs, c[kChS], a);
   // 5. epilogue
   EFG_LAUNCH(k_epilogue, ceil_div(cnt, B), B, 0, s, a, cnt, ef, total, flags, T_out, W_out);
   return info;

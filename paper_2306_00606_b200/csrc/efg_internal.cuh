@@ -70,6 +70,7 @@ struct Prepared {
   int32_t* deg = nullptr;       // [n]
   int32_t* nd = nullptr;        // [2m]  degree of each adjacency entry
   int64_t* s1 = nullptr;        // [n]   sum of neighbour degrees
+  int64_t* s2 = nullptr;        // [n]   sum of squared neighbour degrees
   double* ftab = nullptr;       // [3*dmax+8]  F[d] = d ln d (0 for d = 0)
   double* gtab = nullptr;       // [3*dmax+8]  G[S] = F(S-6) - F(S-4)
   int64_t ftab_len = 0;

@@ -47,25 +47,28 @@ __device__ __forceinline__ bool ranks_above(int32_t dj, int32_t j, int32_t di, i
 // Warp per row: s1[v] = sum of neighbour degrees; dplus[v] = |Adj+(v)|.
 __global__ void k_row_sums(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
                            const int32_t* __restrict__ nd, int64_t r0, int64_t r1, int64_t* __restrict__ s1,
-                           int64_t* __restrict__ dplus) {
+                           int64_t* __restrict__ s2, int64_t* __restrict__ dplus) {
   const int lane = threadIdx.x & 31;
   int64_t v = r0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (v >= r1) return;
   int64_t b = offsets[v], e = offsets[v + 1];
   int32_t dv = (int32_t)(e - b);
-  int64_t s = 0;
+  int64_t s = 0, q = 0;
   int cnt = 0;
   for (int64_t p = b + lane; p < e; p += 32) {
     int32_t dj = nd[p];
     s += dj;
+    q += (int64_t)dj * dj;
     cnt += ranks_above(dj, nbr[p], dv, (int32_t)v);
   }
   for (int o = 16; o; o >>= 1) {
     s += __shfl_xor_sync(0xffffffffu, s, o);
+    q += __shfl_xor_sync(0xffffffffu, q, o);
     cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
   }
   if (lane == 0) {
     s1[v] = s;
+    s2[v] = q;
     dplus[v] = cnt;
   }
 }
@@ -252,6 +255,7 @@ void prepare_head(Context& ctx, const CSRView& g, bool need_orientation, Prepare
   P.deg = ctx.buf("deg").as<int32_t>(n);
   P.nd = ctx.buf("nd").as<int32_t>(m2);
   P.s1 = ctx.buf("s1").as<int64_t>(n);
+  P.s2 = ctx.buf("s2").as<int64_t>(n);
   EFG_LAUNCH(k_deg, ceil_div(n, B), B, 0, s, g.offsets, n, P.deg);
   // dmax -> F table length (cluster degree <= 3*dmax - 4)
   int32_t* dmax_d = ctx.buf("dmax").as<int32_t>(1);
@@ -298,7 +302,8 @@ void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t e0,
   const int B = 256;
   int64_t* dplus64 = ctx.buf("dplus64").as<int64_t>(P.g.n + 1);
   EFG_LAUNCH(k_nd, ceil_div(e1 - e0, B), B, 0, s, P.g.nbr, e0, e1, P.deg, P.nd);
-  EFG_LAUNCH(k_row_sums, ceil_div((r1 - r0) * 32, B), B, 0, s, P.g.offsets, P.g.nbr, P.nd, r0, r1, P.s1, dplus64);
+  EFG_LAUNCH(k_row_sums, ceil_div((r1 - r0) * 32, B), B, 0, s, P.g.offsets, P.g.nbr, P.nd, r0, r1, P.s1, P.s2,
+             dplus64);
 }
 
 // Everything that needs all neighbours: the label-sorted orientation.

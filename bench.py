@@ -7,9 +7,12 @@ Contract (one JSON line on rank 0):
 A "step" is one full-graph EF pass (every seed: ef, cluster_total, flags) over
 the device-resident CSR of BASELINE.json's configs[2] graph (R-MAT scale 22,
 avg degree 21, seed 0: n=2,181,017, m=44,040,192; edge set bit-identical to
-the reference generator, verified by sha256 fingerprint).  N>1: seeds are
-sharded by balanced work prefix (K2) and gathered with one NCCL all-gather, so
-per-step work is the whole graph for any N ("strong" scaling of a fixed job).
+the reference generator, verified by sha256 fingerprint).  N>1: each rank
+runs one part of the whole-graph pass (its nodes' chain tables and pushes,
+its share of the triangle-listing work units) and one NCCL all-reduce sums
+the per-node integer words; every rank then finishes all seeds (direct
+engine: seeds sharded by balanced work prefix, K2, and one all-gather).
+Per-step work is the whole graph for any N ("strong" scaling of a fixed job).
 
 value       = seeds/s over the timed steps (inputs resident in HBM), max over ranks
 e2e         = seeds/s through the public API ef_cluster_centric(g) from pinned
@@ -302,7 +305,7 @@ def main():
     import paper_2306_00606_b200 as efg
     from paper_2306_00606_b200 import _native
     from paper_2306_00606_b200 import device as D
-    from paper_2306_00606_b200.distributed import ef_sharded
+    from paper_2306_00606_b200.distributed import ef_distributed, ef_sharded
 
     rank, world, local = env_rank()
     torch.cuda.set_device(local)
@@ -352,6 +355,8 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def step():
+        if world > 1 and args.engine == "factorized":
+            return ef_distributed(dg)  # parts of the whole-graph pass + one all-reduce of integer words
         return ef_sharded(dg, engine=args.engine, bounds=bounds)
 
     for _ in range(args.warmup):
@@ -427,12 +432,14 @@ def main():
     b_alg = int(algorithmic_bytes_per_seed(offs, nbrs).sum())
     model = kernel_bytes_model(offs, nbrs) if args.engine == "factorized" else {}
     dom_ms = dom[1]["ms"] / max(dom[1]["launches"], 1)
-    dom_bytes = model.get(dom[0], {}).get("bytes")
+    dom_base = dom[0].split("<")[0].strip("() ")  # live names carry template arguments (k_mid_block<false>)
+    dom_bytes = model.get(dom_base, {}).get("bytes")
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "dram_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom[0])
+            tj = json.load(open(tpath))
+            traffic = tj.get(dom[0], tj.get(dom_base))
         except (OSError, ValueError):
             traffic = None
     roofline = {
@@ -461,7 +468,9 @@ def main():
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64+int64", "data": "synthetic",
         "config": {"workload": CONFIGS[args.config], "n": n, "m": m, "engine": args.engine,
-                   "parallelism": f"seed-sharded x{world}", "l2": "flushed between timed steps (256 MB write)",
+                   "parallelism": (f"whole-graph pass in {world} parts + 1 all-reduce" if world > 1 and args.engine == "factorized"
+                                   else f"seed-sharded x{world}"),
+                   "l2": "flushed between timed steps (256 MB write)",
                    "graph_sha256_matches_reference": sha_ok},
         "e2e": e2e,
         "roofline": roofline,

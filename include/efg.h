@@ -110,6 +110,23 @@ EFG_API int efg_expected_force_device(efg_ctx *ctx, const int64_t *d_offsets, co
 EFG_API int efg_shard_bounds(efg_ctx *ctx, const int64_t *d_offsets, const int32_t *d_neighbors, int64_t n,
                      int32_t engine, int32_t parts, int64_t *bounds_out);
 
+/* Distributed whole-graph pass (factorized engine, one part per device):
+ * efg_ef_partial computes part `part` of `nparts` -- the chain tables and
+ * pushes of the nodes v % nparts == part and the triangles listed by every
+ * nparts-th work unit -- into d_words (uint64[EFG_DIST_WORDS * n], exact
+ * integer sums) and d_ws (f64[n], nonzero only at the part's nodes).  The
+ * caller sums both over all parts (one all-reduce: integer addition and
+ * disjoint supports, so the sum is exact and order-free), then
+ * efg_ef_finish turns the sums into the outputs of seeds [seed_lo, seed_hi).
+ * The result equals efg_expected_force_device bitwise.  No reference
+ * counterpart. */
+#define EFG_DIST_WORDS 7
+EFG_API int efg_ef_partial(efg_ctx *ctx, const int64_t *d_offsets, const int32_t *d_neighbors, int64_t n,
+                           int32_t part, int32_t nparts, uint64_t *d_words, double *d_ws, efg_stats *stats);
+EFG_API int efg_ef_finish(efg_ctx *ctx, const int64_t *d_offsets, const int32_t *d_neighbors, int64_t n,
+                          int64_t seed_lo, int64_t seed_hi, const uint64_t *d_words, const double *d_ws,
+                          double *d_ef, int64_t *d_cluster_total, uint8_t *d_flags, int64_t *d_T, double *d_W);
+
 /* K5: key-node ranking -- the k largest EF values, ties to the smaller id,
  * i.e. np.lexsort((ids, -ef))[:k] (cf. analysis.py:101, :240).  ids_out is
  * host int64[k].  The _device form reads a device ef array. */

@@ -400,6 +400,60 @@ int efg_expected_force_device(efg_ctx* ctx, const int64_t* d_offsets, const int3
   });
 }
 
+int efg_ef_partial(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n, int32_t part,
+                   int32_t nparts, uint64_t* d_words, double* d_ws, efg_stats* stats) {
+  if (n < 0 || nparts < 1 || part < 0 || part >= nparts) return fail(efg::EFG_INVALID, "bad part");
+  if (n > 0 && (!d_words || !d_ws)) return fail(efg::EFG_INVALID, "null output array");
+  static_assert(EFG_DIST_WORDS == efg::kDistWords, "word count");
+  return guarded(ctx, [&](Context& c) {
+    efg::g_launches = 0;
+    if (stats) std::memset(stats, 0, sizeof *stats);
+    if (n == 0) return;
+    int64_t off_n = 0;
+    EFG_CUDA_CHECK(cudaMemcpyAsync(&off_n, d_offsets + n, sizeof off_n, cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    efg::CSRView g;
+    g.n = n;
+    g.m2 = off_n;
+    g.offsets = d_offsets;
+    g.nbr = d_neighbors;
+    efg::DistPart dp;
+    dp.part = part;
+    dp.nparts = nparts;
+    dp.words = reinterpret_cast<unsigned long long*>(d_words);
+    dp.ws = d_ws;
+    if (stats) EFG_CUDA_CHECK(cudaEventRecord(c.ev[0], c.stream));
+    efg::ef_factorized(c, g, resident(g), efg::SeedRange{0, n}, nullptr, nullptr, nullptr, nullptr, nullptr, stats,
+                       &dp);
+    if (stats) {
+      EFG_CUDA_CHECK(cudaEventRecord(c.ev[6], c.stream));
+      EFG_CUDA_CHECK(cudaEventSynchronize(c.ev[6]));
+      stats->ms_device = elapsed(c.ev[0], c.ev[6]);
+      stats->launches = efg::g_launches;
+      stats->engine = EFG_ENGINE_FACTORIZED;
+    }
+  });
+}
+
+int efg_ef_finish(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n, int64_t seed_lo,
+                  int64_t seed_hi, const uint64_t* d_words, const double* d_ws, double* d_ef,
+                  int64_t* d_cluster_total, uint8_t* d_flags, int64_t* d_T, double* d_W) {
+  if (n < 0 || seed_lo < 0 || seed_hi < seed_lo || seed_hi > n) return fail(efg::EFG_INVALID, "bad seed range");
+  return guarded(ctx, [&](Context& c) {
+    if (n == 0 || seed_hi == seed_lo) return;
+    int64_t off_n = 0;
+    EFG_CUDA_CHECK(cudaMemcpyAsync(&off_n, d_offsets + n, sizeof off_n, cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    efg::CSRView g;
+    g.n = n;
+    g.m2 = off_n;
+    g.offsets = d_offsets;
+    g.nbr = d_neighbors;
+    efg::ef_finish(c, g, efg::SeedRange{seed_lo, seed_hi}, reinterpret_cast<const unsigned long long*>(d_words), d_ws,
+                   d_ef, d_cluster_total, d_flags, d_T, d_W);
+  });
+}
+
 int efg_shard_bounds(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n, int32_t engine,
                      int32_t parts, int64_t* bounds_out) {
   if (parts < 1 || !bounds_out || n < 0) return fail(efg::EFG_INVALID, "bad shard arguments");

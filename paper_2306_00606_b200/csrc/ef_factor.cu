@@ -929,6 +929,8 @@ struct MArgs {
   unsigned long long* acc;  // [4 n] per node: (hi, lo, count, pad)
   int64_t n, n32;           // labels < n32: degree > 32
   int64_t nhubs, ntasks;    // labels < nhubs come as ntasks row-range tasks
+  int32_t part, nparts;     // distributed pass: this part takes work units u with u % nparts == part
+  int32_t nunits;           // k_mid_block work units: ntasks + (n32 - nhubs)
 };
 
 __global__ void k_gfix(const double* __restrict__ G, int64_t len, int64_t* __restrict__ PT) {
@@ -1075,7 +1077,7 @@ k_mid_warp(MArgs a) {
   __shared__ int64_t sP[kMidWarps][32];
   __shared__ uint32_t sC[kMidWarps][32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t r = a.n32 + (int64_t)blockIdx.x * kMidWarps + w;
+  const int64_t r = a.n32 + ((int64_t)blockIdx.x * kMidWarps + w) * a.nparts + a.part;
   if (r >= a.n) return;
   const int32_t v = __ldg(a.by_rank + r);
   const int64_t ob = __ldg(a.offsets + v);
@@ -1146,6 +1148,7 @@ struct MidSmem {
   int32_t nrows;
 };
 
+template <bool PART>
 __global__ void __launch_bounds__(kMidThreads)
 k_mid_block(MArgs a, HubTasks tk) {
   __shared__ MidSmem sm;
@@ -1157,12 +1160,15 @@ k_mid_block(MArgs a, HubTasks tk) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   constexpr int NW = kMidThreads / 32;
   int32_t v, x0, x1;
-  if (blockIdx.x < a.ntasks) {  // a row range of a hub
-    v = tk.seed[blockIdx.x];
-    x0 = tk.x0[blockIdx.x];
-    x1 = tk.x1[blockIdx.x];
+  // work unit of this part (PART: grid sized per part, units u % nparts == part)
+  const int32_t unit = PART ? (int32_t)blockIdx.x * a.nparts + a.part : (int32_t)blockIdx.x;
+  if (PART && unit >= a.nunits) return;
+  if (unit < a.ntasks) {  // a row range of a hub
+    v = tk.seed[unit];
+    x0 = tk.x0[unit];
+    x1 = tk.x1[unit];
   } else {
-    v = __ldg(a.by_rank + a.nhubs + (blockIdx.x - a.ntasks));
+    v = __ldg(a.by_rank + a.nhubs + (unit - a.ntasks));
     x0 = 0;
     x1 = (int32_t)(__ldg(a.offsets + v + 1) - __ldg(a.offsets + v));
   }
@@ -1308,10 +1314,11 @@ __global__ void k_epilogue(FArgs a, int64_t count, double* __restrict__ ef, int6
 
 struct DegRange {
   const int64_t* offsets;
-  int64_t lo, hi;  // lo < dv <= hi
+  int64_t lo, hi;           // lo < dv <= hi
+  int32_t nparts = 1, part = 0;  // and v % nparts == part
   __host__ __device__ bool operator()(const int32_t& v) const {
     int64_t d = offsets[v + 1] - offsets[v];
-    return d > lo && d <= hi;
+    return d > lo && d <= hi && v % nparts == part;
   }
 };
 
@@ -1365,7 +1372,8 @@ constexpr int64_t kHistWarpMax = 32, kHistBlockMax = kHistThreads * kHistItems, 
 // Node-class lists.  Histogram and chain-table classes are selected per row
 // chunk (chunk k's part of list X starts at X + row[k]), so their kernels can
 // run on a chunk as soon as its neighbours are resident.
-static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, SeedRange r, int64_t* cdev, bool seeds) {
+static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, SeedRange r, int64_t* cdev, bool seeds,
+                        int32_t nparts = 1, int32_t part = 0) {
   const int64_t n = P.g.n, cnt = r.hi - r.lo;
   auto list = [&](const char* name, int64_t len) { return ctx.buf(name).as<int32_t>(len > 0 ? len : 1); };
   const int64_t* off = P.g.offsets;
@@ -1381,13 +1389,13 @@ static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, See
   for (int k = 0; k < stg.nchunks; ++k) {
     const SeedRange ch{stg.row[k], stg.row[k + 1]};
     const int64_t o = stg.row[k];
-    select_seeds(ctx, ch, DegRange{off, -1, kHistWarpMax}, L.hw + o, cdev + cslot(kHW, k));
-    select_seeds(ctx, ch, DegRange{off, kHistWarpMax, 256}, L.hs + o, cdev + cslot(kHS, k));
-    select_seeds(ctx, ch, DegRange{off, 256, kHistBlockMax}, L.hb + o, cdev + cslot(kHB, k));
-    select_seeds(ctx, ch, DegRange{off, kHistBlockMax, INT64_MAX}, L.hl + o, cdev + cslot(kHL, k));
+    select_seeds(ctx, ch, DegRange{off, -1, kHistWarpMax, nparts, part}, L.hw + o, cdev + cslot(kHW, k));
+    select_seeds(ctx, ch, DegRange{off, kHistWarpMax, 256, nparts, part}, L.hs + o, cdev + cslot(kHS, k));
+    select_seeds(ctx, ch, DegRange{off, 256, kHistBlockMax, nparts, part}, L.hb + o, cdev + cslot(kHB, k));
+    select_seeds(ctx, ch, DegRange{off, kHistBlockMax, INT64_MAX, nparts, part}, L.hl + o, cdev + cslot(kHL, k));
     if (!seeds) continue;
-    select_seeds(ctx, ch, DegRange{off, -1, kCtabGroupMax}, L.cg + o, cdev + cslot(kCG, k));
-    select_seeds(ctx, ch, DegRange{off, kCtabGroupMax, INT64_MAX}, L.cb + o, cdev + cslot(kCB, k));
+    select_seeds(ctx, ch, DegRange{off, -1, kCtabGroupMax, nparts, part}, L.cg + o, cdev + cslot(kCG, k));
+    select_seeds(ctx, ch, DegRange{off, kCtabGroupMax, INT64_MAX, nparts, part}, L.cb + o, cdev + cslot(kCB, k));
   }
   if (!seeds) return L;
   L.trs = list("f_l_trs", cnt);
@@ -1453,7 +1461,7 @@ void factorized_work(Context& ctx, Prepared& P, int64_t* d_work) {
 // staged host inputs the per-row work (neighbour degrees, histograms, chain
 // tables) of each row chunk runs while the next chunk is still copied.
 PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedRange r, double* ef, int64_t* total,
-                       uint8_t* flags, int64_t* T_out, double* W_out, efg_stats* st) {
+                       uint8_t* flags, int64_t* T_out, double* W_out, efg_stats* st, const DistPart* dp) {
   cudaStream_t s = ctx.stream;
   const int64_t n = g.n, m2 = g.m2 > 0 ? g.m2 : 1;
   const int B = 256;
@@ -1465,7 +1473,12 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   // ---- phase 1: class lists and counts on the device, one read-back
   int64_t* cdev = ctx.buf("f_counts").as<int64_t>(kNCounts);
   EFG_CUDA_CHECK(cudaMemsetAsync(cdev, 0, kNCounts * sizeof(int64_t), s));
-  Lists L = make_lists(ctx, P, stg, r, cdev, true);
+  Lists L = make_lists(ctx, P, stg, r, cdev, true, dp ? dp->nparts : 1, dp ? dp->part : 0);
+  if (dp) {
+    EFG_REQUIRE(P.dmax <= kListMaxDeg, "distributed pass: maximum degree above the listing bound");
+    EFG_CUDA_CHECK(cudaMemsetAsync(dp->words, 0, kDistWords * n * sizeof(unsigned long long), s));
+    EFG_CUDA_CHECK(cudaMemsetAsync(dp->ws, 0, n * sizeof(double), s));
+  }
   EFG_LAUNCH(k_hub_count, 2 * ctx.num_sms, 256, 0, s, L.hub, cdev + kHubs, g.offsets,
              reinterpret_cast<unsigned long long*>(cdev + kNTasks));
   int64_t c[kNCounts];
@@ -1477,12 +1490,12 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   double* ctab = ctx.buf("f_ctab").as<double>(m2);
   ChainAcc ca;
   {
-    unsigned long long* acc = ctx.buf("f_chain_acc").as<unsigned long long>(3 * n);
-    EFG_CUDA_CHECK(cudaMemsetAsync(acc, 0, 3 * n * sizeof(unsigned long long), s));
+    unsigned long long* acc = dp ? dp->words : ctx.buf("f_chain_acc").as<unsigned long long>(3 * n);
+    if (!dp) EFG_CUDA_CHECK(cudaMemsetAsync(acc, 0, 3 * n * sizeof(unsigned long long), s));
     ca.wh = acc;
     ca.wl = acc + n;
     ca.p2 = acc + 2 * n;
-    ca.ws = ctx.buf("f_chain_ws").as<double>(n);
+    ca.ws = dp ? dp->ws : ctx.buf("f_chain_ws").as<double>(n);
     const double d3 = 3.0 * (P.dmax > 1 ? P.dmax : 1);
     ca.c0 = (P.dmax > 1 ? P.dmax : 1) * d3 * log(d3);
   }
@@ -1509,7 +1522,7 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   prepare_tail(ctx, P, true);
   if (st) EFG_CUDA_CHECK(cudaEventRecord(ctx.ev[3], s));
   const PrepInfo info{P.dmax, P.sum_c2};
-  if (cnt <= 0) return info;
+  if (cnt <= 0 && !dp) return info;
   FArgs a;
   a.offsets = P.g.offsets;
   a.nbr = P.g.nbr;
@@ -1534,9 +1547,9 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   a.cp2 = ca.p2;
   a.cws = ca.ws;
   a.c0 = ca.c0;
-  a.tri = ctx.buf("f_tri").as<int64_t>(cnt);
-  a.Wth = ctx.buf("f_Wth").as<int64_t>(cnt);
-  a.Wtl = ctx.buf("f_Wtl").as<int64_t>(cnt);
+  a.tri = ctx.buf("f_tri").as<int64_t>(cnt > 0 ? cnt : 1);
+  a.Wth = ctx.buf("f_Wth").as<int64_t>(cnt > 0 ? cnt : 1);
+  a.Wtl = ctx.buf("f_Wtl").as<int64_t>(cnt > 0 ? cnt : 1);
   {
     int64_t* PT = ctx.buf("l_pt").as<int64_t>(P.ftab_len);
     EFG_LAUNCH(k_gfix, ceil_div(P.ftab_len, B), B, 0, s, P.gtab, P.ftab_len, PT);
@@ -1544,7 +1557,7 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   }
   // 2. triangles: listed once each for whole-graph passes, else per seed (the long kernels first)
   const int64_t nhubs = c[kHubs], ntasks = c[kNTasks];
-  const bool listing = r.lo == 0 && r.hi == n && P.dmax <= kListMaxDeg;
+  const bool listing = dp || (r.lo == 0 && r.hi == n && P.dmax <= kListMaxDeg);
   // hub tasks (hubs in descending work order, kHubRows rows each) serve both triangle paths
   HubTasks tk{};
   int64_t* tstart = nullptr;
@@ -1575,8 +1588,8 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   }
   if (listing) {
     MArgs ma;
-    unsigned long long* acc = ctx.buf("l_acc").as<unsigned long long>(4 * n);
-    EFG_CUDA_CHECK(cudaMemsetAsync(acc, 0, 4 * n * sizeof(unsigned long long), s));
+    unsigned long long* acc = dp ? dp->words + 3 * n : ctx.buf("l_acc").as<unsigned long long>(4 * n);
+    if (!dp) EFG_CUDA_CHECK(cudaMemsetAsync(acc, 0, 4 * n * sizeof(unsigned long long), s));
     ma.offsets = P.g.offsets;
     ma.nbr = P.g.nbr;
     ma.nd = P.nd;
@@ -1594,8 +1607,16 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     ma.n32 = c[kTr1] + c[kTr2] + c[kTr3] + c[kHubs];  // whole-graph pass: nodes of degree > 32
     ma.nhubs = nhubs;                                  // labels [0, nhubs): degree > kHashMaxDeg
     ma.ntasks = ntasks;
-    EFG_LAUNCH(k_mid_block, ntasks + (ma.n32 - nhubs), kMidThreads, 0, s, ma, tk);
-    EFG_LAUNCH(k_mid_warp, ceil_div(n - ma.n32, kMidWarps), kMidWarps * 32, 0, s, ma);
+    ma.nparts = dp ? dp->nparts : 1;
+    ma.part = dp ? dp->part : 0;
+    ma.nunits = (int32_t)(ntasks + (ma.n32 - nhubs));
+    if (dp) {
+      EFG_LAUNCH(k_mid_block<true>, ceil_div(ntasks + (ma.n32 - nhubs), ma.nparts), kMidThreads, 0, s, ma, tk);
+    } else {
+      EFG_LAUNCH(k_mid_block<false>, ntasks + (ma.n32 - nhubs), kMidThreads, 0, s, ma, tk);
+    }
+    EFG_LAUNCH(k_mid_warp, ceil_div(ceil_div(n - ma.n32, ma.nparts), kMidWarps), kMidWarps * 32, 0, s, ma);
+    if (dp) return info;  // the caller reduces the words over all parts, then ef_finish
     EFG_LAUNCH(k_list_out, ceil_div(cnt, B), B, 0, s, acc, a, cnt);
   } else if (nhubs) {
     // exact bitmaps over rank labels, per-task partials merged in task order
@@ -1632,6 +1653,35 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   // 5. epilogue
   EFG_LAUNCH(k_epilogue, ceil_div(cnt, B), B, 0, s, a, cnt, ef, total, flags, T_out, W_out);
   return info;
+}
+
+// Epilogue of a distributed pass for seeds r, from the words and stars terms
+// reduced over all parts (ef_factorized with a DistPart).
+void ef_finish(Context& ctx, const CSRView& g, SeedRange r, const unsigned long long* words, const double* ws,
+               double* ef, int64_t* total, uint8_t* flags, int64_t* T_out, double* W_out) {
+  cudaStream_t s = ctx.stream;
+  const int B = 256;
+  const int64_t n = g.n, cnt = r.hi - r.lo;
+  if (cnt <= 0) return;
+  Prepared P;
+  prepare_head(ctx, g, false, P);
+  prepare_rows(ctx, P, 0, n, 0, g.m2);
+  FArgs a{};
+  a.offsets = g.offsets;
+  a.s1 = P.s1;
+  a.s2 = P.s2;
+  a.cwh = words;
+  a.cwl = words + n;
+  a.cp2 = words + 2 * n;
+  a.cws = ws;
+  const double d3 = 3.0 * (P.dmax > 1 ? P.dmax : 1);
+  a.c0 = (P.dmax > 1 ? P.dmax : 1) * d3 * log(d3);
+  a.seed_lo = r.lo;
+  a.tri = ctx.buf("f_tri").as<int64_t>(cnt);
+  a.Wth = ctx.buf("f_Wth").as<int64_t>(cnt);
+  a.Wtl = ctx.buf("f_Wtl").as<int64_t>(cnt);
+  EFG_LAUNCH(k_list_out, ceil_div(cnt, B), B, 0, s, words + 3 * n, a, cnt);
+  EFG_LAUNCH(k_epilogue, ceil_div(cnt, B), B, 0, s, a, cnt, ef, total, flags, T_out, W_out);
 }
 
 }  // namespace efg

@@ -118,8 +118,21 @@ struct PrepInfo {
   int32_t dmax = 0;
   int64_t sum_c2 = 0;
 };
+// One part of a distributed whole-graph pass (efg_ef_partial): the part
+// builds the chain tables and pushes of the rows v % nparts == part and lists
+// the triangles of every nparts-th work unit; its integer words (planar chain
+// hi / lo / S1 sums, then per node triangle hi / lo / count / pad) and stars
+// terms are summed over all parts by the caller before ef_finish.
+constexpr int kDistWords = 7;  // u64 words per node
+struct DistPart {
+  int32_t part = 0, nparts = 1;
+  unsigned long long* words = nullptr;  // [kDistWords n]
+  double* ws = nullptr;                 // [n]
+};
 PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedRange r, double* ef, int64_t* total,
-                       uint8_t* flags, int64_t* T_out, double* W_out, efg_stats* st);
+                       uint8_t* flags, int64_t* T_out, double* W_out, efg_stats* st, const DistPart* dp = nullptr);
+void ef_finish(Context& ctx, const CSRView& g, SeedRange r, const unsigned long long* words, const double* ws,
+               double* ef, int64_t* total, uint8_t* flags, int64_t* T_out, double* W_out);
 
 // ef_direct.cu -- direct per-seed enumeration (original formulation)
 void ef_direct(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* total, uint8_t* flags,

@@ -71,6 +71,36 @@ def ef_range(dg: DeviceGraph, lo: int, hi: int, out_ef, out_total, out_flags, en
     return st.as_dict() if st is not None else None
 
 
+DIST_WORDS = 7  # EFG_DIST_WORDS: uint64 words per node of a distributed pass
+
+
+def ef_partial(dg: DeviceGraph, part: int, nparts: int, words, ws, stats: bool = False):
+    """One part of a distributed whole-graph pass (efg_ef_partial): integer
+    words int64[DIST_WORDS * n] and stars terms f64[n] of part `part` of
+    `nparts`; sum both over all parts, then ef_finish."""
+    import torch
+
+    ctx = _ctx_for(dg.offsets)
+    L = _native.lib()
+    _bind_stream(ctx, torch.cuda.current_stream(dg.offsets.device))
+    st = _native.Stats() if stats else None
+    _native.check(L.efg_ef_partial(ctx.handle, _dptr(dg.offsets), _dptr(dg.neighbors), dg.n, int(part), int(nparts),
+                                   _dptr(words), _dptr(ws), ctypes.byref(st) if st is not None else None))
+    return st.as_dict() if st is not None else None
+
+
+def ef_finish(dg: DeviceGraph, lo: int, hi: int, words, ws, out_ef, out_total, out_flags, T=None, W=None):
+    """Outputs of seeds [lo, hi) from the summed words of all parts (efg_ef_finish)."""
+    import torch
+
+    ctx = _ctx_for(dg.offsets)
+    L = _native.lib()
+    _bind_stream(ctx, torch.cuda.current_stream(dg.offsets.device))
+    _native.check(L.efg_ef_finish(ctx.handle, _dptr(dg.offsets), _dptr(dg.neighbors), dg.n, int(lo), int(hi),
+                                  _dptr(words), _dptr(ws), _dptr(out_ef), _dptr(out_total), _dptr(out_flags),
+                                  _dptr(T), _dptr(W)))
+
+
 def shard_bounds(dg: DeviceGraph, parts: int, engine="factorized") -> np.ndarray:
     """K2: contiguous seed shards of balanced engine work (identical on every rank)."""
     import torch

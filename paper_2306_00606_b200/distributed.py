@@ -1,13 +1,23 @@
-"""Multi-GPU Expected Force: replicated graph, seeds sharded, one all-gather.
+"""Multi-GPU Expected Force.
 
-One process per GPU (torch.distributed, NCCL over NVLink on B200 boxes).
-Every rank holds the full CSR in its HBM (370 MB at R-MAT22); K2 cuts the
-seed range into contiguous shards of equal engine work (`shard_bounds`, the
-same bounds on every rank because they depend only on the graph); each rank
-runs the EF kernels on its shard; the per-seed outputs (ef f64, cluster_total
-i64, flags u8 = 17 B/seed) are exchanged with ONE all-gather of a packed,
-padded byte buffer.  Seeds have a single owner and their sums run in a fixed
-order, so the result is bitwise identical for any world size.
+Two schemes, both one process per GPU (torch.distributed, NCCL over NVLink on
+B200 boxes) with the full CSR replicated in every rank's HBM:
+
+* ``ef_distributed`` (whole-graph passes, the default of bench.py): every
+  rank runs one part of the factorized pass -- the chain tables / pushes of
+  its nodes and the triangles listed by its share of work units
+  (efg_ef_partial) -- and ONE all-reduce sums the per-node integer words and
+  stars terms; every rank then finishes all seeds locally (efg_ef_finish).
+  Integer sums and disjoint supports make the result bitwise identical to the
+  single-GPU pass for any world size.
+* ``ef_sharded`` (seed shards; the direct engine and explicit seed ranges):
+  K2 cuts the seed range into contiguous shards of equal engine work
+  (`shard_bounds`, the same bounds on every rank because they depend only on
+  the graph); each rank runs the EF kernels on its shard; the per-seed
+  outputs (ef f64, cluster_total i64, flags u8 = 17 B/seed) are exchanged
+  with ONE all-gather of a packed, padded byte buffer.  Seeds have a single
+  owner and their sums run in a fixed order, so the result is bitwise
+  identical for any world size.
 
 There is no reference counterpart (the reference is single-process threads,
 expected_force.py:163-167); SURVEY.md §8(e) specifies this path.
@@ -17,6 +27,41 @@ from __future__ import annotations
 import numpy as np
 
 RECORD_BYTES = 17  # f64 ef + i64 cluster_total + u8 flags
+
+
+def ef_distributed(dg, group=None, partial=None, finish=None, T=None, W=None):
+    """EF of every seed of DeviceGraph `dg`, the whole-graph pass split over
+    the ranks of `group`; returns (ef, cluster_total, flags) on every rank.
+    `partial(dg, part, nparts, words, ws)` / `finish(dg, words, ws, ef, tot,
+    fl)` default to the GPU library (device.ef_partial / ef_finish); tests
+    substitute CPU stand-ins under gloo."""
+    import torch
+    import torch.distributed as dist
+
+    from . import device as D
+
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    dev = dg.offsets.device
+    n = dg.n
+    words = torch.empty(D.DIST_WORDS * n, dtype=torch.int64, device=dev)
+    ws = torch.empty(n, dtype=torch.float64, device=dev)
+    if partial is None:
+        D.ef_partial(dg, rank, world, words, ws)
+    else:
+        partial(dg, rank, world, words, ws)
+    if world > 1:
+        # integer words: exact in any order; stars terms: one nonzero per node
+        dist.all_reduce(words, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(ws, op=dist.ReduceOp.SUM, group=group)
+    ef = torch.empty(n, dtype=torch.float64, device=dev)
+    tot = torch.empty(n, dtype=torch.int64, device=dev)
+    fl = torch.empty(n, dtype=torch.uint8, device=dev)
+    if finish is None:
+        D.ef_finish(dg, 0, n, words, ws, ef, tot, fl, T=T, W=W)
+    else:
+        finish(dg, words, ws, ef, tot, fl)
+    return ef, tot, fl
 
 
 def row_bytes(pad_to: int) -> int:

@@ -48,4 +48,7 @@ if out_json:
         out[k] = t["dram_bytes"] / t["launches"]
         if k in alias:
             out[alias[k]] = out[k]
+        base = k.split("<")[0]
+        if base != k and base not in out:
+            out[base] = out[k]
     json.dump(out, open(out_json, "w"), indent=1)

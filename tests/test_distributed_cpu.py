@@ -85,3 +85,63 @@ def test_pack_unpack_roundtrip():
     assert ef.tolist() == [0, 1, 2, 20, 21, 22, 23]
     assert tot.tolist() == [0, 7, 14, 2, 9, 16, 23]
     assert fl.tolist() == [0, 0, 0, 2, 2, 2, 2]
+
+
+# --- ef_distributed: parts of the whole-graph pass + one all-reduce --------
+def _split_partial(T, W):
+    """Stand-in for efg_ef_partial: part p holds an arbitrary (seeded) integer
+    split of every node's T in word 0 (negative pieces exercise wrap-free
+    int64 sums) and W of the nodes v % nparts == p (disjoint supports)."""
+    def partial(dg, part, nparts, words, ws):
+        n = dg.n
+        rng = np.random.default_rng(1234)  # same draws on every rank
+        pieces = rng.integers(-2**40, 2**40, size=(nparts, n))
+        pieces[-1] = T - pieces[:-1].sum(axis=0)
+        w = np.zeros(words.numel(), np.int64)
+        w[:n] = pieces[part]
+        words.copy_(torch.from_numpy(w))
+        s = np.where(np.arange(n) % nparts == part, W, 0.0)
+        ws.copy_(torch.from_numpy(s))
+    return partial
+
+
+def _finish(dg, words, ws, ef, tot, fl):
+    n = dg.n
+    T = words[:n].numpy()
+    W = ws.numpy()
+    e = np.where(T > 0, np.log(np.maximum(T, 1)) - W / np.maximum(T, 1), 0.0)
+    ef.copy_(torch.from_numpy(e))
+    tot.copy_(torch.from_numpy(T))
+    fl.zero_()
+
+
+def _dist_worker(rank, world, port, offsets, neighbors, T, W, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dg = HostGraph(offsets, neighbors)
+        ef, tot, fl = Dist.ef_distributed(dg, partial=_split_partial(T, W), finish=_finish)
+        np.savez(f"{out_path}.{rank}.npz", ef=ef.numpy(), tot=tot.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_distributed_allreduce_is_exact(golden, tmp_path, world):
+    case = golden["rmat_12_8_3"]
+    off, nb = case.get("offsets"), case.get("neighbors")
+    _, _, _, T, W = O.ef_seeds(off, nb, threads=2)
+    ctx = mp.get_context("spawn")
+    port = _free_port()
+    procs = [ctx.Process(target=_dist_worker, args=(r, world, port, off, nb, T, W, str(tmp_path / "d")))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=240)
+        assert p.exitcode == 0
+    want = np.where(T > 0, np.log(np.maximum(T, 1)) - W / np.maximum(T, 1), 0.0)
+    for r in range(world):
+        z = np.load(tmp_path / f"d.{r}.npz")
+        assert np.array_equal(z["tot"], T)
+        assert np.array_equal(z["ef"], want)

@@ -138,3 +138,29 @@ def test_dense_core_shards_bitwise(dense_core):
     torch.cuda.synchronize()
     for x, y in zip(full, outs):
         assert torch.equal(x, y)
+
+
+@pytest.mark.parametrize("nparts", [1, 3, 8])
+def test_distributed_parts_bitwise(rmat18, nparts):
+    # parts of a whole-graph pass summed as the all-reduce would, then finished:
+    # bitwise equal to the single-GPU pass
+    import torch
+    from paper_2306_00606_b200 import device as D
+
+    dg = D.DeviceGraph.from_host(rmat18)
+    n = rmat18.n
+    full = [torch.empty(n, dtype=t, device="cuda") for t in (torch.float64, torch.int64, torch.uint8)]
+    D.ef_range(dg, 0, n, *full)
+    words = torch.zeros(D.DIST_WORDS * n, dtype=torch.int64, device="cuda")
+    ws = torch.zeros(n, dtype=torch.float64, device="cuda")
+    w = torch.empty_like(words)
+    s = torch.empty_like(ws)
+    for p in range(nparts):
+        D.ef_partial(dg, p, nparts, w, s)
+        words += w
+        ws += s
+    out = [torch.empty(n, dtype=t, device="cuda") for t in (torch.float64, torch.int64, torch.uint8)]
+    D.ef_finish(dg, 0, n, words, ws, *out)
+    torch.cuda.synchronize()
+    for x, y in zip(full, out):
+        assert torch.equal(x, y)

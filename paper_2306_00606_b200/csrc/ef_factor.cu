@@ -418,14 +418,18 @@ __global__ void k_push_warp(const int32_t* __restrict__ rows, int64_t count, con
   if (lane < d) chain_push(ca, v, y, val, s1[i]);
 }
 
-// d > 32: CTA per row; H_i's keys in shared memory (global beyond 4096).
-constexpr int kPushThreads = 128, kPushKeys = 4096;
+// d > 32: CTA per row.  Keys below kPushDirect (most neighbour degrees) are
+// located through a direct-mapped shared table (key -> position; only keys
+// present are ever read, so it needs no clearing), larger ones by binary
+// search over H_i's keys (shared memory, global beyond kPushKeys).
+constexpr int kPushThreads = 128, kPushKeys = 4096, kPushDirect = 4096;
 __global__ void __launch_bounds__(kPushThreads)
 k_push_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
              const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd, const int32_t* __restrict__ dcnt,
              const int32_t* __restrict__ hkey, const int32_t* __restrict__ hcnt, const double* __restrict__ ctab,
              const int64_t* __restrict__ s1, ChainAcc ca) {
   __shared__ int32_t sk[kPushKeys];
+  __shared__ int16_t pos[kPushDirect];
   __shared__ double red[kPushThreads / 32];
   const int64_t q = blockIdx.x;
   if (q >= count) return;
@@ -438,18 +442,25 @@ k_push_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
   for (int k = threadIdx.x; k < D; k += kPushThreads) {
     const int32_t kk = hkey[b + k];
     if (D <= kPushKeys) sk[k] = kk;
+    if (kk < kPushDirect && k < 32768) pos[kk] = (int16_t)k;
     hc += (double)hcnt[b + k] * ctab[b + k];
   }
-  hc = block_sum<kPushThreads>(hc, red);  // syncs: sk is complete afterwards
+  hc = block_sum<kPushThreads>(hc, red);  // syncs: the tables are complete afterwards
   if (threadIdx.x == 0) ca.ws[i] = hc;
   __syncthreads();
   const int64_t s1i = s1[i];
   for (int p = threadIdx.x; p < d; p += kPushThreads) {
     const int32_t y = nd[b + p];
-    int lo = 0, hi = D - 1;  // y is present: v is a neighbour of i
-    while (lo < hi) {
-      const int mid = (lo + hi) >> 1;
-      if (keys[mid] < y) lo = mid + 1; else hi = mid;
+    int lo;
+    if (y < kPushDirect && D <= 32768) {
+      lo = pos[y];
+    } else {
+      lo = 0;
+      int hi = D - 1;  // y is present: v is a neighbour of i
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (keys[mid] < y) lo = mid + 1; else hi = mid;
+      }
     }
     chain_push(ca, nbr[b + p], y, __ldg(ctab + b + lo), s1i);
   }

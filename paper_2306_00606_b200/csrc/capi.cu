@@ -327,7 +327,9 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
     EFG_CUDA_CHECK(cudaMemcpyAsync(d_off, offsets, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c.copy_stream));
     EFG_CUDA_CHECK(cudaEventRecord(c.chunk_ev[0], c.copy_stream));
     efg::Staging stg;
-    stg.nchunks = m2 >= (int64_t(1) << 22) ? 4 : 1;  // measured best at R-MAT22 (2: 54.9, 4: 54.6, 8: 57.1 ms e2e)
+    // chunk count measured at R-MAT22 (1: 51.8, 2: 50.6, 4: 52.7, 8: 58.7 ms e2e): splitting
+    // kernels costs launch tails, so two chunks balance overlap against them
+    stg.nchunks = m2 >= (int64_t(1) << 22) ? 2 : 1;
     for (int k = 0; k <= stg.nchunks; ++k) {
       const int64_t target = m2 * k / stg.nchunks;
       stg.row[k] = k == stg.nchunks ? n : std::lower_bound(offsets, offsets + n + 1, target) - offsets;

@@ -57,7 +57,7 @@ struct FArgs {
   const int32_t* dcnt;     // |D_i|: H_i = hkey/hcnt[offsets[i], offsets[i] + dcnt[i])
   const int32_t* hkey;
   const int32_t* hcnt;
-  const int4* rowhash;     // bucketed hash of Adj+(i) for |Adj+(i)| >= kRevMin, at bucket 2*offp[i]
+  const int4* rowhash;     // bucketed hash of Adj+(i) for |Adj+(i)| >= kRevMin, at bucket 2*offsets[i]
   // per node: pushed chain sums (see chain_push) and the stars term
   const int64_t* s2;
   const unsigned long long* cwh;
@@ -612,7 +612,7 @@ __device__ __forceinline__ void tri_rows(const FArgs& a, int64_t ob, int nrows, 
 // Reverse probing.  A row Adj+(i) much longer than Adj(v) is cheaper to test
 // the other way round: each j in Adj(v) is looked up in a global bucketed
 // hash of Adj+(i) (built once per pass for |Adj+(i)| >= kRevMin, 4 keys per
-// 16-byte bucket, load <= 1/4, located at bucket 2*offp[i]).  A hit is
+// 16-byte bucket, load <= 1/4, located at bucket 2*offsets[i]).  A hit is
 // exactly j in Adj+(i), i.e. the same triangle the forward scan would find.
 constexpr int kRevMin = 64;
 constexpr int kRevKappa = 2;
@@ -632,13 +632,13 @@ __device__ __forceinline__ bool rowhash_has(const int4* __restrict__ base, uint3
 }
 
 // Warp per node with |Adj+(i)| >= kRevMin: clear its buckets, insert its labels.
-__global__ void k_rowhash(const int64_t* __restrict__ offp, const int32_t* __restrict__ adjj, int64_t n,
-                          int4* __restrict__ rowhash) {
+__global__ void k_rowhash(const int64_t* __restrict__ offsets, const int32_t* __restrict__ dplus,
+                          const int32_t* __restrict__ adjj, int64_t n, int4* __restrict__ rowhash) {
   const int lane = threadIdx.x & 31;
   const int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (i >= n) return;
-  const int64_t p0 = offp[i];
-  const int32_t pc = (int32_t)(offp[i + 1] - p0);
+  const int64_t p0 = offsets[i];
+  const int32_t pc = dplus[i];
   if (pc < kRevMin) return;
   const uint32_t lg = rowhash_lg(pc), nb = 1u << lg;
   int4* base = rowhash + 2 * p0;
@@ -930,7 +930,7 @@ struct MArgs {
   const int32_t* nd;
   const int64_t* ps;  // per slot e = (v -> u): start of Adj+(u)
   const int32_t* pc;  // per slot: |Adj+(u)|
-  const int64_t* offp;
+  const int32_t* dplus;     // |Adj+(v)|: Adj+(v) at adjj[offsets[v], offsets[v] + dplus[v])
   const int32_t* adjj;
   const int32_t* adjd;
   const int32_t* rank_of;
@@ -1185,8 +1185,8 @@ k_mid_block(MArgs a, HubTasks tk) {
   }
   const int64_t ob = __ldg(a.offsets + v);
   const int32_t dv = (int32_t)(__ldg(a.offsets + v + 1) - ob);
-  const int64_t pb = __ldg(a.offp + v);
-  const int32_t pv = (int32_t)(__ldg(a.offp + v + 1) - pb);
+  const int64_t pb = __ldg(a.offsets + v);
+  const int32_t pv = __ldg(a.dplus + v);
   const int32_t labv = __ldg(a.rank_of + v);
   if (pv == 0) return;  // no triangle has v in the middle
   Acc2 av;
@@ -1606,7 +1606,7 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     ma.nd = P.nd;
     ma.ps = P.ps;
     ma.pc = P.pc;
-    ma.offp = P.offp;
+    ma.dplus = P.dplus;
     ma.adjj = P.adjj;
     ma.adjd = P.adjd;
     ma.rank_of = P.rank_of;
@@ -1645,8 +1645,8 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     EFG_LAUNCH(k_hub_merge, ceil_div(nhubs, B), B, 0, s, hs, nhubs, tstart, tk.ptri, tk.pWh, tk.pWl, a);
   }
   if (!listing) {
-    int4* rowhash = ctx.buf("f_rowhash").as<int4>(m2);  // 2 * m buckets: bucket 2*offp[i] starts Adj+(i)
-    EFG_LAUNCH(k_rowhash, ceil_div(n * 32, B), B, 0, s, P.offp, P.adjj, n, rowhash);
+    int4* rowhash = ctx.buf("f_rowhash").as<int4>(2 * m2);  // bucket 2*offsets[i] starts Adj+(i)'s hash
+    EFG_LAUNCH(k_rowhash, ceil_div(n * 32, B), B, 0, s, P.g.offsets, P.dplus, P.adjj, n, rowhash);
     a.rowhash = rowhash;
     // buckets of 4 keys: dv <= 256 at load <= 1/8 with degrees, dv <= 1024 / 4096 at load <= 1/4
     auto k_tri_seed_256 = k_tri_seed<128, 512, true>;

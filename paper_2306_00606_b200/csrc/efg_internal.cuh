@@ -75,13 +75,13 @@ struct Prepared {
   double* gtab = nullptr;       // [3*dmax+8]  G[S] = F(S-6) - F(S-4)
   int64_t ftab_len = 0;
   // degree-ordered orientation: j in Adj+(i) iff (d_j, j) > (d_i, i)
-  int64_t* offp = nullptr;      // [n+1]
-  int32_t* adjj = nullptr;      // [m]  Adj+ rows as rank labels
-  int32_t* adjd = nullptr;      // [m]  degree of each Adj+ entry
+  int32_t* dplus = nullptr;     // [n]   |Adj+(v)|
+  int32_t* adjj = nullptr;      // [2m] Adj+ rows as rank labels, slot space: row v at [offsets[v], +dplus[v])
+  int32_t* adjd = nullptr;      // [2m] degree of each Adj+ entry
   int32_t* rank_of = nullptr;   // [n]  position in descending (degree, id) order
   int32_t* deg_by_rank = nullptr;  // [n]
   int32_t* by_rank = nullptr;   // [n]  node of each rank label
-  int64_t* ps = nullptr;        // [2m] per slot (v->i): offp[i]
+  int64_t* ps = nullptr;        // [2m] per slot (v->i): offsets[i] (start of Adj+(i))
   int32_t* pc = nullptr;        // [2m] per slot (v->i): |Adj+(i)|
 };
 

@@ -44,74 +44,60 @@ __device__ __forceinline__ bool ranks_above(int32_t dj, int32_t j, int32_t di, i
   return dj > di || (dj == di && j > i);
 }
 
-// Warp per row: s1[v] = sum of neighbour degrees; dplus[v] = |Adj+(v)|.
+// Warp per row: s1[v] = sum of neighbour degrees, s2[v] = sum of their
+// squares, and (with the orientation) Adj+(v) = the neighbours ranking above
+// v, compacted in order as rank labels + degrees into v's own slot range
+// [offsets[v], offsets[v] + dplus[v]) -- slot space, so no scan is needed and
+// the pass runs per row chunk while the rest of the graph is still copied.
 __global__ void k_row_sums(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
                            const int32_t* __restrict__ nd, int64_t r0, int64_t r1, int64_t* __restrict__ s1,
-                           int64_t* __restrict__ s2, int64_t* __restrict__ dplus) {
+                           int64_t* __restrict__ s2, int32_t* __restrict__ dplus, const int32_t* __restrict__ rank_of,
+                           int32_t* __restrict__ adjj, int32_t* __restrict__ adjd) {
   const int lane = threadIdx.x & 31;
   int64_t v = r0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (v >= r1) return;
   int64_t b = offsets[v], e = offsets[v + 1];
   int32_t dv = (int32_t)(e - b);
   int64_t s = 0, q = 0;
-  int cnt = 0;
-  for (int64_t p = b + lane; p < e; p += 32) {
-    int32_t dj = nd[p];
-    s += dj;
-    q += (int64_t)dj * dj;
-    cnt += ranks_above(dj, nbr[p], dv, (int32_t)v);
-  }
-  for (int o = 16; o; o >>= 1) {
-    s += __shfl_xor_sync(0xffffffffu, s, o);
-    q += __shfl_xor_sync(0xffffffffu, q, o);
-    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-  }
-  if (lane == 0) {
-    s1[v] = s;
-    s2[v] = q;
-    dplus[v] = cnt;
-  }
-}
-
-// Warp per row: ordered compaction of Adj+(v), stored as rank labels.
-__global__ void k_fill_adjp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
-                            const int32_t* __restrict__ nd, int64_t n, const int64_t* __restrict__ offp,
-                            const int32_t* __restrict__ rank_of, int32_t* __restrict__ adjj,
-                            int32_t* __restrict__ adjd) {
-  const int lane = threadIdx.x & 31;
-  int64_t v = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  if (v >= n) return;
-  int64_t b = offsets[v], e = offsets[v + 1];
-  int32_t dv = (int32_t)(e - b);
-  int64_t out = offp[v];
+  int64_t out = b;
   for (int64_t p0 = b; p0 < e; p0 += 32) {
-    int64_t p = p0 + lane;
+    const int64_t p = p0 + lane;
     int32_t j = 0, dj = 0;
     bool take = false;
     if (p < e) {
       j = nbr[p];
       dj = nd[p];
+      s += dj;
+      q += (int64_t)dj * dj;
       take = ranks_above(dj, j, dv, (int32_t)v);
     }
-    unsigned mask = __ballot_sync(0xffffffffu, take);
-    if (take) {
+    const unsigned mask = __ballot_sync(0xffffffffu, take);
+    if (take && adjj) {
       const int64_t o = out + __popc(mask & ((1u << lane) - 1));
       adjj[o] = __ldg(rank_of + j);
       adjd[o] = dj;
     }
     out += __popc(mask);
   }
+  for (int o = 16; o; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    q += __shfl_xor_sync(0xffffffffu, q, o);
+  }
+  if (lane == 0) {
+    s1[v] = s;
+    s2[v] = q;
+    dplus[v] = (int32_t)(out - b);
+  }
 }
 
 // Per adjacency slot e = (v -> i): where Adj+(i) starts and how long it is.
-__global__ void k_slot_plus(const int32_t* __restrict__ nbr, int64_t m2, const int64_t* __restrict__ offp,
-                            int64_t* __restrict__ ps, int32_t* __restrict__ pc) {
+__global__ void k_slot_plus(const int32_t* __restrict__ nbr, int64_t m2, const int64_t* __restrict__ offsets,
+                            const int32_t* __restrict__ dplus, int64_t* __restrict__ ps, int32_t* __restrict__ pc) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= m2) return;
   const int32_t i = nbr[e];
-  const int64_t a = offp[i];
-  ps[e] = a;
-  pc[e] = (int32_t)(offp[i + 1] - a);
+  ps[e] = offsets[i];
+  pc[e] = dplus[i];
 }
 
 // Rank label of each node: its position in descending (degree, id) order, so
@@ -195,21 +181,22 @@ __device__ __forceinline__ void sort_row(int32_t* __restrict__ row, int32_t* __r
 // [PMIN, PMAX]; rows above 1024 entries (rare) rank by counting through a
 // scratch row.  Two instantiations keep the small-row kernel's registers low.
 template <int PMIN, int PMAX>
-__global__ void k_sort_rows(const int64_t* __restrict__ offp, int64_t n, const int32_t* __restrict__ deg_by_rank,
+__global__ void k_sort_rows(const int64_t* __restrict__ offsets, const int32_t* __restrict__ dplus, int64_t n,
+                            const int32_t* __restrict__ deg_by_rank,
                             int32_t* __restrict__ adjj, int32_t* __restrict__ adjd, int32_t* __restrict__ scratch) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g * 32 < n; g += nw) {
     const int64_t mine = g * 32 + lane;
     int p = 0;
-    if (mine < n) p = (int)(offp[mine + 1] - offp[mine]);
+    if (mine < n) p = dplus[mine];
     unsigned todo = __ballot_sync(0xffffffffu, p >= PMIN && p <= PMAX && p >= 2);
     while (todo) {
       const int x = __ffs(todo) - 1;
       todo &= todo - 1;
       const int64_t v = g * 32 + x;
       const int pv = __shfl_sync(0xffffffffu, p, x);
-      const int64_t b = offp[v];
+      const int64_t b = offsets[v];
       int32_t* row = adjj + b;
       int32_t* rowd = adjd + b;
       if (PMAX <= 256) {
@@ -293,17 +280,20 @@ void prepare_head(Context& ctx, const CSRView& g, bool need_orientation, Prepare
   P.deg_by_rank = ctx.buf("deg_by_rank").as<int32_t>(n);
   EFG_LAUNCH(k_rank_scatter, ceil_div(n, B), B, 0, s, val + n, n, P.deg, P.rank_of, P.deg_by_rank);
   P.by_rank = val + n;
+  // Adj+ in slot space: row v at [offsets[v], offsets[v] + dplus[v])
+  P.adjj = ctx.buf("adjj").as<int32_t>(m2 > 0 ? m2 : 1);
+  P.adjd = ctx.buf("adjd").as<int32_t>(m2 > 0 ? m2 : 1);
 }
 
 // Rows [r0, r1) (slots [e0, e1)) whose neighbours are resident: neighbour
-// degrees, S1 and |Adj+|.
+// degrees, S1, S2 and (with the orientation) Adj+ in slot space.
 void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t e0, int64_t e1) {
   cudaStream_t s = ctx.stream;
   const int B = 256;
-  int64_t* dplus64 = ctx.buf("dplus64").as<int64_t>(P.g.n + 1);
+  P.dplus = ctx.buf("dplus").as<int32_t>(P.g.n > 0 ? P.g.n : 1);
   EFG_LAUNCH(k_nd, ceil_div(e1 - e0, B), B, 0, s, P.g.nbr, e0, e1, P.deg, P.nd);
   EFG_LAUNCH(k_row_sums, ceil_div((r1 - r0) * 32, B), B, 0, s, P.g.offsets, P.g.nbr, P.nd, r0, r1, P.s1, P.s2,
-             dplus64);
+             P.dplus, P.rank_of, P.rank_of ? P.adjj : nullptr, P.adjd);
 }
 
 // Everything that needs all neighbours: the label-sorted orientation.
@@ -313,30 +303,20 @@ void prepare_tail(Context& ctx, Prepared& P, bool need_orientation) {
   const int B = 256;
   const CSRView& g = P.g;
   const int64_t n = g.n, m2 = g.m2;
-  int64_t* dplus64 = ctx.buf("dplus64").as<int64_t>(n + 1);
-  size_t tmp = 0;
-  P.offp = ctx.buf("offp").as<int64_t>(n + 1);
-  EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(nullptr, tmp, dplus64, P.offp, n + 1, s));
-  EFG_CUDA_CHECK(cudaMemsetAsync(dplus64 + n, 0, sizeof(int64_t), s));
-  EFG_REGION("cub::DeviceScan::ExclusiveSum", s, EFG_CUDA_CHECK(cub::DeviceScan::ExclusiveSum(ctx.buf("cub").get(tmp), tmp, dplus64, P.offp, n + 1, s)));
-  P.adjj = ctx.buf("adjj").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);
-  P.adjd = ctx.buf("adjd").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);
-  EFG_LAUNCH(k_fill_adjp, ceil_div(n * 32, B), B, 0, s, g.offsets, g.nbr, P.nd, n, P.offp, P.rank_of, P.adjj,
-             P.adjd);
   {
     // rows sorted by label: a row scan for a higher-ranked v can stop at v (triangle listing)
-    int32_t* scratch = ctx.buf("adjj_scratch").as<int32_t>(m2 / 2 > 0 ? m2 / 2 : 1);
+    int32_t* scratch = ctx.buf("adjj_scratch").as<int32_t>(m2 > 0 ? m2 : 1);
     auto k_sort_small = k_sort_rows<2, 256>;
     auto k_sort_large = k_sort_rows<257, INT32_MAX>;
     const int64_t groups = ceil_div(n, 32);
-    EFG_LAUNCH(k_sort_small, std::min<int64_t>(ceil_div(groups * 32, B), 16 * ctx.num_sms), B, 0, s, P.offp, n,
-               P.deg_by_rank, P.adjj, P.adjd, scratch);
-    EFG_LAUNCH(k_sort_large, std::min<int64_t>(ceil_div(groups * 32, B), 4 * ctx.num_sms), B, 0, s, P.offp, n,
-               P.deg_by_rank, P.adjj, P.adjd, scratch);
+    EFG_LAUNCH(k_sort_small, std::min<int64_t>(ceil_div(groups * 32, B), 16 * ctx.num_sms), B, 0, s, g.offsets,
+               P.dplus, n, P.deg_by_rank, P.adjj, P.adjd, scratch);
+    EFG_LAUNCH(k_sort_large, std::min<int64_t>(ceil_div(groups * 32, B), 4 * ctx.num_sms), B, 0, s, g.offsets,
+               P.dplus, n, P.deg_by_rank, P.adjj, P.adjd, scratch);
   }
   P.ps = ctx.buf("ps").as<int64_t>(m2);
   P.pc = ctx.buf("pc").as<int32_t>(m2);
-  EFG_LAUNCH(k_slot_plus, ceil_div(m2, B), B, 0, s, g.nbr, m2, P.offp, P.ps, P.pc);
+  EFG_LAUNCH(k_slot_plus, ceil_div(m2, B), B, 0, s, g.nbr, m2, g.offsets, P.dplus, P.ps, P.pc);
 }
 
 void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P) {

@@ -917,8 +917,9 @@ __global__ void k_hub_bitmaps(const int32_t* __restrict__ hubs, int64_t nhubs, c
 // (a row has < 2^16 hits, a node < 2^31 partial sums).
 constexpr int kMidWarps = 8;
 constexpr int kMidThreads = 256;
-constexpr int kMidNB = 1024;        // shared map of Adj+(v): |Adj+(v)| <= 1024 at load <= 1/4
-constexpr int kMidMaxP = kMidNB;    // longer Adj+(v) are processed in parts of this size
+constexpr int kMidNB = 512;         // shared map of Adj+(v): <= 1024 keys at load <= 1/2
+constexpr int kMidLgNB = 9;
+constexpr int kMidMaxP = 1024;      // longer Adj+(v) are processed in parts of this size
 constexpr int kMidChunk = 256;
 constexpr int kMidUnroll = 4;      // rows between entry flushes: 32-bit entry words cannot overflow
 constexpr int kListScale = 40;      // P = rint(G * 2^40)
@@ -1005,9 +1006,9 @@ __device__ __forceinline__ void smap_insert(int4* keys, V* vals, uint32_t lg, in
 // Scan of one row Adj+(u)[lane::32] in phases of kUnroll entries (labels +
 // degrees, then membership, then the G gathers), calling hit(y, label, P)
 // for every w found in Adj+(v) (y = its position there).
-template <int U, class Find, class Hit>
+template <int U, class Find, class Deg, class Hit>
 __device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu, int32_t lim, int32_t s0, int lane,
-                                         Find find, Hit hit) {
+                                         Find find, Deg degree, Hit hit) {
   // Adj+(u) is sorted by label and only labels < lim = rank(v) can lie in
   // Adj+(v): the scan stops at the first entry >= lim (i.e. at v itself)
   const int32_t* __restrict__ row = a.adjj + psu;
@@ -1026,9 +1027,9 @@ __device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu
       past |= j[k] >= lim;
       y[k] = j[k] < lim ? find(j[k]) : -1;
     }
-    // only hits need w's degree: gathered by label (4 B streamed per probe instead of 8)
+    // only hits need w's degree: looked up by its position in Adj+(v) (4 B streamed per probe instead of 8)
 #pragma unroll
-    for (int k = 0; k < U; ++k) d[k] = y[k] >= 0 ? __ldg(a.deg_by_rank + j[k]) : 0;
+    for (int k = 0; k < U; ++k) d[k] = y[k] >= 0 ? degree(y[k], j[k]) : 0;
 #pragma unroll
     for (int k = 0; k < U; ++k) g[k] = y[k] >= 0 ? __ldg(pt + d[k]) : 0;
 #pragma unroll
@@ -1123,6 +1124,7 @@ k_mid_warp(MArgs a) {
     uint32_t rc = 0;
     mid_scan<kMidUnroll>(
         a, psx, pux, (int32_t)r, s0, lane, [&](int32_t key) { return smap_find(sK[w], sV[w], 5, key); },
+        [&](int32_t, int32_t key) { return __ldg(a.deg_by_rank + key); },
         [&](int32_t y, int32_t, int64_t g) {
           rs += g;
           ++rc;
@@ -1153,7 +1155,7 @@ struct MidSmem {
   int4 lk[kMidNB];
   int64_t rps[kMidChunk];  // compacted rows of the current chunk: Adj+(u) start,
   int32_t ru[kMidChunk], rdu[kMidChunk], rpu[kMidChunk];  // u, du, |Adj+(u)|
-  int32_t node[kMidMaxP];
+  int32_t node[kMidMaxP], edeg[kMidMaxP];
   uint32_t elo[kMidMaxP], ehi[kMidMaxP], ec[kMidMaxP];
   int16_t lv[4 * kMidNB];
   int32_t nrows;
@@ -1195,7 +1197,7 @@ k_mid_block(MArgs a, HubTasks tk) {
   for (int32_t q0 = 0; q0 < pv; q0 += kMidMaxP) {
     const int32_t np = min(pv - q0, kMidMaxP);
     const int32_t lim = q0 + np < pv ? __ldg(a.adjj + pb + q0 + np) : labv;
-    const uint32_t lgl = 32u - __clz(max(np, 2) - 1);  // NB = 2^lgl >= np buckets
+    const uint32_t lgl = min(32u - __clz(max(np, 2) - 1), (uint32_t)kMidLgNB);  // NB = min(2^lgl >= np, kMidNB)
     __syncthreads();
     for (int b = threadIdx.x; b < (1 << lgl); b += blockDim.x) sm.lk[b] = make_int4(-1, -1, -1, -1);
     __syncthreads();
@@ -1203,6 +1205,7 @@ k_mid_block(MArgs a, HubTasks tk) {
       const int32_t l = __ldg(a.adjj + pb + q0 + t);
       smap_insert(sm.lk, sm.lv, lgl, l, t);
       sm.node[t] = __ldg(a.by_rank + l);
+      sm.edeg[t] = __ldg(a.deg_by_rank + l);
       sm.elo[t] = 0;
       sm.ehi[t] = 0;
       sm.ec[t] = 0;
@@ -1239,6 +1242,7 @@ k_mid_block(MArgs a, HubTasks tk) {
         uint32_t rc = 0;
         mid_scan<kMidUnroll>(
             a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); },
+            [&](int32_t y, int32_t) { return sm.edeg[y]; },
             [&](int32_t y, int32_t, int64_t g) {
               rs += g;
               ++rc;

@@ -1088,6 +1088,7 @@ k_mid_warp(MArgs a) {
   __shared__ int8_t sV[kMidWarps][128];
   __shared__ int64_t sP[kMidWarps][32];
   __shared__ uint32_t sC[kMidWarps][32];
+  __shared__ int32_t sE[kMidWarps][32];  // degree of each slot's neighbour (entries of Adj+(v) among them)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t r = a.n32 + ((int64_t)blockIdx.x * kMidWarps + w) * a.nparts + a.part;
   if (r >= a.n) return;
@@ -1107,6 +1108,7 @@ k_mid_warp(MArgs a) {
   sK[w][lane] = make_int4(-1, -1, -1, -1);
   sP[w][lane] = 0;
   sC[w][lane] = 0;
+  sE[w][lane] = du;
   __syncwarp();
   if (up) smap_insert(sK[w], sV[w], 5, __ldg(a.rank_of + u), lane);
   __syncwarp();
@@ -1124,7 +1126,7 @@ k_mid_warp(MArgs a) {
     uint32_t rc = 0;
     mid_scan<kMidUnroll>(
         a, psx, pux, (int32_t)r, s0, lane, [&](int32_t key) { return smap_find(sK[w], sV[w], 5, key); },
-        [&](int32_t, int32_t key) { return __ldg(a.deg_by_rank + key); },
+        [&](int32_t y, int32_t) { return sE[w][y]; },
         [&](int32_t y, int32_t, int64_t g) {
           rs += g;
           ++rc;

@@ -383,39 +383,72 @@ __device__ __forceinline__ void chain_push(const ChainAcc& ca, int32_t v, int32_
   atomicAdd(ca.p2 + v, (unsigned long long)s1i);
 }
 
-// d <= 32: warp per row i; lane k holds H_i's k-th key and C_i value, lane
-// e its slot's neighbour.  Also writes the stars term of i.
-__global__ void k_push_warp(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
-                            const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd,
-                            const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey,
-                            const int32_t* __restrict__ hcnt, const double* __restrict__ ctab,
-                            const int64_t* __restrict__ s1, ChainAcc ca) {
+// d <= 32, fused: one warp per row i does the histogram, the chain table and
+// the pushes in registers (nothing of H_i or C_i reaches memory).  Lane e
+// holds slot e; the sorted degrees' run heads give H_i in lanes 0..D-1; lane
+// k computes C_i(key_k) over the D keys (shuffled in), and each slot takes the
+// value of its degree's run.  Same table values as k_hist_warp + k_ctab_group
+// (same summation order).
+constexpr int kSmallWarps = 8;
+__global__ void __launch_bounds__(kSmallWarps * 32)
+k_small_rows(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
+                             const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd,
+                             const int32_t* __restrict__ deg, const double* __restrict__ F,
+                             const int64_t* __restrict__ s1, ChainAcc ca) {
   const int lane = threadIdx.x & 31;
   const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (q >= count) return;
   const int32_t i = rows[q];
   const int64_t b = offsets[i];
   const int d = (int)(offsets[i + 1] - b);
-  const int D = dcnt[i];
-  int32_t key = -1;
-  double c = 0.0, hc = 0.0;
+  const int32_t y = lane < d ? nd[b + lane] : 0x7fffffff;  // this slot's neighbour degree
+  (void)deg;
+  int32_t x = y;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int32_t o = __shfl_xor_sync(0xffffffffu, x, j);
+      const bool up = (lane & k) == 0;
+      const bool lower = (lane & j) == 0;
+      x = (lower == up) ? min(x, o) : max(x, o);
+    }
+  }
+  const int32_t prev = __shfl_up_sync(0xffffffffu, x, 1);
+  const bool head = lane < d && (lane == 0 || x != prev);
+  const unsigned heads = __ballot_sync(0xffffffffu, head);
+  const int D = __popc(heads);
+  // run k (k < D): key and count, gathered into lane k
+  __shared__ int2 runs[kSmallWarps][32];
+  const int w = threadIdx.x >> 5;
+  if (head) {
+    const unsigned after = heads & ~((2u << lane) - 1);  // heads after this lane
+    const int nxt = after ? __ffs(after) - 1 : d;
+    runs[w][__popc(heads & ((1u << lane) - 1))] = make_int2(x, nxt - lane);
+  }
+  __syncwarp();
+  int32_t key = 0x7fffffff, cntk = 0;
   if (lane < D) {
-    key = hkey[b + lane];
-    c = ctab[b + lane];
-    hc = (double)hcnt[b + lane] * c;
+    key = runs[w][lane].x;
+    cntk = runs[w][lane].y;
   }
-  hc = warp_sum(hc);
+  // chain table: C_i(key_k) = sum_a h_a F[key_k + di - 4 + x_a] - F[2 key_k + di - 4]
+  const int64_t base = (int64_t)key + d - 4;
+  double c = 0.0;
+  for (int a = 0; a < D; ++a) {
+    const int32_t xa = __shfl_sync(0xffffffffu, key, a);
+    const int32_t ha = __shfl_sync(0xffffffffu, cntk, a);
+    if (lane < D) c += (double)ha * __ldg(F + base + xa);
+  }
+  if (lane < D) c -= __ldg(F + base + key);
+  const double hc = warp_sum(lane < D ? (double)cntk * c : 0.0);
   if (lane == 0) ca.ws[i] = hc;
-  int32_t y = -2, v = 0;
-  if (lane < d) {
-    y = nd[b + lane];
-    v = nbr[b + lane];
-  }
+  // pushes: slot e takes C of its degree's run
   int idx = 0;
   for (int k = 0; k < D; ++k)
     if (__shfl_sync(0xffffffffu, key, k) == y) idx = k;
   const double val = __shfl_sync(0xffffffffu, c, idx);
-  if (lane < d) chain_push(ca, v, y, val, s1[i]);
+  if (lane < d) chain_push(ca, nbr[b + lane], y, val, s1[i]);
 }
 
 // d > 32: CTA per row.  Keys below kPushDirect (most neighbour degrees) are
@@ -1411,7 +1444,7 @@ static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, See
     select_seeds(ctx, ch, DegRange{off, 256, kHistBlockMax, nparts, part}, L.hb + o, cdev + cslot(kHB, k));
     select_seeds(ctx, ch, DegRange{off, kHistBlockMax, INT64_MAX, nparts, part}, L.hl + o, cdev + cslot(kHL, k));
     if (!seeds) continue;
-    select_seeds(ctx, ch, DegRange{off, -1, kCtabGroupMax, nparts, part}, L.cg + o, cdev + cslot(kCG, k));
+    select_seeds(ctx, ch, DegRange{off, kHistWarpMax, kCtabGroupMax, nparts, part}, L.cg + o, cdev + cslot(kCG, k));
     select_seeds(ctx, ch, DegRange{off, kCtabGroupMax, INT64_MAX, nparts, part}, L.cb + o, cdev + cslot(kCB, k));
   }
   if (!seeds) return L;
@@ -1430,13 +1463,13 @@ static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, See
 
 // Neighbour-degree histograms H_i for every node (slot space, see H build).
 static void build_histograms(Context& ctx, const Prepared& P, const Lists& L, const int64_t* c, const Staging& stg,
-                             int k, int32_t* hkey, int32_t* hcnt, int32_t* dcnt) {
+                             int k, int32_t* hkey, int32_t* hcnt, int32_t* dcnt, bool small_rows = true) {
   cudaStream_t s = ctx.stream;
   const int B = 256;
   const int64_t* off = P.g.offsets;
   const int64_t o = stg.row[k];
   const int64_t nw = c[cslot(kHW, k)], ns = c[cslot(kHS, k)], nb = c[cslot(kHB, k)], nl = c[cslot(kHL, k)];
-  EFG_LAUNCH(k_hist_warp, ceil_div(nw * 32, B), B, 0, s, L.hw + o, nw, off, P.nd, hkey, hcnt, dcnt);
+  if (small_rows) EFG_LAUNCH(k_hist_warp, ceil_div(nw * 32, B), B, 0, s, L.hw + o, nw, off, P.nd, hkey, hcnt, dcnt);
   int bits = 1;
   while (bits < 31 && (int64_t(1) << bits) <= (int64_t)P.dmax + 1) ++bits;
   EFG_LAUNCH((k_hist_block<64, 4>), ns, 64, 0, s, L.hs + o, ns, off, P.nd, hkey, hcnt, dcnt, bits);
@@ -1519,16 +1552,18 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   for (int k = 0; k < stg.nchunks; ++k) {
     if (stg.ready[k]) EFG_CUDA_CHECK(cudaStreamWaitEvent(s, stg.ready[k], 0));
     prepare_rows(ctx, P, stg.row[k], stg.row[k + 1], stg.slot[k], stg.slot[k + 1]);
-    build_histograms(ctx, P, L, c, stg, k, hkey, hcnt, dcnt);
-    // chain tables C_i(y): rows with d <= 64 by 8-lane groups, the rest by CTAs
+    build_histograms(ctx, P, L, c, stg, k, hkey, hcnt, dcnt, false);
+    // rows with d <= 32: histogram, chain table and pushes fused in registers
+    const int64_t nsm = c[cslot(kHW, k)];
+    EFG_LAUNCH(k_small_rows, ceil_div(nsm, kSmallWarps), kSmallWarps * 32, 0, s, L.hw + stg.row[k], nsm, g.offsets,
+               g.nbr, P.nd, P.deg, P.ftab, P.s1, ca);
+    // chain tables C_i(y): rows with 32 < d <= 64 by 8-lane groups, the rest by CTAs
     const int64_t o = stg.row[k], ng = c[cslot(kCG, k)], nb = c[cslot(kCB, k)];
     EFG_LAUNCH(k_ctab_group<8>, ceil_div(ng * 8, B), B, 0, s, L.cg + o, ng, g.offsets, dcnt, hkey, hcnt, P.deg,
                P.ftab, ctab);
     EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab);
     // chains pushed from the rows whose tables are now complete
-    const int64_t pw = c[cslot(kHW, k)], ps1 = c[cslot(kHS, k)], pb = c[cslot(kHB, k)], pl = c[cslot(kHL, k)];
-    EFG_LAUNCH(k_push_warp, ceil_div(pw * 32, B), B, 0, s, L.hw + o, pw, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt,
-               ctab, P.s1, ca);
+    const int64_t ps1 = c[cslot(kHS, k)], pb = c[cslot(kHB, k)], pl = c[cslot(kHL, k)];
     EFG_LAUNCH(k_push_block, ps1, kPushThreads, 0, s, L.hs + o, ps1, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,
                P.s1, ca);
     EFG_LAUNCH(k_push_block, pb, kPushThreads, 0, s, L.hb + o, pb, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,

@@ -91,7 +91,8 @@ def kernel_bytes_model(offsets, neighbors):
     """Algorithmic bytes per launch of the triangle-listing kernels.
 
     A whole-graph pass lists each triangle at its middle vertex v
-    (csrc/ef_factor.cu k_mid_block for dv > 32, k_mid_warp for dv <= 32):
+    (csrc/ef_factor.cu k_mid_big for dv > 256, k_mid_small for 32 < dv <= 256,
+    k_mid_warp for dv <= 32):
     every lower-ranked neighbour u of v is a row, and the label-sorted Adj+(u)
     is read up to v itself (pos_u(v) + 1 labels of 4 B).  Per examined slot of
     v's row 8 B (neighbour id + degree), per kept row 12 B (|Adj+(u)|, start),
@@ -123,8 +124,8 @@ def kernel_bytes_model(offsets, neighbors):
     rows_v = torch.bincount(v[keep], minlength=n)
     pv = torch.bincount(u, minlength=n)  # |Adj+| per node
     out = {}
-    for name, big in (("k_mid_block", True), ("k_mid_warp", False)):
-        msk = deg > 32 if big else deg <= 32
+    for name, lo, hi in (("k_mid_big", 256, 1 << 40), ("k_mid_small", 32, 256), ("k_mid_warp", -1, 32)):
+        msk = (deg > lo) & (deg <= hi)
         probes = int(probes_v[msk].sum())
         rows = int(rows_v[msk].sum())
         slots = int(deg[msk].sum())

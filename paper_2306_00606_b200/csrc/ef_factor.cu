@@ -953,8 +953,18 @@ constexpr int kMidThreads = 256;
 constexpr int kMidNB = 512;         // shared map of Adj+(v): <= 1024 keys at load <= 1/2
 constexpr int kMidLgNB = 9;
 constexpr int kMidMaxP = 1024;      // longer Adj+(v) are processed in parts of this size
-constexpr int kMidChunk = 256;
-constexpr int kMidUnroll = 4;      // rows between entry flushes: 32-bit entry words cannot overflow
+constexpr int kMidChunk = 256;     // rows between entry flushes: 32-bit entry words cannot overflow
+constexpr int kMidUnroll = 4;
+constexpr int kMidSmallDeg = 256;  // middle vertices of degree <= this run in small CTAs
+
+// CTA shapes of k_mid_block: big (hub tasks and degree > kMidSmallDeg) and
+// small (32 < degree <= kMidSmallDeg, where |Adj+(v)| and the rows are few).
+struct MidBig {
+  static constexpr int kThreads = kMidThreads, kNB = kMidNB, kLgNB = kMidLgNB, kMaxP = kMidMaxP, kChunk = kMidChunk;
+};
+struct MidSmall {
+  static constexpr int kThreads = 128, kNB = 128, kLgNB = 7, kMaxP = kMidSmallDeg, kChunk = kMidSmallDeg;
+};
 constexpr int kListScale = 40;      // P = rint(G * 2^40)
 constexpr int64_t kListMaxDeg = 1000000;  // |G(3 dmax)| < 32
 
@@ -975,7 +985,8 @@ struct MArgs {
   int64_t n, n32;           // labels < n32: degree > 32
   int64_t nhubs, ntasks;    // labels < nhubs come as ntasks row-range tasks
   int32_t part, nparts;     // distributed pass: this part takes work units u with u % nparts == part
-  int32_t nunits;           // k_mid_block work units: ntasks + (n32 - nhubs)
+  int32_t nunits;           // k_mid_block work units of this launch: ntasks hub tasks, then labels
+  int64_t label0;           // first label of the launch's label units
 };
 
 __global__ void k_gfix(const double* __restrict__ G, int64_t len, int64_t* __restrict__ PT) {
@@ -1186,20 +1197,22 @@ k_mid_warp(MArgs a) {
 // dv > 32 (labels < n32, hubs first): CTA per v, warps take rows.  Entry
 // sums of Adj+(v) in shared memory as 32-bit words (Q = -P split 22 + 23
 // bits, count), flushed every kMidChunk rows.
+template <class C>
 struct MidSmem {
-  int4 lk[kMidNB];
-  int64_t rps[kMidChunk];  // compacted rows of the current chunk: Adj+(u) start,
-  int32_t ru[kMidChunk], rdu[kMidChunk], rpu[kMidChunk];  // u, du, |Adj+(u)|
-  int32_t node[kMidMaxP], edeg[kMidMaxP];
-  uint32_t elo[kMidMaxP], ehi[kMidMaxP], ec[kMidMaxP];
-  int16_t lv[4 * kMidNB];
+  int4 lk[C::kNB];
+  int64_t rps[C::kChunk];  // compacted rows of the current chunk: Adj+(u) start,
+  int32_t ru[C::kChunk], rdu[C::kChunk], rpu[C::kChunk];  // u, du, |Adj+(u)|
+  int32_t node[C::kMaxP], edeg[C::kMaxP];
+  uint32_t elo[C::kMaxP], ehi[C::kMaxP], ec[C::kMaxP];
+  int16_t lv[4 * C::kNB];
   int32_t nrows;
 };
 
-template <bool PART>
-__global__ void __launch_bounds__(kMidThreads)
-k_mid_block(MArgs a, HubTasks tk) {
-  __shared__ MidSmem sm;
+template <bool PART, class C>
+__device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& tk) {
+  constexpr int kMidThreads = C::kThreads, kMidNB = C::kNB, kMidLgNB = C::kLgNB, kMidMaxP = C::kMaxP,
+                kMidChunk = C::kChunk;
+  __shared__ MidSmem<C> sm;
   const uint32_t kb = (uint32_t)__cvta_generic_to_shared(sm.lk), vb = (uint32_t)__cvta_generic_to_shared(sm.lv);
   const uint32_t eb_lo = (uint32_t)__cvta_generic_to_shared(sm.elo), eb_hi = (uint32_t)__cvta_generic_to_shared(sm.ehi),
                  eb_c = (uint32_t)__cvta_generic_to_shared(sm.ec);
@@ -1216,7 +1229,7 @@ k_mid_block(MArgs a, HubTasks tk) {
     x0 = tk.x0[unit];
     x1 = tk.x1[unit];
   } else {
-    v = __ldg(a.by_rank + a.nhubs + (unit - a.ntasks));
+    v = __ldg(a.by_rank + a.label0 + (unit - a.ntasks));
     x0 = 0;
     x1 = (int32_t)(__ldg(a.offsets + v + 1) - __ldg(a.offsets + v));
   }
@@ -1316,6 +1329,18 @@ k_mid_block(MArgs a, HubTasks tk) {
     atomicAdd(q + 1, (unsigned long long)vl);
     atomicAdd(q + 2, (unsigned long long)vc);
   }
+}
+
+// Launch shapes: the big instantiation keeps ptxas's own register choice (48,
+// with a few spill bytes: 5 CTAs per SM measured faster than 58 registers at
+// 4), the small one asks for 12 CTAs per SM.
+template <bool PART>
+__global__ void __launch_bounds__(MidBig::kThreads) k_mid_big(MArgs a, HubTasks tk) {
+  mid_block_body<PART, MidBig>(a, tk);
+}
+template <bool PART>
+__global__ void __launch_bounds__(MidSmall::kThreads, 12) k_mid_small(MArgs a, HubTasks tk) {
+  mid_block_body<PART, MidSmall>(a, tk);
 }
 
 // Per-seed results of the listing: t(v) and the two W_t words.
@@ -1661,11 +1686,20 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     ma.ntasks = ntasks;
     ma.nparts = dp ? dp->nparts : 1;
     ma.part = dp ? dp->part : 0;
-    ma.nunits = (int32_t)(ntasks + (ma.n32 - nhubs));
+    // big CTAs: hub tasks and labels [nhubs, n256); small CTAs: labels [n256, n32)
+    const int64_t n256 = c[kTr2] + c[kTr3] + c[kHubs];
+    ma.label0 = nhubs;
+    ma.nunits = (int32_t)(ntasks + (n256 - nhubs));
+    MArgs ms = ma;
+    ms.ntasks = 0;
+    ms.label0 = n256;
+    ms.nunits = (int32_t)(ma.n32 - n256);
     if (dp) {
-      EFG_LAUNCH(k_mid_block<true>, ceil_div(ntasks + (ma.n32 - nhubs), ma.nparts), kMidThreads, 0, s, ma, tk);
+      EFG_LAUNCH(k_mid_big<true>, ceil_div(ma.nunits, ma.nparts), MidBig::kThreads, 0, s, ma, tk);
+      EFG_LAUNCH(k_mid_small<true>, ceil_div(ms.nunits, ms.nparts), MidSmall::kThreads, 0, s, ms, tk);
     } else {
-      EFG_LAUNCH(k_mid_block<false>, ntasks + (ma.n32 - nhubs), kMidThreads, 0, s, ma, tk);
+      EFG_LAUNCH(k_mid_big<false>, ma.nunits, MidBig::kThreads, 0, s, ma, tk);
+      EFG_LAUNCH(k_mid_small<false>, ms.nunits, MidSmall::kThreads, 0, s, ms, tk);
     }
     EFG_LAUNCH(k_mid_warp, ceil_div(ceil_div(n - ma.n32, ma.nparts), kMidWarps), kMidWarps * 32, 0, s, ma);
     if (dp) return info;  // the caller reduces the words over all parts, then ef_finish

@@ -1075,7 +1075,7 @@ __device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu
 #pragma unroll
     for (int k = 0; k < U; ++k) d[k] = y[k] >= 0 ? degree(y[k], j[k]) : 0;
 #pragma unroll
-    for (int k = 0; k < U; ++k) g[k] = y[k] >= 0 ? __ldg(pt + d[k]) : 0;
+    for (int k = 0; k < U; ++k) g[k] = y[k] >= 0 ? __ldg(pt + (uint32_t)d[k]) : 0;  // 32-bit index off a row base
 #pragma unroll
     for (int k = 0; k < U; ++k)
       if (y[k] >= 0) hit(y[k], j[k], g[k]);
@@ -1089,6 +1089,11 @@ __device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu
 __device__ __forceinline__ int4 lds128(uint32_t addr) {
   int4 v;
   asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ int32_t lds32(uint32_t addr) {
+  int32_t v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ int32_t lds_s16(uint32_t addr) {
@@ -1215,7 +1220,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
   __shared__ MidSmem<C> sm;
   const uint32_t kb = (uint32_t)__cvta_generic_to_shared(sm.lk), vb = (uint32_t)__cvta_generic_to_shared(sm.lv);
   const uint32_t eb_lo = (uint32_t)__cvta_generic_to_shared(sm.elo), eb_hi = (uint32_t)__cvta_generic_to_shared(sm.ehi),
-                 eb_c = (uint32_t)__cvta_generic_to_shared(sm.ec);
+                 eb_c = (uint32_t)__cvta_generic_to_shared(sm.ec), db = (uint32_t)__cvta_generic_to_shared(sm.edeg);
   __shared__ int64_t red_h[kMidThreads / 32], red_l[kMidThreads / 32];
   __shared__ uint32_t red_c[kMidThreads / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -1290,7 +1295,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
         uint32_t rc = 0;
         mid_scan<kMidUnroll>(
             a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); },
-            [&](int32_t y, int32_t) { return sm.edeg[y]; },
+            [&](int32_t y, int32_t) { return lds32(db + 4 * y); },
             [&](int32_t y, int32_t, int64_t g) {
               rs += g;
               ++rc;

@@ -1083,6 +1083,18 @@ __device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu
   }
 }
 
+// Warp sums on the native reduction unit (REDUX): a 32-bit count directly,
+// a 64-bit row sum (|s| < 2^57 per lane) as three 26/26/12-bit pieces that
+// cannot overflow 32 bits over 32 lanes.
+__device__ __forceinline__ uint32_t warp_count(uint32_t c) { return __reduce_add_sync(0xffffffffu, c); }
+__device__ __forceinline__ int64_t warp_sum64(int64_t x) {
+  const uint32_t p0 = (uint32_t)(x & 0x3ffffff), p1 = (uint32_t)((x >> 26) & 0x3ffffff);
+  const int32_t p2 = (int32_t)(x >> 52);
+  const uint64_t s0 = __reduce_add_sync(0xffffffffu, p0), s1 = __reduce_add_sync(0xffffffffu, p1);
+  const int64_t s2 = __reduce_add_sync(0xffffffffu, p2);
+  return (int64_t)s0 + ((int64_t)s1 << 26) + (s2 << 52);
+}
+
 // Explicit shared-window loads for the listing's probe loop: the map base is
 // converted once, so the loop carries a 32-bit address instead of
 // re-deriving the shared window of a generic pointer on every probe.
@@ -1182,9 +1194,9 @@ k_mid_warp(MArgs a) {
           sP[w][y] += g;
           sC[w][y] += 1;
         });
-    rc = warp_sum(rc);
+    rc = warp_count(rc);
     if (rc) {
-      rs = warp_sum(rs);
+      rs = warp_sum64(rs);
       av.add_row(rs, rc);
       if (lane == 0) red_node(a.acc, ux, rs, rc);
     }
@@ -1304,9 +1316,9 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
               reds_add(eb_hi + 4 * y, (uint32_t)(q >> 22));
               reds_add(eb_c + 4 * y, 1u);
             });
-        rc = warp_sum(rc);
+        rc = warp_count(rc);
         if (rc) {
-          rs = warp_sum(rs);
+          rs = warp_sum64(rs);
           if (lane == 0) {
             red_node(a.acc, u, rs, rc);
             av.add_row(rs, rc);

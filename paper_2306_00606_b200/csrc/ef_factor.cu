@@ -499,6 +499,42 @@ k_push_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
   }
 }
 
+// 32 < d <= 256: warp per row, H_i's keys (<= 256) in the warp's shared slice,
+// binary search per slot.
+constexpr int kPushWarps = 8, kPushWarpKeys = 256;
+__global__ void __launch_bounds__(kPushWarps * 32)
+k_push_warp256(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
+               const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd, const int32_t* __restrict__ dcnt,
+               const int32_t* __restrict__ hkey, const int32_t* __restrict__ hcnt, const double* __restrict__ ctab,
+               const int64_t* __restrict__ s1, ChainAcc ca) {
+  __shared__ int32_t sk[kPushWarps][kPushWarpKeys];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t q = (int64_t)blockIdx.x * kPushWarps + w;
+  if (q >= count) return;
+  const int32_t i = rows[q];
+  const int64_t b = offsets[i];
+  const int d = (int)(offsets[i + 1] - b);
+  const int D = dcnt[i];
+  double hc = 0.0;
+  for (int k = lane; k < D; k += 32) {
+    sk[w][k] = hkey[b + k];
+    hc += (double)hcnt[b + k] * ctab[b + k];
+  }
+  hc = warp_sum(hc);
+  if (lane == 0) ca.ws[i] = hc;
+  __syncwarp();
+  const int64_t s1i = s1[i];
+  for (int p = lane; p < d; p += 32) {
+    const int32_t y = nd[b + p];
+    int lo = 0, hi = D - 1;  // y is present: v is a neighbour of i
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (sk[w][mid] < y) lo = mid + 1; else hi = mid;
+    }
+    chain_push(ca, nbr[b + p], y, __ldg(ctab + b + lo), s1i);
+  }
+}
+
 // ------------------------------------------------------------- triangles
 // W_t(v) = sum over triangles {v,i,j} of F(S-6) - F(S-4), S = dv+di+dj, and
 // t(v) = their number.  Every triangle at v is found exactly once through the
@@ -1606,8 +1642,8 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab);
     // chains pushed from the rows whose tables are now complete
     const int64_t ps1 = c[cslot(kHS, k)], pb = c[cslot(kHB, k)], pl = c[cslot(kHL, k)];
-    EFG_LAUNCH(k_push_block, ps1, kPushThreads, 0, s, L.hs + o, ps1, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,
-               P.s1, ca);
+    EFG_LAUNCH(k_push_warp256, ceil_div(ps1, kPushWarps), kPushWarps * 32, 0, s, L.hs + o, ps1, g.offsets, g.nbr,
+               P.nd, dcnt, hkey, hcnt, ctab, P.s1, ca);
     EFG_LAUNCH(k_push_block, pb, kPushThreads, 0, s, L.hb + o, pb, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,
                P.s1, ca);
     EFG_LAUNCH(k_push_block, pl, kPushThreads, 0, s, L.hl + o, pl, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,

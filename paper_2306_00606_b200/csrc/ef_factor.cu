@@ -997,9 +997,11 @@ constexpr int kMidSmallDeg = 256;  // middle vertices of degree <= this run in s
 // small (32 < degree <= kMidSmallDeg, where |Adj+(v)| and the rows are few).
 struct MidBig {
   static constexpr int kThreads = kMidThreads, kNB = kMidNB, kLgNB = kMidLgNB, kMaxP = kMidMaxP, kChunk = kMidChunk;
+  static constexpr int kBmWords = 2048;  // label bitmap for rank(v) <= 65536 (same shared bytes as the hash)
 };
 struct MidSmall {
   static constexpr int kThreads = 128, kNB = 128, kLgNB = 7, kMaxP = kMidSmallDeg, kChunk = kMidSmallDeg;
+  static constexpr int kBmWords = 0;
 };
 constexpr int kListScale = 40;      // P = rint(G * 2^40)
 constexpr int64_t kListMaxDeg = 1000000;  // |G(3 dmax)| < 32
@@ -1252,13 +1254,25 @@ k_mid_warp(MArgs a) {
 // bits, count), flushed every kMidChunk rows.
 template <class C>
 struct MidSmem {
-  int4 lk[C::kNB];
+  // Adj+(v) as a map label -> position: a bitmap over labels [0, rank(v)) with
+  // per-word prefix counts (positions are label ranks: Adj+ rows are sorted)
+  // when rank(v) is small enough, else a bucketed hash
+  union {
+    struct {
+      int4 lk[C::kNB];
+      int16_t lv[4 * C::kNB];
+    };
+    struct {
+      uint32_t bm[C::kBmWords > 0 ? C::kBmWords : 1];
+      int16_t bpre[C::kBmWords > 0 ? C::kBmWords : 1];
+    };
+  };
   int64_t rps[C::kChunk];  // compacted rows of the current chunk: Adj+(u) start,
   int32_t ru[C::kChunk], rdu[C::kChunk], rpu[C::kChunk];  // u, du, |Adj+(u)|
   int32_t node[C::kMaxP], edeg[C::kMaxP];
   uint32_t elo[C::kMaxP], ehi[C::kMaxP], ec[C::kMaxP];
-  int16_t lv[4 * C::kNB];
   int32_t nrows;
+  int32_t wtot[C::kThreads / 32];
 };
 
 template <bool PART, class C>
@@ -1299,18 +1313,55 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
     const int32_t np = min(pv - q0, kMidMaxP);
     const int32_t lim = q0 + np < pv ? __ldg(a.adjj + pb + q0 + np) : labv;
     const uint32_t lgl = min(32u - __clz(max(np, 2) - 1), (uint32_t)kMidLgNB);  // NB = min(2^lgl >= np, kMidNB)
+    const bool use_bm = C::kBmWords > 0 && lim <= 32 * C::kBmWords;              // block-uniform
+    const int nbw = use_bm ? (lim + 31) >> 5 : 0;
     __syncthreads();
-    for (int b = threadIdx.x; b < (1 << lgl); b += blockDim.x) sm.lk[b] = make_int4(-1, -1, -1, -1);
+    if (use_bm) {
+      for (int b = threadIdx.x; b < nbw; b += blockDim.x) sm.bm[b] = 0u;
+    } else {
+      for (int b = threadIdx.x; b < (1 << lgl); b += blockDim.x) sm.lk[b] = make_int4(-1, -1, -1, -1);
+    }
     __syncthreads();
     for (int t = threadIdx.x; t < np; t += blockDim.x) {
       const int32_t l = __ldg(a.adjj + pb + q0 + t);
-      smap_insert(sm.lk, sm.lv, lgl, l, t);
+      if (use_bm) atomicOr(&sm.bm[l >> 5], 1u << (l & 31));
+      else smap_insert(sm.lk, sm.lv, lgl, l, t);
       sm.node[t] = __ldg(a.by_rank + l);
       sm.edeg[t] = __ldg(a.deg_by_rank + l);
       sm.elo[t] = 0;
       sm.ehi[t] = 0;
       sm.ec[t] = 0;
     }
+    if (use_bm) {
+      // exclusive prefix of the words' popcounts: thread t owns words [t*per, (t+1)*per)
+      __syncthreads();
+      constexpr int per = C::kBmWords > 0 ? (C::kBmWords + kMidThreads - 1) / kMidThreads : 1;
+      int tot = 0;
+#pragma unroll
+      for (int k = 0; k < per; ++k) {
+        const int wi = threadIdx.x * per + k;
+        tot += wi < nbw ? __popc(sm.bm[wi]) : 0;
+      }
+      int incl = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (lane == 31) sm.wtot[w] = incl;
+      __syncthreads();
+      int base = incl - tot;
+      for (int k = 0; k < w; ++k) base += sm.wtot[k];
+#pragma unroll
+      for (int k = 0; k < per; ++k) {
+        const int wi = threadIdx.x * per + k;
+        if (wi < nbw) {
+          sm.bpre[wi] = (int16_t)base;
+          base += __popc(sm.bm[wi]);
+        }
+      }
+    }
+    const uint32_t bmb = (uint32_t)__cvta_generic_to_shared(sm.bm), bpb = (uint32_t)__cvta_generic_to_shared(sm.bpre);
     for (int32_t c0 = x0; c0 < x1; c0 += kMidChunk) {
       // compact the chunk's rows (lower-ranked u with |Adj+(u)| >= 2) into shared memory
       __syncthreads();
@@ -1342,7 +1393,12 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
         int64_t rs = 0;
         uint32_t rc = 0;
         mid_scan<kMidUnroll>(
-            a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); },
+            a, psu, pu, lim, dv + du, lane,
+            [&](int32_t key) {
+              if (!use_bm) return mfind(kb, vb, lgl, key);
+              const uint32_t word = (uint32_t)lds32(bmb + 4 * (key >> 5)), bit = 1u << (key & 31);
+              return word & bit ? lds_s16(bpb + 2 * (key >> 5)) + __popc(word & (bit - 1)) : -1;
+            },
             [&](int32_t y, int32_t) { return lds32(db + 4 * y); },
             [&](int32_t y, int32_t, int64_t g) {
               rs += g;
@@ -1384,11 +1440,10 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
   }
 }
 
-// Launch shapes: the big instantiation keeps ptxas's own register choice (48,
-// with a few spill bytes: 5 CTAs per SM measured faster than 58 registers at
-// 4), the small one asks for 12 CTAs per SM.
+// Launch shapes: 5 CTAs per SM for the big instantiation (<= 51 registers:
+// measured 14.6 ms against 15.6 at 63 registers / 4 CTAs), 12 for the small.
 template <bool PART>
-__global__ void __launch_bounds__(MidBig::kThreads) k_mid_big(MArgs a, HubTasks tk) {
+__global__ void __launch_bounds__(MidBig::kThreads, 5) k_mid_big(MArgs a, HubTasks tk) {
   mid_block_body<PART, MidBig>(a, tk);
 }
 template <bool PART>

@@ -317,11 +317,16 @@ k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __r
         sh[q] = (double)hcnt[b + q0 + q];
       }
       __syncthreads();
+      static_assert(kCtabOut <= 8, "ctab_outputs dispatch covers K <= 8");
       switch (K) {
         case 1: ctab_outputs<1>(sx, sh, nq, base, F, acc); break;
         case 2: ctab_outputs<2>(sx, sh, nq, base, F, acc); break;
         case 3: ctab_outputs<3>(sx, sh, nq, base, F, acc); break;
-        default: ctab_outputs<4>(sx, sh, nq, base, F, acc); break;
+        case 4: ctab_outputs<4>(sx, sh, nq, base, F, acc); break;
+        case 5: ctab_outputs<kCtabOut >= 5 ? 5 : 1>(sx, sh, nq, base, F, acc); break;
+        case 6: ctab_outputs<kCtabOut >= 6 ? 6 : 1>(sx, sh, nq, base, F, acc); break;
+        case 7: ctab_outputs<kCtabOut >= 7 ? 7 : 1>(sx, sh, nq, base, F, acc); break;
+        default: ctab_outputs<kCtabOut>(sx, sh, nq, base, F, acc); break;
       }
     }
 #pragma unroll

@@ -1815,7 +1815,15 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
       EFG_LAUNCH(k_mid_small<false>, ms.nunits, MidSmall::kThreads, 0, s, ms, tk);
     }
     EFG_LAUNCH(k_mid_warp, ceil_div(ceil_div(n - ma.n32, ma.nparts), kMidWarps), kMidWarps * 32, 0, s, ma);
-    if (dp) return info;  // the caller reduces the words over all parts, then ef_finish
+    if (dp) {  // the caller reduces the words over all parts, then ef_finish (which reuses S1/S2)
+      ctx.part_cache.offsets = g.offsets;
+      ctx.part_cache.nbr = g.nbr;
+      ctx.part_cache.n = n;
+      ctx.part_cache.m2 = g.m2;
+      ctx.part_cache.dmax = P.dmax;
+      ctx.part_cache.valid = true;
+      return info;
+    }
     EFG_LAUNCH(k_list_out, ceil_div(cnt, B), B, 0, s, acc, a, cnt);
   } else if (nhubs) {
     // exact bitmaps over rank labels, per-task partials merged in task order
@@ -1862,9 +1870,17 @@ void ef_finish(Context& ctx, const CSRView& g, SeedRange r, const unsigned long 
   const int B = 256;
   const int64_t n = g.n, cnt = r.hi - r.lo;
   if (cnt <= 0) return;
+  const auto& pc = ctx.part_cache;
   Prepared P;
-  prepare_head(ctx, g, false, P);
-  prepare_rows(ctx, P, 0, n, 0, g.m2);
+  if (pc.valid && pc.offsets == g.offsets && pc.nbr == g.nbr && pc.n == n && pc.m2 == g.m2) {
+    // S1/S2 of the preceding ef_partial on this graph are still resident
+    P.s1 = ctx.buf("s1").as<int64_t>(n);
+    P.s2 = ctx.buf("s2").as<int64_t>(n);
+    P.dmax = pc.dmax;
+  } else {
+    prepare_head(ctx, g, false, P);
+    prepare_rows(ctx, P, 0, n, 0, g.m2);
+  }
   FArgs a{};
   a.offsets = g.offsets;
   a.s1 = P.s1;

@@ -47,6 +47,15 @@ struct Context {
   std::map<std::string, DevBuf> bufs;
   std::mutex mu;
   cudaEvent_t ev[16] = {};
+  // S1/S2/dmax of the last distributed part (ef_partial) for the ef_finish that
+  // follows on the same graph; any other preparation invalidates it
+  struct {
+    const int64_t* offsets = nullptr;
+    const int32_t* nbr = nullptr;
+    int64_t n = -1, m2 = -1;
+    int32_t dmax = 0;
+    bool valid = false;
+  } part_cache;
   cudaStream_t copy_stream = nullptr;   // host->device staging of efg_expected_force inputs
   cudaEvent_t chunk_ev[9] = {};         // offsets + neighbour chunks resident (kMaxChunks + 1)
   Profiler prof;

@@ -235,6 +235,7 @@ struct Choose2 {
 // Offsets-only part: degrees, dmax (the one host sync), the F/G tables and
 // the rank labels.  Runs while the neighbour arrays may still be in flight.
 void prepare_head(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P) {
+  ctx.part_cache.valid = false;  // the s1/s2/deg buffers are about to be rewritten
   cudaStream_t s = ctx.stream;
   const int B = 256;
   P.g = g;

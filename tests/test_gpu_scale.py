@@ -164,3 +164,20 @@ def test_distributed_parts_bitwise(rmat18, nparts):
     torch.cuda.synchronize()
     for x, y in zip(full, out):
         assert torch.equal(x, y)
+
+
+def test_star_beyond_listing_bound():
+    # a star with more than 10^6 leaves: maximum degree above the listing's
+    # fixed-point bound, so the whole-graph pass takes the per-seed triangle
+    # path; closed forms: centre EF = ln(k(k-1)), leaf EF = ln(k-1)
+    k = 1_000_001
+    edges = np.stack([np.zeros(k, np.int64), np.arange(1, k + 1, dtype=np.int64)], 1)
+    g = efg.build_graph(edges)
+    r = efg.ef_cluster_centric(g)
+    deg = np.diff(g.offsets)
+    centre = int(np.argmax(deg))
+    assert deg[centre] == k
+    assert ef_close(np.array([r.ef[centre]]), np.array([np.log(k * (k - 1.0))]))
+    leaves = np.flatnonzero(deg == 1)
+    assert np.all(np.abs(r.ef[leaves] - np.log(k - 1.0)) <= 1e-9 * np.log(k - 1.0) + 1e-12)
+    assert np.array_equal(r.cluster_total, deg * (deg - 1) + np.add.reduceat(deg[g.neighbors], g.offsets[:-1]) - deg)

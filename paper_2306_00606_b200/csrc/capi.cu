@@ -55,6 +55,8 @@ Context::~Context() {
   csr.b_orig.release();
   for (auto& e : ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : aux_ev)
+    if (e) cudaEventDestroy(e);
   for (auto& e : chunk_ev)
     if (e) cudaEventDestroy(e);
   if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -189,6 +191,7 @@ int efg_create(int device, efg_ctx** out) {
     c.own_stream = true;
     for (auto& x : c.ev) EFG_CUDA_CHECK(cudaEventCreate(&x));
     for (auto& x : c.chunk_ev) EFG_CUDA_CHECK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    for (auto& x : c.aux_ev) EFG_CUDA_CHECK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     EFG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
     EFG_CUDA_CHECK(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
   });
@@ -355,10 +358,15 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
     uint8_t* d_fl = c.buf("o_fl").as<uint8_t>(n);
     int64_t* d_T = T_out ? c.buf("o_T").as<int64_t>(n) : nullptr;
     double* d_W = W_out ? c.buf("o_W").as<double>(n) : nullptr;
+    stg.total_host = cluster_total;
+    c.total_sent = false;
     run_engine(c, g, stg, efg::SeedRange{0, n}, eng, d_ef, d_tot, d_fl, d_T, d_W, st);
     EFG_CUDA_CHECK(cudaEventRecord(ev[5], c.stream));
     EFG_CUDA_CHECK(cudaMemcpyAsync(ef, d_ef, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
-    EFG_CUDA_CHECK(cudaMemcpyAsync(cluster_total, d_tot, n * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    if (c.total_sent)  // the engine already queued it on the copy stream
+      EFG_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.aux_ev[1], 0));
+    else
+      EFG_CUDA_CHECK(cudaMemcpyAsync(cluster_total, d_tot, n * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
     EFG_CUDA_CHECK(cudaMemcpyAsync(flags, d_fl, n, cudaMemcpyDeviceToHost, c.stream));
     if (T_out) EFG_CUDA_CHECK(cudaMemcpyAsync(T_out, d_T, n * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
     if (W_out) EFG_CUDA_CHECK(cudaMemcpyAsync(W_out, d_W, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));

@@ -1494,10 +1494,19 @@ __global__ void k_epilogue(FArgs a, int64_t count, double* __restrict__ ef, int6
   // positive-degree cluster class exists (EF mathematically 0)
   if (T > 0) e = fmax(log((double)T) - W / (double)T, 0.0);
   ef[q] = e;
-  total[q] = mass;
+  if (total) total[q] = mass;
   flags[q] = mass == 0 ? 1 : (T == 0 ? 2 : 0);
   if (T_out) T_out[q] = T;
   if (W_out) W_out[q] = W;
+}
+
+// Cluster totals |C(v)| = dv(dv-1) + S1(v) - dv (the epilogue's `mass`).
+__global__ void k_mass(const int64_t* __restrict__ offsets, const int64_t* __restrict__ s1, int64_t n,
+                       int64_t* __restrict__ total) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int64_t dv = offsets[v + 1] - offsets[v];
+  total[v] = dv * (dv - 1) + s1[v] - dv;
 }
 
 struct DegRange {
@@ -1708,6 +1717,16 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
                P.s1, ca);
     EFG_LAUNCH(k_push_block, pl, kPushThreads, 0, s, L.hl + o, pl, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,
                P.s1, ca);
+  }
+  if (stg.total_host && !dp && r.lo == 0 && r.hi == n && n > 0) {
+    // S1 is complete: cluster totals now, their read-back overlaps the listing
+    EFG_LAUNCH(k_mass, ceil_div(n, B), B, 0, s, g.offsets, P.s1, n, total);
+    EFG_CUDA_CHECK(cudaEventRecord(ctx.aux_ev[0], s));
+    EFG_CUDA_CHECK(cudaStreamWaitEvent(ctx.copy_stream, ctx.aux_ev[0], 0));
+    EFG_CUDA_CHECK(cudaMemcpyAsync(stg.total_host, total, n * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.copy_stream));
+    EFG_CUDA_CHECK(cudaEventRecord(ctx.aux_ev[1], ctx.copy_stream));
+    ctx.total_sent = true;
+    total = nullptr;
   }
   prepare_tail(ctx, P, true);
   if (st) EFG_CUDA_CHECK(cudaEventRecord(ctx.ev[3], s));

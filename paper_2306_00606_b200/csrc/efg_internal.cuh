@@ -58,6 +58,8 @@ struct Context {
   } part_cache;
   cudaStream_t copy_stream = nullptr;   // host->device staging of efg_expected_force inputs
   cudaEvent_t chunk_ev[9] = {};         // offsets + neighbour chunks resident (kMaxChunks + 1)
+  cudaEvent_t aux_ev[2] = {};           // early cluster-total read-back: totals written / copied
+  bool total_sent = false;              // set by the engine when it queued that read-back
   Profiler prof;
   DeviceCSR csr;  // resident graph of efg_build_graph / efg_rmat_build
   DevBuf& buf(const std::string& name) { return bufs[name]; }
@@ -120,6 +122,10 @@ struct Staging {
   int64_t row[kMaxChunks + 1] = {};   // row bounds
   int64_t slot[kMaxChunks + 1] = {};  // offsets[row[k]]
   cudaEvent_t ready[kMaxChunks] = {};
+  // whole-graph pass from host inputs: cluster totals depend only on degrees
+  // and S1, so they are read back to `total_host` on the copy stream while the
+  // listing still runs (the epilogue then skips them)
+  int64_t* total_host = nullptr;
 };
 
 // ef_factor.cu -- factorised cluster-centric engine

@@ -49,6 +49,8 @@ __device__ __forceinline__ bool ranks_above(int32_t dj, int32_t j, int32_t di, i
 // v, compacted in order as rank labels + degrees into v's own slot range
 // [offsets[v], offsets[v] + dplus[v]) -- slot space, so no scan is needed and
 // the pass runs per row chunk while the rest of the graph is still copied.
+constexpr int kRowUnroll = 4;
+
 __global__ void k_row_sums(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
                            const int32_t* __restrict__ nd, int64_t r0, int64_t r1, int64_t* __restrict__ s1,
                            int64_t* __restrict__ s2, int32_t* __restrict__ dplus, const int32_t* __restrict__ rank_of,
@@ -60,24 +62,38 @@ __global__ void k_row_sums(const int64_t* __restrict__ offsets, const int32_t* _
   int32_t dv = (int32_t)(e - b);
   int64_t s = 0, q = 0;
   int64_t out = b;
-  for (int64_t p0 = b; p0 < e; p0 += 32) {
-    const int64_t p = p0 + lane;
-    int32_t j = 0, dj = 0;
-    bool take = false;
-    if (p < e) {
-      j = nbr[p];
-      dj = nd[p];
-      s += dj;
-      q += (int64_t)dj * dj;
-      take = ranks_above(dj, j, dv, (int32_t)v);
+  // kRowUnroll groups of 32 per iteration: all loads of a group are in flight
+  // together (hub rows are one warp's serial chain otherwise)
+  constexpr int U = kRowUnroll;
+  for (int64_t p0 = b; p0 < e; p0 += 32 * U) {
+    int32_t j[U], dj[U], lab[U];
+    bool take[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t p = p0 + 32 * k + lane;
+      j[k] = p < e ? nbr[p] : 0;
+      dj[k] = p < e ? nd[p] : 0;
     }
-    const unsigned mask = __ballot_sync(0xffffffffu, take);
-    if (take && adjj) {
-      const int64_t o = out + __popc(mask & ((1u << lane) - 1));
-      adjj[o] = __ldg(rank_of + j);
-      adjd[o] = dj;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      take[k] = false;
+      if (p0 + 32 * k + lane < e) {
+        s += dj[k];
+        q += (int64_t)dj[k] * dj[k];
+        take[k] = ranks_above(dj[k], j[k], dv, (int32_t)v);
+      }
+      lab[k] = take[k] && adjj ? __ldg(rank_of + j[k]) : 0;
     }
-    out += __popc(mask);
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const unsigned mask = __ballot_sync(0xffffffffu, take[k]);
+      if (take[k] && adjj) {
+        const int64_t o = out + __popc(mask & ((1u << lane) - 1));
+        adjj[o] = lab[k];
+        adjd[o] = dj[k];
+      }
+      out += __popc(mask);
+    }
   }
   for (int o = 16; o; o >>= 1) {
     s += __shfl_xor_sync(0xffffffffu, s, o);

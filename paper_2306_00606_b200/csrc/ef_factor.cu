@@ -274,13 +274,14 @@ __global__ void k_ctab_group(const int32_t* __restrict__ rows, int64_t count, co
 // and Z >= base + x_first bounds |delta|/Z by 0.135 (checked per tile), so
 // the truncation at K = 15 is below 1e-16 of the sum.  Tiles of at least
 // kExpMin members are expanded (one F gather + K FMAs per output instead of
-// one gather per member; R-MAT22: 83 % of the terms); the rest are summed
+// one gather per member; R-MAT22: 92 % of the terms); the rest are summed
 // term by term.  Fixed per-output summation order (deterministic).
 constexpr int kCtabStage = 1024;
 constexpr int kCtabThreads = 128;
 constexpr int kCtabOut = 4;
-constexpr int kExpK = 15, kExpTiles = 64, kExpGrid = 128, kExpMin = 24, kExpMinD = 128;
+constexpr int kExpK = 15, kExpTiles = 64, kExpGrid = 128, kExpMin = 12, kExpMinD = 128;
 constexpr double kExpRatio = 0.135;
+constexpr float kExpGrowth = 1.25f;  // tile t: x in [base (g^t - 1), base (g^(t+1) - 1))
 
 template <int K>
 __device__ __forceinline__ void ctab_outputs(const int32_t* __restrict__ sx, const double* __restrict__ sh, int nq,
@@ -298,21 +299,25 @@ __device__ __forceinline__ void ctab_outputs(const int32_t* __restrict__ sx, con
   }
 }
 
-__device__ __forceinline__ int exp_tile(int32_t x, double inv_base, double inv_l125) {
-  return (int)fmin(log1p((double)x * inv_base) * inv_l125, (double)kExpGrid);
+// tile of input x (fast single precision: a boundary off by one only moves a
+// member to a neighbouring tile, and every expanded tile's ratio is checked)
+__device__ __forceinline__ int exp_tile(int32_t x, float inv_base, float inv_lg) {
+  return (int)fminf(__log2f(fmaf((float)x, inv_base, 1.0f)) * inv_lg, (float)kExpGrid);
 }
 
 __global__ void __launch_bounds__(kCtabThreads)
 k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __restrict__ offsets,
              const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey, const int32_t* __restrict__ hcnt,
-             const int32_t* __restrict__ deg, const double* __restrict__ F, double* __restrict__ ctab) {
+             const int32_t* __restrict__ deg, const double* __restrict__ F, double* __restrict__ ctab,
+             int exp_min, int exp_min_d) {
   __shared__ int32_t sx[kCtabStage];
   __shared__ double sh[kCtabStage];
   __shared__ int32_t tbeg[kExpGrid], tend[kExpGrid];
   __shared__ int32_t ebeg[kExpTiles], eend[kExpTiles], exc[kExpTiles];  // expanded tiles: entries, centre
   __shared__ double ecoef[kExpTiles][kExpK + 2];                         // m0, m1, c_1..c_K
   __shared__ int32_t rlo[kExpTiles + 1], rpre[kExpTiles + 2];            // direct ranges: start, prefix
-  __shared__ int32_t sne, snr;
+  __shared__ int32_t emp[kExpTiles], wcnt[kCtabThreads / 32], wmem[kCtabThreads / 32];
+  __shared__ int32_t sne;
   const int64_t r = blockIdx.x;
   if (r >= nrows) return;
   const int32_t i = rows[r];
@@ -322,9 +327,9 @@ k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __r
   constexpr int T = kCtabThreads;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int ne = 0, nr = 1;
-  if (D >= kExpMinD) {
+  if (D >= exp_min_d) {
     const double tb = (double)(di - 3);
-    const double inv_base = 1.0 / tb, inv_l125 = 1.0 / log(1.25);
+    const float inv_base = 1.0f / (float)tb, inv_l125 = 1.0f / log2f(kExpGrowth);
     for (int t = threadIdx.x; t < kExpGrid; t += T) tbeg[t] = -1;
     __syncthreads();
     for (int a = threadIdx.x; a < D; a += T) {
@@ -335,36 +340,52 @@ k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __r
       }
     }
     __syncthreads();
-    if (threadIdx.x == 0) {  // expanded tiles in ascending order and the direct ranges around them
-      int n_e = 0, n_r = 0, cur = 0, pre = 0;
-      for (int t = 0; t < kExpGrid && n_e < kExpTiles; ++t) {
-        const int32_t a0 = tbeg[t];
-        if (a0 < 0) continue;
-        const int32_t a1 = tend[t];
-        if (a1 - a0 < kExpMin) continue;
-        const int32_t x0 = hkey[b + a0], x1 = hkey[b + a1 - 1], xc = (x0 + x1) >> 1;
-        if ((double)max(xc - x0, x1 - xc) > kExpRatio * (tb + (double)x0)) continue;
-        ebeg[n_e] = a0;
-        eend[n_e] = a1;
-        exc[n_e] = xc;
-        ++n_e;
-        rlo[n_r] = cur;
-        rpre[n_r] = pre;
-        pre += a0 - cur;
-        ++n_r;
-        cur = a1;
+    {  // thread t judges grid tile t; expanded tiles compacted in ascending order by a block scan
+      static_assert(kExpGrid == T, "one grid tile per thread");
+      const int t = threadIdx.x;
+      const int32_t a0 = tbeg[t], a1 = a0 >= 0 ? tend[t] : 0;
+      int32_t xc = 0;
+      bool ok = a0 >= 0 && a1 - a0 >= exp_min;
+      if (ok) {
+        const int32_t x0 = hkey[b + a0], x1 = hkey[b + a1 - 1];
+        xc = (x0 + x1) >> 1;
+        ok = (double)max(xc - x0, x1 - xc) <= kExpRatio * (tb + (double)x0);
       }
-      rlo[n_r] = cur;
-      rpre[n_r] = pre;
-      pre += D - cur;
-      ++n_r;
-      rpre[n_r] = pre;
-      sne = n_e;
-      snr = n_r;
+      const int own = ok ? a1 - a0 : 0;
+      int f = ok, mem = own;  // inclusive warp prefix of (flag, members)
+      for (int o = 1; o < 32; o <<= 1) {
+        const int fu = __shfl_up_sync(0xffffffffu, f, o), mu = __shfl_up_sync(0xffffffffu, mem, o);
+        if (lane >= o) f += fu, mem += mu;
+      }
+      if (lane == 31) wcnt[w] = f, wmem[w] = mem;
+      __syncthreads();
+      int fb = 0, mb = 0, ft = 0;
+      for (int u = 0; u < T / 32; ++u) {
+        if (u < w) fb += wcnt[u], mb += wmem[u];
+        ft += wcnt[u];
+      }
+      const int e = fb + f - ok;  // tiles past kExpTiles stay direct
+      if (ok && e < kExpTiles) {
+        ebeg[e] = a0;
+        eend[e] = a1;
+        exc[e] = xc;
+        emp[e] = mb + mem - own;  // members of the expanded tiles before e
+      }
+      const int n_e = min(ft, kExpTiles);
+      __syncthreads();
+      if (t <= n_e) {  // direct range t = [eend[t-1] or 0, ebeg[t] or D), rpre = direct entries before it
+        const int32_t lo = t ? eend[t - 1] : 0;
+        const int32_t mp = t < n_e ? emp[t] : (n_e ? emp[n_e - 1] + eend[n_e - 1] - ebeg[n_e - 1] : 0);
+        rlo[t] = lo;
+        rpre[t] = lo - mp;
+        if (t == n_e) rpre[t + 1] = D - mp;
+      }
+      if (t == 0) sne = n_e;
     }
     __syncthreads();
     ne = sne;
-    nr = snr;
+    nr = ne + 1;
+
     // moments: warp per expanded tile, fixed lane order and butterfly
     for (int e = w; e < ne; e += T / 32) {
       double m[kExpK + 2];
@@ -1830,7 +1851,8 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     const int64_t o = stg.row[k], ng = c[cslot(kCG, k)], nb = c[cslot(kCB, k)];
     EFG_LAUNCH(k_ctab_group<8>, ceil_div(ng * 8, B), B, 0, s, L.cg + o, ng, g.offsets, dcnt, hkey, hcnt, P.deg,
                P.ftab, ctab);
-    EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab);
+    EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab,
+               kExpMin, kExpMinD);
     // chains pushed from the rows whose tables are now complete
     const int64_t ps1 = c[cslot(kHS, k)], pb = c[cslot(kHB, k)], pl = c[cslot(kHL, k)];
     EFG_LAUNCH(k_push_warp256, ceil_div(ps1, kPushWarps), kPushWarps * 32, 0, s, L.hs + o, ps1, g.offsets, g.nbr,

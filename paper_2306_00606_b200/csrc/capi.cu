@@ -334,9 +334,11 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
     // equal sizes -- splitting kernels costs launch tails), the first one small:
     // the engine starts once it lands and its rows (low ids: the heavy hubs in
     // skewed graphs) keep the GPU busy while the rest copies.  First-chunk share
-    // measured: 50 %: 45.6, 25 %: 44.2, 15 %: 43.6, 10 %: 44.0, 5 %: 44.8 ms e2e.
+    // measured: 50 %: 45.6, 25 %: 44.2, 15 %: 43.6, 10 %: 44.0, 5 %: 44.8 ms e2e; after the
+    // chain-table expansion (32.7 ms pass): 10 %: 37.7, 15 %: 37.3, 25 %: 37.0, 35 %: 37.4;
+    // three chunks (15/50, 25/60 %): 38.0, 38.4.
     stg.nchunks = m2 >= (int64_t(1) << 22) ? 2 : 1;
-    const int first_pct = 15;
+    const int first_pct = 25;
     for (int k = 0; k <= stg.nchunks; ++k) {
       const int64_t target = k == 0 ? 0 : k == stg.nchunks ? m2 : m2 * first_pct / 100;
       stg.row[k] = k == stg.nchunks ? n : std::lower_bound(offsets, offsets + n + 1, target) - offsets;

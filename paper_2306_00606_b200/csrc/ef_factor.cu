@@ -1540,22 +1540,27 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
         const int64_t psu = sm.rps[x];
         int64_t rs = 0;
         uint32_t rc = 0;
-        mid_scan<kMidUnroll>(
-            a, psu, pu, lim, dv + du, lane,
-            [&](int32_t key) {
-              if (!use_bm) return mfind(kb, vb, lgl, key);
-              const uint32_t word = (uint32_t)lds32(bmb + 4 * (key >> 5)), bit = 1u << (key & 31);
-              return word & bit ? lds_s16(bpb + 2 * (key >> 5)) + __popc(word & (bit - 1)) : -1;
-            },
-            [&](int32_t y, int32_t) { return lds32(db + 4 * y); },
-            [&](int32_t y, int32_t, int64_t g) {
-              rs += g;
-              ++rc;
-              const uint64_t q = (uint64_t)(-g);
-              reds_add(eb_lo + 4 * y, (uint32_t)(q & 0x3fffff));
-              reds_add(eb_hi + 4 * y, (uint32_t)(q >> 22));
-              reds_add(eb_c + 4 * y, 1u);
-            });
+        const auto degree = [&](int32_t y, int32_t) { return lds32(db + 4 * y); };
+        const auto hit = [&](int32_t y, int32_t, int64_t g) {
+          rs += g;
+          ++rc;
+          const uint64_t q = (uint64_t)(-g);
+          reds_add(eb_lo + 4 * y, (uint32_t)(q & 0x3fffff));
+          reds_add(eb_hi + 4 * y, (uint32_t)(q >> 22));
+          reds_add(eb_c + 4 * y, 1u);
+        };
+        // the map kind is block-uniform: one loop per kind, no branch in the probe
+        if (use_bm)
+          mid_scan<kMidUnroll>(
+              a, psu, pu, lim, dv + du, lane,
+              [&](int32_t key) {
+                const uint32_t word = (uint32_t)lds32(bmb + 4 * (key >> 5)), bit = 1u << (key & 31);
+                return word & bit ? lds_s16(bpb + 2 * (key >> 5)) + __popc(word & (bit - 1)) : -1;
+              },
+              degree, hit);
+        else
+          mid_scan<kMidUnroll>(
+              a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); }, degree, hit);
         rc = warp_count(rc);
         if (rc) {
           rs = warp_sum64(rs);

@@ -1236,7 +1236,7 @@ __device__ __forceinline__ void smap_insert(int4* keys, V* vals, uint32_t lg, in
 // Scan of one row Adj+(u)[lane::32] in phases of kUnroll entries (labels +
 // degrees, then membership, then the G gathers), calling hit(y, label, P)
 // for every w found in Adj+(v) (y = its position there).
-template <int U, class Find, class Deg, class Hit>
+template <int U, bool BF = false, class Find, class Deg, class Hit>
 __device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu, int32_t lim, int32_t s0, int lane,
                                          Find find, Deg degree, Hit hit) {
   // Adj+(u) is sorted by label and only labels < lim = rank(v) can lie in
@@ -1254,12 +1254,25 @@ __device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu
     bool past = false;
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      past |= j[k] >= lim;
-      y[k] = j[k] < lim ? find(j[k]) : -1;
+      const bool in = j[k] < lim;
+      past |= !in;
+      if (BF) {  // branch-free (cheap constant-time maps): every lane looks up a valid key, misses selected away
+        const int32_t yy = find(in ? j[k] : 0);
+        y[k] = in ? yy : -1;
+      } else {
+        y[k] = in ? find(j[k]) : -1;
+      }
     }
     // only hits need w's degree: looked up by its position in Adj+(v) (4 B streamed per probe instead of 8)
 #pragma unroll
-    for (int k = 0; k < U; ++k) d[k] = y[k] >= 0 ? degree(y[k], j[k]) : 0;
+    for (int k = 0; k < U; ++k) {
+      if (BF) {
+        const int32_t dd = degree(y[k] >= 0 ? y[k] : 0, j[k]);
+        d[k] = y[k] >= 0 ? dd : 0;
+      } else {
+        d[k] = y[k] >= 0 ? degree(y[k], j[k]) : 0;
+      }
+    }
 #pragma unroll
     for (int k = 0; k < U; ++k) g[k] = y[k] >= 0 ? __ldg(pt + (uint32_t)d[k]) : 0;  // 32-bit index off a row base
 #pragma unroll
@@ -1286,17 +1299,17 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t x) {
 // re-deriving the shared window of a generic pointer on every probe.
 __device__ __forceinline__ int4 lds128(uint32_t addr) {
   int4 v;
-  asm volatile("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  asm("ld.shared.v4.s32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ int32_t lds32(uint32_t addr) {
   int32_t v;
-  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
+  asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
 __device__ __forceinline__ int32_t lds_s16(uint32_t addr) {
   short v;
-  asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(addr));
+  asm("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(addr));
   return v;
 }
 
@@ -1551,7 +1564,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
         };
         // the map kind is block-uniform: one loop per kind, no branch in the probe
         if (use_bm)
-          mid_scan<kMidUnroll>(
+          mid_scan<kMidUnroll, true>(
               a, psu, pu, lim, dv + du, lane,
               [&](int32_t key) {
                 const uint32_t word = (uint32_t)lds32(bmb + 4 * (key >> 5)), bit = 1u << (key & 31);

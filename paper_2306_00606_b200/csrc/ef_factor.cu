@@ -1138,7 +1138,10 @@ constexpr int kMidNB = 512;         // shared map of Adj+(v): <= 1024 keys at lo
 constexpr int kMidLgNB = 9;
 constexpr int kMidMaxP = 1024;      // longer Adj+(v) are processed in parts of this size
 constexpr int kMidChunk = 256;     // rows between entry flushes: 32-bit entry words cannot overflow
-constexpr int kMidUnroll = 4;
+// probe-loop unroll (entries per lane per step), measured per loop: k_mid_warp 2
+// (0.85 vs 0.95 ms at 4), bitmap 2 (12.6 vs 13.2 ms), hash 4 in big CTAs, 2 in small
+constexpr int kMidUnroll = 2;
+constexpr int kMidUnrollBm = 2;
 constexpr int kMidSmallDeg = 256;  // middle vertices of degree <= this run in small CTAs
 
 // CTA shapes of k_mid_block: big (hub tasks and degree > kMidSmallDeg) and
@@ -1146,10 +1149,12 @@ constexpr int kMidSmallDeg = 256;  // middle vertices of degree <= this run in s
 struct MidBig {
   static constexpr int kThreads = kMidThreads, kNB = kMidNB, kLgNB = kMidLgNB, kMaxP = kMidMaxP, kChunk = kMidChunk;
   static constexpr int kBmWords = 2048;  // label bitmap for rank(v) <= 65536 (same shared bytes as the hash)
+  static constexpr int kUnrollHash = 4;
 };
 struct MidSmall {
   static constexpr int kThreads = 128, kNB = 128, kLgNB = 7, kMaxP = kMidSmallDeg, kChunk = kMidSmallDeg;
   static constexpr int kBmWords = 0;
+  static constexpr int kUnrollHash = 2;
 };
 constexpr int kListScale = 40;      // P = rint(G * 2^40)
 constexpr int64_t kListMaxDeg = 1000000;  // |G(3 dmax)| < 32
@@ -1564,7 +1569,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
         };
         // the map kind is block-uniform: one loop per kind, no branch in the probe
         if (use_bm)
-          mid_scan<kMidUnroll, true>(
+          mid_scan<kMidUnrollBm, true>(
               a, psu, pu, lim, dv + du, lane,
               [&](int32_t key) {
                 const uint32_t word = (uint32_t)lds32(bmb + 4 * (key >> 5)), bit = 1u << (key & 31);
@@ -1572,7 +1577,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
               },
               degree, hit);
         else
-          mid_scan<kMidUnroll>(
+          mid_scan<C::kUnrollHash>(
               a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); }, degree, hit);
         rc = warp_count(rc);
         if (rc) {

@@ -1577,7 +1577,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
               },
               degree, hit);
         else
-          mid_scan<C::kUnrollHash>(
+          mid_scan<C::kUnrollHash, true>(
               a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); }, degree, hit);
         rc = warp_count(rc);
         if (rc) {

@@ -133,6 +133,16 @@ EFG_API int efg_ef_finish(efg_ctx *ctx, const int64_t *d_offsets, const int32_t 
 EFG_API int efg_topk(efg_ctx *ctx, const double *ef, int64_t n, int64_t k, int64_t *ids_out);
 EFG_API int efg_topk_device(efg_ctx *ctx, const double *d_ef, int64_t n, int64_t k, int64_t *ids_out);
 
+/* Ranking consumers of K5.
+ * efg_rank_ascending: order_out (host int64[n]) = np.argsort(ef, kind="stable"),
+ *   the ranking analysis.py:240 (immunization_experiment) cuts windows from.
+ * efg_ef_bins: analysis.py:84-103 ef_bins -- k targets equally spaced over
+ *   [min ef, max ef] (same IEEE operation order), and per target the node
+ *   nearest to it, ties to the lowest id.  Status 1 (ValueError) when k < 1 or
+ *   when there are fewer than k distinct values (message names the count). */
+EFG_API int efg_rank_ascending(efg_ctx *ctx, const double *ef, int64_t n, int64_t *order_out);
+EFG_API int efg_ef_bins(efg_ctx *ctx, const double *ef, int64_t n, int64_t k, double *target_out, int64_t *rep_out);
+
 /* Live per-kernel device timing: when enabled, every kernel launch (and each
  * CUB call) records a CUDA event pair on the launching stream; the report is
  * JSON {"kernel": [total_ms, launches], ...} accumulated since the last reset. */

@@ -4,7 +4,8 @@ Public surface mirrors efgraph/__init__.py:3-20 for the hot path: graph
 construction (Graph, RmatParams, build_graph, generate_rmat, cluster_count)
 and Expected Force (EFResult, cluster_degree, ef, ef_cluster_centric,
 ef_vertex_centric, entropy_from_histogram, write_ef_csv), plus key_nodes
-(device top-k).  The compute runs in libefg.so (sm_100a CUDA behind the C ABI
+(device top-k) and the ranking consumers of analysis.py (ef_bins,
+ef_rank_ascending, immunization_windows).  The compute runs in libefg.so (sm_100a CUDA behind the C ABI
 of include/efg.h); importing this package does not touch the GPU.
 """
 from .graph import (
@@ -29,6 +30,7 @@ from .expected_force import (
     write_ef_csv,
 )
 from .io import load_edge_list, write_edge_list
+from .ranking import EFBin, ef_bins, ef_rank_ascending, immunization_windows
 from ._native import EFGDeviceError, set_device
 
 __version__ = "0.1.0"

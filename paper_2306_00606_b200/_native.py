@@ -32,7 +32,7 @@ EXPORTED = (
     "efg_synchronize", "efg_build_graph", "efg_fetch_graph", "efg_graph_device",
     "efg_expected_force", "efg_expected_force_device", "efg_shard_bounds", "efg_ef_partial", "efg_ef_finish",
     "efg_topk",
-    "efg_topk_device", "efg_host_alloc", "efg_host_free", "efg_profile_enable", "efg_profile_reset",
+    "efg_topk_device", "efg_rank_ascending", "efg_ef_bins", "efg_host_alloc", "efg_host_free", "efg_profile_enable", "efg_profile_reset",
     "efg_profile_report", "efg_rmat_build",
 )
 
@@ -104,6 +104,8 @@ def lib():
             "efg_ef_finish": ([p, p, p, i64, i64, i64, p, p, p, p, p, p, p], ctypes.c_int),
             "efg_topk": ([p, p, i64, i64, p], ctypes.c_int),
             "efg_topk_device": ([p, p, i64, i64, p], ctypes.c_int),
+            "efg_rank_ascending": ([p, p, i64, p], ctypes.c_int),
+            "efg_ef_bins": ([p, p, i64, i64, p, p], ctypes.c_int),
             "efg_host_alloc": ([i64, P(p)], ctypes.c_int),
             "efg_host_free": ([p], ctypes.c_int),
             "efg_profile_enable": ([p, i32], ctypes.c_int),

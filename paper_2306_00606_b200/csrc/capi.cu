@@ -555,4 +555,36 @@ int efg_topk(efg_ctx* ctx, const double* ef, int64_t n, int64_t k, int64_t* ids_
   });
 }
 
+int efg_rank_ascending(efg_ctx* ctx, const double* ef, int64_t n, int64_t* order_out) {
+  if (n < 0 || (n > 0 && (!ef || !order_out))) return fail(efg::EFG_INVALID, "bad rank arguments");
+  return guarded(ctx, [&](Context& c) {
+    if (n == 0) return;
+    const double* d_ef = stage(c, "t_in", ef, n);
+    int64_t* d_order = c.buf("t_out").as<int64_t>(n);
+    efg::rank_ascending_device(c, d_ef, n, d_order);
+    EFG_CUDA_CHECK(cudaMemcpyAsync(order_out, d_order, n * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+  });
+}
+
+int efg_ef_bins(efg_ctx* ctx, const double* ef, int64_t n, int64_t k, double* target_out, int64_t* rep_out) {
+  if (k < 1) return fail(efg::EFG_INVALID, "k must be >= 1");
+  if (n < 0 || (n > 0 && !ef) || !target_out || !rep_out) return fail(efg::EFG_INVALID, "bad ef_bins arguments");
+  return guarded(ctx, [&](Context& c) {
+    int64_t distinct = 0;
+    if (n > 0) {
+      const double* d_ef = stage(c, "t_in", ef, n);
+      double* d_t = c.buf("t_bin_t").as<double>(k);
+      int64_t* d_r = c.buf("t_out").as<int64_t>(k);
+      distinct = efg::ef_bins_device(c, d_ef, n, k, d_t, d_r);
+      if (distinct >= k) {
+        EFG_CUDA_CHECK(cudaMemcpyAsync(target_out, d_t, k * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+        EFG_CUDA_CHECK(cudaMemcpyAsync(rep_out, d_r, k * sizeof(int64_t), cudaMemcpyDeviceToHost, c.stream));
+        EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+      }
+    }
+    EFG_REQUIRE(distinct >= k, "only " + std::to_string(distinct) + " distinct EF values; choose k <= that");
+  });
+}
+
 }  // extern "C"

@@ -159,5 +159,9 @@ void direct_work(Context& ctx, Prepared& P, int64_t* d_work);
 
 // topk.cu -- K5
 void topk_device(Context& ctx, const double* d_ef, int64_t n, int64_t k, int64_t* d_ids_out);
+// ranking consumers: np.argsort(ef, kind="stable") and ef_bins (analysis.py:84-103, :240)
+void rank_ascending_device(Context& ctx, const double* d_ef, int64_t n, int64_t* d_order);
+// returns the number of distinct values; outputs are written only when it is >= k
+int64_t ef_bins_device(Context& ctx, const double* d_ef, int64_t n, int64_t k, double* d_targets, int64_t* d_rep);
 
 }  // namespace efg

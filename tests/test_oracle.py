@@ -93,3 +93,23 @@ def test_seed_subset_equals_full_run(golden):
     ef, tot, fl, T, W = O.ef_seeds(off, nb, seeds=seeds, threads=3)
     assert np.array_equal(ef, case.get("ef")[seeds]) or ef_close(ef, case.get("ef")[seeds], 1e-14, 0)
     assert np.array_equal(tot, case.get("cluster_total")[seeds])
+
+
+def test_ranking_oracle_known_answers():
+    """oracle/ranking.py against the reference's own ef_bins known answers
+    (pkg/tests/test_analysis.py:61-84)."""
+    import pytest as _pytest
+    from oracle import ranking as R
+
+    bins = R.ef_bins(list(range(10)), k=10)
+    assert [b[0] for b in bins] == list(map(float, range(10)))
+    assert [b[1] for b in bins] == list(range(10))
+    assert [b[1] for b in R.ef_bins([0.0, 10.0], k=2)] == [0, 1]
+    assert R.ef_bins([0.0, 10.0, 0.0], k=2)[0][1] == 0
+    values = np.random.default_rng(3).random(50) * 7
+    lo, hi = values.min(), values.max()
+    for i, b in enumerate(R.ef_bins(values, k=10)):
+        assert b[0] == lo + i * (hi - lo) / 9
+    with _pytest.raises(ValueError, match="distinct"):
+        R.ef_bins([1.0, 1.0, 2.0], k=3)
+    assert R.rank_ascending([2.0, 1.0, 2.0, 0.5]).tolist() == [3, 1, 0, 2]

@@ -17,7 +17,7 @@ import weakref
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libefg.so")
+LIB_PATH = os.environ.get("EFG_LIB") or os.path.join(_HERE, "libefg.so")  # EFG_LIB: A/B builds
 
 MODE_CLUSTER_CENTRIC = 0
 MODE_VERTEX_CENTRIC = 1

@@ -50,16 +50,114 @@ __device__ __forceinline__ bool ranks_above(int32_t dj, int32_t j, int32_t di, i
 // [offsets[v], offsets[v] + dplus[v]) -- slot space, so no scan is needed and
 // the pass runs per row chunk while the rest of the graph is still copied.
 constexpr int kRowUnroll = 4;
+constexpr int kRowThreads = 256;
+// Rows longer than kRowBig (hubs) would be one warp's serial chain of
+// dependent loads (the top R-MAT22 hub: 965 steps, ~1 ms); with the
+// orientation they go to the first kRowBigBlocks CTAs of the same launch,
+// which walk the ranks in descending degree order, a CTA per row.
+constexpr int32_t kRowBig = 2048;
+constexpr int kRowBigBlocks = 148;
 
-__global__ void k_row_sums(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
-                           const int32_t* __restrict__ nd, int64_t r0, int64_t r1, int64_t* __restrict__ s1,
-                           int64_t* __restrict__ s2, int32_t* __restrict__ dplus, const int32_t* __restrict__ rank_of,
-                           int32_t* __restrict__ adjj, int32_t* __restrict__ adjd) {
+__device__ __forceinline__ void row_sums_big(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
+                                             const int32_t* __restrict__ nd, int64_t r0, int64_t r1,
+                                             int64_t* __restrict__ s1, int64_t* __restrict__ s2,
+                                             int32_t* __restrict__ dplus, const int32_t* __restrict__ rank_of,
+                                             int32_t* __restrict__ adjj, int32_t* __restrict__ adjd,
+                                             const int32_t* __restrict__ by_rank,
+                                             const int32_t* __restrict__ deg_by_rank, int64_t n, int32_t nbig) {
+  constexpr int T = kRowThreads, NW = T / 32, U = kRowUnroll;
+  __shared__ int wc[U * NW];
+  __shared__ int64_t ws[NW], wq[NW];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t r = blockIdx.x; r < n; r += nbig) {
+    if (deg_by_rank[r] <= kRowBig) break;  // ranks are in descending degree order
+    const int32_t v = by_rank[r];
+    if (v < r0 || v >= r1) continue;
+    const int64_t b = offsets[v], e = offsets[v + 1];
+    const int32_t dv = (int32_t)(e - b);
+    int64_t s = 0, q = 0, out = b;
+    // tiles of T*U slots; slot order (k, thread) is kept by a scan of the
+    // per-(k, warp) counts, so Adj+(v) comes out exactly as the warp path writes it
+    for (int64_t p0 = b; p0 < e; p0 += T * U) {
+      int32_t j[U], dj[U], lab[U];
+      bool take[U];
+      unsigned msk[U];
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        const int64_t p = p0 + T * k + threadIdx.x;
+        j[k] = p < e ? nbr[p] : 0;
+        dj[k] = p < e ? nd[p] : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        take[k] = false;
+        if (p0 + T * k + threadIdx.x < e) {
+          s += dj[k];
+          q += (int64_t)dj[k] * dj[k];
+          take[k] = ranks_above(dj[k], j[k], dv, v);
+        }
+        lab[k] = take[k] ? __ldg(rank_of + j[k]) : 0;
+        msk[k] = __ballot_sync(0xffffffffu, take[k]);
+        if (lane == 0) wc[k * NW + w] = __popc(msk[k]);
+      }
+      __syncthreads();
+      int64_t before[U];
+      int total = 0;
+#pragma unroll
+      for (int k = 0; k < U; ++k) {
+        for (int x = 0; x < NW; ++x) {
+          if (x == w) before[k] = total;
+          total += wc[k * NW + x];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k)
+        if (take[k]) {
+          const int64_t o = out + before[k] + __popc(msk[k] & ((1u << lane) - 1));
+          adjj[o] = lab[k];
+          adjd[o] = dj[k];
+        }
+      out += total;
+      __syncthreads();  // wc is rewritten by the next tile
+    }
+    for (int o = 16; o; o >>= 1) {
+      s += __shfl_xor_sync(0xffffffffu, s, o);
+      q += __shfl_xor_sync(0xffffffffu, q, o);
+    }
+    if (lane == 0) {
+      ws[w] = s;
+      wq[w] = q;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t ts = 0, tq = 0;
+      for (int x = 0; x < NW; ++x) {
+        ts += ws[x];
+        tq += wq[x];
+      }
+      s1[v] = ts;
+      s2[v] = tq;
+      dplus[v] = (int32_t)(out - b);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kRowThreads) k_row_sums(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd, int64_t r0,
+    int64_t r1, int64_t* __restrict__ s1, int64_t* __restrict__ s2, int32_t* __restrict__ dplus,
+    const int32_t* __restrict__ rank_of, int32_t* __restrict__ adjj, int32_t* __restrict__ adjd,
+    const int32_t* __restrict__ by_rank, const int32_t* __restrict__ deg_by_rank, int64_t n, int32_t nbig) {
+  if ((int32_t)blockIdx.x < nbig) {
+    row_sums_big(offsets, nbr, nd, r0, r1, s1, s2, dplus, rank_of, adjj, adjd, by_rank, deg_by_rank, n, nbig);
+    return;
+  }
   const int lane = threadIdx.x & 31;
-  int64_t v = r0 + ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  int64_t v = r0 + (((blockIdx.x - nbig) * (int64_t)blockDim.x + threadIdx.x) >> 5);
   if (v >= r1) return;
   int64_t b = offsets[v], e = offsets[v + 1];
   int32_t dv = (int32_t)(e - b);
+  if (nbig > 0 && dv > kRowBig) return;  // a hub: one of the first nbig CTAs has it
   int64_t s = 0, q = 0;
   int64_t out = b;
   // kRowUnroll groups of 32 per iteration: all loads of a group are in flight
@@ -309,8 +407,10 @@ void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t e0,
   const int B = 256;
   P.dplus = ctx.buf("dplus").as<int32_t>(P.g.n > 0 ? P.g.n : 1);
   EFG_LAUNCH(k_nd, ceil_div(e1 - e0, B), B, 0, s, P.g.nbr, e0, e1, P.deg, P.nd);
-  EFG_LAUNCH(k_row_sums, ceil_div((r1 - r0) * 32, B), B, 0, s, P.g.offsets, P.g.nbr, P.nd, r0, r1, P.s1, P.s2,
-             P.dplus, P.rank_of, P.rank_of ? P.adjj : nullptr, P.adjd);
+  const int32_t nbig = P.rank_of ? kRowBigBlocks : 0;  // hub CTAs need the rank order
+  EFG_LAUNCH(k_row_sums, nbig + ceil_div((r1 - r0) * 32, kRowThreads), kRowThreads, 0, s, P.g.offsets, P.g.nbr, P.nd,
+             r0, r1, P.s1, P.s2, P.dplus, P.rank_of, P.rank_of ? P.adjj : nullptr, P.adjd, P.by_rank, P.deg_by_rank,
+             P.g.n, nbig);
 }
 
 // Everything that needs all neighbours: the label-sorted orientation.

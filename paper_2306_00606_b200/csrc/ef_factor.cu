@@ -176,8 +176,11 @@ k_hist_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
 // compacted in ascending order by a block scan.  Windows are visited from
 // the smallest degree up, jumping over empty value ranges (next window = the
 // smallest degree not yet counted), so a row costs one pass per non-empty
-// window (R-MAT22 hubs: 1-8).
-constexpr int kHistWin = 16384, kHistBigThreads = 512;
+// window (R-MAT22 hubs: 1-8).  Values past the first window are mostly the
+// degrees of other hubs -- few -- so the first pass also collects them
+// (<= kHistOvf) and counts them by pairwise comparison instead of further
+// window passes over the whole row.
+constexpr int kHistWin = 16384, kHistBigThreads = 512, kHistOvf = 2048;
 __global__ void __launch_bounds__(kHistBigThreads)
 k_hist_count(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
              const int32_t* __restrict__ nd, int32_t* __restrict__ hkey, int32_t* __restrict__ hcnt,
@@ -189,7 +192,8 @@ k_hist_count(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
     typename Scan::TempStorage scan;
     typename Red::TempStorage red;
   } tmp;
-  __shared__ int32_t next_lo;
+  __shared__ int32_t next_lo, novf;
+  __shared__ int32_t ovf[kHistOvf];
   constexpr int kPer = kHistWin / kHistBigThreads;  // counters per thread in the compaction
   const int64_t q = blockIdx.x;
   if (q >= count) return;
@@ -203,14 +207,23 @@ k_hist_count(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
   if (threadIdx.x == 0) next_lo = mn;
   __syncthreads();
   int32_t lo = next_lo, base = 0;
+  bool first = true;
   while (lo != INT32_MAX) {
     for (int k = threadIdx.x; k < kHistWin; k += kHistBigThreads) wcnt[k] = 0;
+    if (threadIdx.x == 0) novf = 0;
     __syncthreads();
     int32_t nxt = INT32_MAX;  // smallest degree beyond this window
     for (int p = threadIdx.x; p < d; p += kHistBigThreads) {
       const int32_t k = nd[b + p];
-      if (k >= lo && k - lo < kHistWin) atomicAdd(&wcnt[k - lo], 1);
-      else if (k >= lo) nxt = min(nxt, k);
+      if (k >= lo && k - lo < kHistWin) {
+        atomicAdd(&wcnt[k - lo], 1);
+      } else if (k >= lo) {
+        nxt = min(nxt, k);
+        if (first) {  // values past the first window: few (hub degrees), kept for one small sort
+          const int32_t at = atomicAdd(&novf, 1);
+          if (at < kHistOvf) ovf[at] = k;
+        }
+      }
     }
     nxt = Red(tmp.red).Reduce(nxt, cub::Min());
     if (threadIdx.x == 0) next_lo = nxt;
@@ -233,6 +246,42 @@ k_hist_count(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
     base += total;
     lo = next_lo;
     __syncthreads();
+    if (first) {
+      first = false;
+      const int32_t no = novf;
+      if (no <= kHistOvf) {
+        // all values past the first window are in ovf: distinct values and
+        // their counts by pairwise comparison (no <= kHistOvf), appended in
+        // ascending order after the window's entries.  wcnt is free now.
+        for (int e = threadIdx.x; e < no; e += kHistBigThreads) {
+          const int32_t x = ovf[e];
+          int32_t c = 0;
+          bool lead = true;
+          for (int f = 0; f < no; ++f) {
+            const bool eq = ovf[f] == x;
+            c += eq;
+            lead &= !(eq && f < e);
+          }
+          wcnt[e] = lead ? c : 0;
+        }
+        __syncthreads();
+        int32_t mine = 0;
+        for (int e = threadIdx.x; e < no; e += kHistBigThreads) {
+          if (wcnt[e] == 0) continue;
+          const int32_t x = ovf[e];
+          int32_t r = 0;
+          for (int f = 0; f < no; ++f) r += wcnt[f] != 0 && ovf[f] < x;
+          hkey[b + base + r] = x;
+          hcnt[b + base + r] = wcnt[e];
+          ++mine;
+        }
+        const int32_t nd_ovf = Red(tmp.red).Sum(mine);
+        if (threadIdx.x == 0) next_lo = nd_ovf;
+        __syncthreads();
+        base += next_lo;
+        break;
+      }
+    }
   }
   if (threadIdx.x == 0) dcnt[i] = base;
 }

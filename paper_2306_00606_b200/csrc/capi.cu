@@ -59,7 +59,10 @@ Context::~Context() {
     if (e) cudaEventDestroy(e);
   for (auto& e : chunk_ev)
     if (e) cudaEventDestroy(e);
+  for (auto& e : side_ev)
+    if (e) cudaEventDestroy(e);
   if (copy_stream) cudaStreamDestroy(copy_stream);
+  if (side_stream) cudaStreamDestroy(side_stream);
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 }  // namespace efg
@@ -193,6 +196,8 @@ int efg_create(int device, efg_ctx** out) {
     for (auto& x : c.chunk_ev) EFG_CUDA_CHECK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     for (auto& x : c.aux_ev) EFG_CUDA_CHECK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
     EFG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking));
+    for (auto& x : c.side_ev) EFG_CUDA_CHECK(cudaEventCreateWithFlags(&x, cudaEventDisableTiming));
+    EFG_CUDA_CHECK(cudaStreamCreateWithFlags(&c.side_stream, cudaStreamNonBlocking));
     EFG_CUDA_CHECK(cudaDeviceGetAttribute(&c.num_sms, cudaDevAttrMultiProcessorCount, device));
   });
   if (rc) {

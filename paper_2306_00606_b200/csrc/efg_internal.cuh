@@ -59,6 +59,8 @@ struct Context {
   cudaStream_t copy_stream = nullptr;   // host->device staging of efg_expected_force inputs
   cudaEvent_t chunk_ev[9] = {};         // offsets + neighbour chunks resident (kMaxChunks + 1)
   cudaEvent_t aux_ev[2] = {};           // early cluster-total read-back: totals written / copied
+  cudaStream_t side_stream = nullptr;   // independent preparation kernels run beside the main stream
+  cudaEvent_t side_ev[2] = {};          // fork / join of side_stream
   bool total_sent = false;              // set by the engine when it queued that read-back
   Profiler prof;
   DeviceCSR csr;  // resident graph of efg_build_graph / efg_rmat_build

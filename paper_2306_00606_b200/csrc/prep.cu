@@ -426,14 +426,20 @@ void prepare_tail(Context& ctx, Prepared& P, bool need_orientation) {
     auto k_sort_small = k_sort_rows<2, 256>;
     auto k_sort_large = k_sort_rows<257, INT32_MAX>;
     const int64_t groups = ceil_div(n, 32);
+    // the few long rows (> 256 entries, a warp each for a long time) sort on
+    // the side stream while the short rows and the slot table fill the GPU
+    EFG_CUDA_CHECK(cudaEventRecord(ctx.side_ev[0], s));
+    EFG_CUDA_CHECK(cudaStreamWaitEvent(ctx.side_stream, ctx.side_ev[0], 0));
+    EFG_LAUNCH(k_sort_large, std::min<int64_t>(ceil_div(groups * 32, B), 4 * ctx.num_sms), B, 0, ctx.side_stream,
+               g.offsets, P.dplus, n, P.deg_by_rank, P.adjj, P.adjd, scratch);
+    EFG_CUDA_CHECK(cudaEventRecord(ctx.side_ev[1], ctx.side_stream));
     EFG_LAUNCH(k_sort_small, std::min<int64_t>(ceil_div(groups * 32, B), 16 * ctx.num_sms), B, 0, s, g.offsets,
-               P.dplus, n, P.deg_by_rank, P.adjj, P.adjd, scratch);
-    EFG_LAUNCH(k_sort_large, std::min<int64_t>(ceil_div(groups * 32, B), 4 * ctx.num_sms), B, 0, s, g.offsets,
                P.dplus, n, P.deg_by_rank, P.adjj, P.adjd, scratch);
   }
   P.ps = ctx.buf("ps").as<int64_t>(m2);
   P.pc = ctx.buf("pc").as<int32_t>(m2);
   EFG_LAUNCH(k_slot_plus, ceil_div(m2, B), B, 0, s, g.nbr, m2, g.offsets, P.dplus, P.ps, P.pc);
+  EFG_CUDA_CHECK(cudaStreamWaitEvent(s, ctx.side_ev[1], 0));  // join: rows sorted
 }
 
 void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P) {

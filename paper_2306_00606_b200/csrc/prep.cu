@@ -290,53 +290,74 @@ __device__ __forceinline__ void sort_row(int32_t* __restrict__ row, int32_t* __r
   }
 }
 
-// Warp per row.  Each warp scans 32 nodes at a time (interleaved over the
-// grid: long rows cluster at small ids in skewed graphs) and sorts those in
-// [PMIN, PMAX]; rows above 1024 entries (rare) rank by counting through a
-// scratch row.  Two instantiations keep the small-row kernel's registers low.
-template <int PMIN, int PMAX>
-__global__ void k_sort_rows(const int64_t* __restrict__ offsets, const int32_t* __restrict__ dplus, int64_t n,
-                            const int32_t* __restrict__ deg_by_rank,
-                            int32_t* __restrict__ adjj, int32_t* __restrict__ adjd, int32_t* __restrict__ scratch) {
+// Warp per row (register bitonic sort up to 1024 entries; longer rows, rare,
+// rank by counting through a scratch row).  Two kernels keep the short-row
+// kernel's registers low.
+// Sort one Adj+ row (pv >= 2 entries) by label.
+template <bool SMALL>
+__device__ __forceinline__ void sort_one(int64_t b, int pv, int lane, const int32_t* __restrict__ deg_by_rank,
+                                         int32_t* __restrict__ adjj, int32_t* __restrict__ adjd,
+                                         int32_t* __restrict__ scratch) {
+  int32_t* row = adjj + b;
+  int32_t* rowd = adjd + b;
+  if (SMALL) {
+    if (pv <= 32) sort_row<1>(row, rowd, pv, lane, deg_by_rank);
+    else if (pv <= 64) sort_row<2>(row, rowd, pv, lane, deg_by_rank);
+    else if (pv <= 128) sort_row<4>(row, rowd, pv, lane, deg_by_rank);
+    else sort_row<8>(row, rowd, pv, lane, deg_by_rank);
+  } else if (pv <= 512) {
+    sort_row<16>(row, rowd, pv, lane, deg_by_rank);
+  } else if (pv <= 1024) {
+    sort_row<32>(row, rowd, pv, lane, deg_by_rank);
+  } else {
+    for (int t = lane; t < pv; t += 32) {
+      const int32_t key = row[t];
+      int32_t rank = 0;
+      for (int o = 0; o < pv; ++o) rank += row[o] < key;
+      scratch[b + rank] = key;
+    }
+    __syncwarp();
+    for (int t = lane; t < pv; t += 32) {
+      row[t] = scratch[b + t];
+      rowd[t] = __ldg(deg_by_rank + row[t]);
+    }
+  }
+  __syncwarp();
+}
+
+// Rows of 2..256 entries: a warp per group of 32 nodes sorts the group's rows.
+__global__ void k_sort_small(const int64_t* __restrict__ offsets, const int32_t* __restrict__ dplus, int64_t n,
+                             const int32_t* __restrict__ deg_by_rank, int32_t* __restrict__ adjj,
+                             int32_t* __restrict__ adjd, int32_t* __restrict__ scratch) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g * 32 < n; g += nw) {
     const int64_t mine = g * 32 + lane;
     int p = 0;
     if (mine < n) p = dplus[mine];
-    unsigned todo = __ballot_sync(0xffffffffu, p >= PMIN && p <= PMAX && p >= 2);
+    unsigned todo = __ballot_sync(0xffffffffu, p >= 2 && p <= 256);
     while (todo) {
       const int x = __ffs(todo) - 1;
       todo &= todo - 1;
-      const int64_t v = g * 32 + x;
       const int pv = __shfl_sync(0xffffffffu, p, x);
-      const int64_t b = offsets[v];
-      int32_t* row = adjj + b;
-      int32_t* rowd = adjd + b;
-      if (PMAX <= 256) {
-        if (pv <= 32) sort_row<1>(row, rowd, pv, lane, deg_by_rank);
-        else if (pv <= 64) sort_row<2>(row, rowd, pv, lane, deg_by_rank);
-        else if (pv <= 128) sort_row<4>(row, rowd, pv, lane, deg_by_rank);
-        else sort_row<8>(row, rowd, pv, lane, deg_by_rank);
-      } else if (pv <= 512) {
-        sort_row<16>(row, rowd, pv, lane, deg_by_rank);
-      } else if (pv <= 1024) {
-        sort_row<32>(row, rowd, pv, lane, deg_by_rank);
-      } else {
-        for (int t = lane; t < pv; t += 32) {
-          const int32_t key = row[t];
-          int32_t rank = 0;
-          for (int o = 0; o < pv; ++o) rank += row[o] < key;
-          scratch[b + rank] = key;
-        }
-        __syncwarp();
-        for (int t = lane; t < pv; t += 32) {
-          row[t] = scratch[b + t];
-          rowd[t] = __ldg(deg_by_rank + row[t]);
-        }
-      }
-      __syncwarp();
+      sort_one<true>(offsets[g * 32 + x], pv, lane, deg_by_rank, adjj, adjd, scratch);
     }
+  }
+}
+
+// Rows of more than 256 entries belong to nodes of degree > 256: a warp per
+// node in rank (descending degree) order, so the long rows -- clustered at
+// low ids in R-MAT graphs -- spread over all warps.
+__global__ void k_sort_large(const int64_t* __restrict__ offsets, const int32_t* __restrict__ dplus, int64_t n,
+                             const int32_t* __restrict__ by_rank, const int32_t* __restrict__ deg_by_rank,
+                             int32_t* __restrict__ adjj, int32_t* __restrict__ adjd, int32_t* __restrict__ scratch) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
+    if (deg_by_rank[r] <= 256) break;
+    const int32_t v = by_rank[r];
+    const int pv = dplus[v];
+    if (pv > 256) sort_one<false>(offsets[v], pv, lane, deg_by_rank, adjj, adjd, scratch);
   }
 }
 
@@ -423,15 +444,13 @@ void prepare_tail(Context& ctx, Prepared& P, bool need_orientation) {
   {
     // rows sorted by label: a row scan for a higher-ranked v can stop at v (triangle listing)
     int32_t* scratch = ctx.buf("adjj_scratch").as<int32_t>(m2 > 0 ? m2 : 1);
-    auto k_sort_small = k_sort_rows<2, 256>;
-    auto k_sort_large = k_sort_rows<257, INT32_MAX>;
     const int64_t groups = ceil_div(n, 32);
     // the few long rows (> 256 entries, a warp each for a long time) sort on
     // the side stream while the short rows and the slot table fill the GPU
     EFG_CUDA_CHECK(cudaEventRecord(ctx.side_ev[0], s));
     EFG_CUDA_CHECK(cudaStreamWaitEvent(ctx.side_stream, ctx.side_ev[0], 0));
-    EFG_LAUNCH(k_sort_large, std::min<int64_t>(ceil_div(groups * 32, B), 4 * ctx.num_sms), B, 0, ctx.side_stream,
-               g.offsets, P.dplus, n, P.deg_by_rank, P.adjj, P.adjd, scratch);
+    EFG_LAUNCH(k_sort_large, 4 * ctx.num_sms, B, 0, ctx.side_stream, g.offsets, P.dplus, n, P.by_rank,
+               P.deg_by_rank, P.adjj, P.adjd, scratch);
     EFG_CUDA_CHECK(cudaEventRecord(ctx.side_ev[1], ctx.side_stream));
     EFG_LAUNCH(k_sort_small, std::min<int64_t>(ceil_div(groups * 32, B), 16 * ctx.num_sms), B, 0, s, g.offsets,
                P.dplus, n, P.deg_by_rank, P.adjj, P.adjd, scratch);

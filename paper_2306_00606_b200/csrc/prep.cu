@@ -160,6 +160,23 @@ __global__ void __launch_bounds__(kRowThreads) k_row_sums(
   if (nbig > 0 && dv > kRowBig) return;  // a hub: one of the first nbig CTAs has it
   int64_t s = 0, q = 0;
   int64_t out = b;
+  if (dv <= 32) {  // most rows: one group, no unrolled predicated tail
+    const bool in = lane < dv;
+    const int32_t j = in ? nbr[b + lane] : 0, dj = in ? nd[b + lane] : 0;
+    const bool take = in && ranks_above(dj, j, dv, (int32_t)v);
+    const int32_t lab = take && adjj ? __ldg(rank_of + j) : 0;
+    int32_t s32 = dj;  // dv <= 32 neighbours of degree < 2^31 each: s fits 64 bits, q per lane too
+    int64_t q64 = (int64_t)dj * dj;
+    const unsigned mask = __ballot_sync(0xffffffffu, take);
+    if (take && adjj) {
+      const int64_t o = b + __popc(mask & ((1u << lane) - 1));
+      adjj[o] = lab;
+      adjd[o] = dj;
+    }
+    s = s32;
+    q = q64;
+    out = b + __popc(mask);
+  } else {
   // kRowUnroll groups of 32 per iteration: all loads of a group are in flight
   // together (hub rows are one warp's serial chain otherwise)
   constexpr int U = kRowUnroll;
@@ -192,6 +209,7 @@ __global__ void __launch_bounds__(kRowThreads) k_row_sums(
       }
       out += __popc(mask);
     }
+  }
   }
   for (int o = 16; o; o >>= 1) {
     s += __shfl_xor_sync(0xffffffffu, s, o);

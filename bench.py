@@ -231,12 +231,12 @@ def stratified_sample(offsets, neighbors, rng_seed=0, budget=3.0e9):
     return work, picks
 
 
-def cpu_port_rate(offsets, neighbors, threads, rng_seed=0):
+def cpu_port_rate(offsets, neighbors, threads, rng_seed=0, budget=3.0e9):
     """Time the oracle port on the stratified sample; extrapolate the full-graph
     time by per-bucket work ratio.  Returns (seconds_full_graph_est, sample_desc, sample_seconds)."""
     from oracle import ef as O
 
-    work, picks = stratified_sample(offsets, neighbors, rng_seed)
+    work, picks = stratified_sample(offsets, neighbors, rng_seed, budget)
     est = 0.0
     total_sample_s = 0.0
     desc = []
@@ -265,8 +265,11 @@ def run_reference(args):
     setup_s = time.perf_counter() - t0
     threads = len(os.sched_getaffinity(0))
     times, est = [], None
+    # per-step sample work scaled so the whole K+W run stays within a few
+    # minutes (the default 20+3 steps: ~6 s of sampled CPU work each)
+    budget = 3.0e9 * min(1.0, 8.0 / max(1, args.warmup + args.steps))
     for step in range(args.warmup + args.steps):
-        t_est, sample, sample_s = cpu_port_rate(offsets, neighbors, threads, rng_seed=step)
+        t_est, sample, sample_s = cpu_port_rate(offsets, neighbors, threads, rng_seed=step, budget=budget)
         if step >= args.warmup:
             times.append(t_est)
             est = (sample, sample_s)

@@ -34,12 +34,6 @@ __global__ void k_gtab(const double* __restrict__ F, double* __restrict__ G, int
   if (S < len) G[S] = S >= 6 ? F[S - 6] - F[S - 4] : 0.0;
 }
 
-__global__ void k_nd(const int32_t* __restrict__ nbr, int64_t e0, int64_t e1, const int32_t* __restrict__ deg,
-                     int32_t* __restrict__ nd) {
-  int64_t e = e0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (e < e1) nd[e] = __ldg(deg + nbr[e]);
-}
-
 __device__ __forceinline__ bool ranks_above(int32_t dj, int32_t j, int32_t di, int32_t i) {
   return dj > di || (dj == di && j > i);
 }
@@ -59,7 +53,8 @@ constexpr int32_t kRowBig = 2048;
 constexpr int kRowBigBlocks = 148;
 
 __device__ __forceinline__ void row_sums_big(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
-                                             const int32_t* __restrict__ nd, int64_t r0, int64_t r1,
+                                             int32_t* __restrict__ nd, const int32_t* __restrict__ deg,
+                                             int64_t r0, int64_t r1,
                                              int64_t* __restrict__ s1, int64_t* __restrict__ s2,
                                              int32_t* __restrict__ dplus, const int32_t* __restrict__ rank_of,
                                              int32_t* __restrict__ adjj, int32_t* __restrict__ adjd,
@@ -86,7 +81,13 @@ __device__ __forceinline__ void row_sums_big(const int64_t* __restrict__ offsets
       for (int k = 0; k < U; ++k) {
         const int64_t p = p0 + T * k + threadIdx.x;
         j[k] = p < e ? nbr[p] : 0;
-        dj[k] = p < e ? nd[p] : 0;
+      }
+#pragma unroll
+      for (int k = 0; k < U; ++k) {  // neighbour degrees (written out as nd: k_nd fused here)
+        const int64_t p = p0 + T * k + threadIdx.x;
+        dj[k] = p < e ? __ldg(deg + j[k]) : 0;
+        lab[k] = p < e ? __ldg(rank_of + j[k]) : 0;
+        if (p < e) nd[p] = dj[k];
       }
 #pragma unroll
       for (int k = 0; k < U; ++k) {
@@ -96,7 +97,6 @@ __device__ __forceinline__ void row_sums_big(const int64_t* __restrict__ offsets
           q += (int64_t)dj[k] * dj[k];
           take[k] = ranks_above(dj[k], j[k], dv, v);
         }
-        lab[k] = take[k] ? __ldg(rank_of + j[k]) : 0;
         msk[k] = __ballot_sync(0xffffffffu, take[k]);
         if (lane == 0) wc[k * NW + w] = __popc(msk[k]);
       }
@@ -144,12 +144,12 @@ __device__ __forceinline__ void row_sums_big(const int64_t* __restrict__ offsets
 }
 
 __global__ void __launch_bounds__(kRowThreads) k_row_sums(
-    const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd, int64_t r0,
-    int64_t r1, int64_t* __restrict__ s1, int64_t* __restrict__ s2, int32_t* __restrict__ dplus,
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr, int32_t* __restrict__ nd,
+    const int32_t* __restrict__ deg, int64_t r0, int64_t r1, int64_t* __restrict__ s1, int64_t* __restrict__ s2, int32_t* __restrict__ dplus,
     const int32_t* __restrict__ rank_of, int32_t* __restrict__ adjj, int32_t* __restrict__ adjd,
     const int32_t* __restrict__ by_rank, const int32_t* __restrict__ deg_by_rank, int64_t n, int32_t nbig) {
   if ((int32_t)blockIdx.x < nbig) {
-    row_sums_big(offsets, nbr, nd, r0, r1, s1, s2, dplus, rank_of, adjj, adjd, by_rank, deg_by_rank, n, nbig);
+    row_sums_big(offsets, nbr, nd, deg, r0, r1, s1, s2, dplus, rank_of, adjj, adjd, by_rank, deg_by_rank, n, nbig);
     return;
   }
   const int lane = threadIdx.x & 31;
@@ -162,9 +162,10 @@ __global__ void __launch_bounds__(kRowThreads) k_row_sums(
   int64_t out = b;
   if (dv <= 32) {  // most rows: one group, no unrolled predicated tail
     const bool in = lane < dv;
-    const int32_t j = in ? nbr[b + lane] : 0, dj = in ? nd[b + lane] : 0;
+    const int32_t j = in ? nbr[b + lane] : 0, dj = in ? __ldg(deg + j) : 0;
+    const int32_t lab = in && adjj ? __ldg(rank_of + j) : 0;  // used only where taken
+    if (in) nd[b + lane] = dj;
     const bool take = in && ranks_above(dj, j, dv, (int32_t)v);
-    const int32_t lab = take && adjj ? __ldg(rank_of + j) : 0;
     int32_t s32 = dj;  // dv <= 32 neighbours of degree < 2^31 each: s fits 64 bits, q per lane too
     int64_t q64 = (int64_t)dj * dj;
     const unsigned mask = __ballot_sync(0xffffffffu, take);
@@ -187,7 +188,13 @@ __global__ void __launch_bounds__(kRowThreads) k_row_sums(
     for (int k = 0; k < U; ++k) {
       const int64_t p = p0 + 32 * k + lane;
       j[k] = p < e ? nbr[p] : 0;
-      dj[k] = p < e ? nd[p] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t p = p0 + 32 * k + lane;
+      dj[k] = p < e ? __ldg(deg + j[k]) : 0;
+      lab[k] = p < e && adjj ? __ldg(rank_of + j[k]) : 0;
+      if (p < e) nd[p] = dj[k];
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
@@ -197,7 +204,6 @@ __global__ void __launch_bounds__(kRowThreads) k_row_sums(
         q += (int64_t)dj[k] * dj[k];
         take[k] = ranks_above(dj[k], j[k], dv, (int32_t)v);
       }
-      lab[k] = take[k] && adjj ? __ldg(rank_of + j[k]) : 0;
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
@@ -441,14 +447,12 @@ void prepare_head(Context& ctx, const CSRView& g, bool need_orientation, Prepare
 
 // Rows [r0, r1) (slots [e0, e1)) whose neighbours are resident: neighbour
 // degrees, S1, S2 and (with the orientation) Adj+ in slot space.
-void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t e0, int64_t e1) {
+void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t, int64_t) {
   cudaStream_t s = ctx.stream;
-  const int B = 256;
   P.dplus = ctx.buf("dplus").as<int32_t>(P.g.n > 0 ? P.g.n : 1);
-  EFG_LAUNCH(k_nd, ceil_div(e1 - e0, B), B, 0, s, P.g.nbr, e0, e1, P.deg, P.nd);
   const int32_t nbig = P.rank_of ? kRowBigBlocks : 0;  // hub CTAs need the rank order
   EFG_LAUNCH(k_row_sums, nbig + ceil_div((r1 - r0) * 32, kRowThreads), kRowThreads, 0, s, P.g.offsets, P.g.nbr, P.nd,
-             r0, r1, P.s1, P.s2, P.dplus, P.rank_of, P.rank_of ? P.adjj : nullptr, P.adjd, P.by_rank, P.deg_by_rank,
+             P.deg, r0, r1, P.s1, P.s2, P.dplus, P.rank_of, P.rank_of ? P.adjj : nullptr, P.adjd, P.by_rank, P.deg_by_rank,
              P.g.n, nbig);
 }
 

@@ -47,7 +47,6 @@ struct FArgs {
   const double* F;
   const double* G;         // G[S] = F(S-6) - F(S-4): triangle correction per unit weight
   const int64_t* PT;       // P[S] = rint(G[S] 2^40): triangle sums are exact integers (any order, any path)
-  const int64_t* ps;       // [2m] start of Adj+(nbr[e]) in adjp
   const int32_t* pc;       // [2m] |Adj+(nbr[e])|
   const int32_t* adjj;     // oriented adjacency Adj+ as rank labels
   const int32_t* adjd;     // degree of each Adj+ entry
@@ -871,7 +870,7 @@ __device__ __forceinline__ void tri_rows(const FArgs& a, int64_t ob, int nrows, 
     const int64_t e = ob + x;
     const int32_t pc = __ldg(a.pc + e);
     if (pc == 0) continue;
-    tri_row(a, a.adjj + __ldg(a.ps + e), 0, pc, dv + __ldg(a.nd + e), lane, map, tri, Wt);
+    tri_row(a, a.adjj + __ldg(a.offsets + __ldg(a.nbr + e)), 0, pc, dv + __ldg(a.nd + e), lane, map, tri, Wt);
   }
 }
 
@@ -940,10 +939,11 @@ k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
   int32_t myl = -1, myd = 0, mypc = 0;
   int64_t myps = 0;
   if (lane < dv) {
-    myl = __ldg(a.rank_of + a.nbr[ob + lane]);
+    const int32_t i = a.nbr[ob + lane];
+    myl = __ldg(a.rank_of + i);
     myd = a.nd[ob + lane];
     mypc = __ldg(a.pc + ob + lane);
-    myps = __ldg(a.ps + ob + lane);
+    myps = __ldg(a.offsets + i);
   }
   __syncwarp();
   if (lane < dv) map.insert(myl, myd);
@@ -1212,7 +1212,6 @@ struct MArgs {
   const int64_t* offsets;
   const int32_t* nbr;
   const int32_t* nd;
-  const int64_t* ps;  // per slot e = (v -> u): start of Adj+(u)
   const int32_t* pc;  // per slot: |Adj+(u)|
   const int32_t* dplus;     // |Adj+(v)|: Adj+(v) at adjj[offsets[v], offsets[v] + dplus[v])
   const int32_t* adjj;
@@ -1417,7 +1416,7 @@ k_mid_warp(MArgs a) {
     du = __ldg(a.nd + ob + lane);
     up = above(du, u, dv, v);
     pu = __ldg(a.pc + ob + lane);
-    psu = __ldg(a.ps + ob + lane);
+    psu = __ldg(a.offsets + u);  // Adj+(u) starts at u's own row (slot space)
   }
   sK[w][lane] = make_int4(-1, -1, -1, -1);
   sP[w][lane] = 0;
@@ -1597,7 +1596,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
           sm.ru[k] = u;
           sm.rdu[k] = du;
           sm.rpu[k] = pu;
-          sm.rps[k] = __ldg(a.ps + e);
+          sm.rps[k] = __ldg(a.offsets + u);
         }
       }
       __syncthreads();
@@ -1955,7 +1954,6 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   a.s1 = P.s1;
   a.F = P.ftab;
   a.G = P.gtab;
-  a.ps = P.ps;
   a.pc = P.pc;
   a.adjj = P.adjj;
   a.adjd = P.adjd;
@@ -2018,7 +2016,6 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     ma.offsets = P.g.offsets;
     ma.nbr = P.g.nbr;
     ma.nd = P.nd;
-    ma.ps = P.ps;
     ma.pc = P.pc;
     ma.dplus = P.dplus;
     ma.adjj = P.adjj;

@@ -94,7 +94,6 @@ struct Prepared {
   int32_t* rank_of = nullptr;   // [n]  position in descending (degree, id) order
   int32_t* deg_by_rank = nullptr;  // [n]
   int32_t* by_rank = nullptr;   // [n]  node of each rank label
-  int64_t* ps = nullptr;        // [2m] per slot (v->i): offsets[i] (start of Adj+(i))
   int32_t* pc = nullptr;        // [2m] per slot (v->i): |Adj+(i)|
 };
 

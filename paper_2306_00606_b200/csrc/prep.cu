@@ -228,14 +228,12 @@ __global__ void __launch_bounds__(kRowThreads) k_row_sums(
   }
 }
 
-// Per adjacency slot e = (v -> i): where Adj+(i) starts and how long it is.
-__global__ void k_slot_plus(const int32_t* __restrict__ nbr, int64_t m2, const int64_t* __restrict__ offsets,
-                            const int32_t* __restrict__ dplus, int64_t* __restrict__ ps, int32_t* __restrict__ pc) {
+// Per adjacency slot e = (v -> i): how long Adj+(i) is (it starts at offsets[i]: slot space).
+__global__ void k_slot_plus(const int32_t* __restrict__ nbr, int64_t m2, const int32_t* __restrict__ dplus,
+                            int32_t* __restrict__ pc) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= m2) return;
-  const int32_t i = nbr[e];
-  ps[e] = offsets[i];
-  pc[e] = dplus[i];
+  pc[e] = dplus[nbr[e]];
 }
 
 // Rank label of each node: its position in descending (degree, id) order, so
@@ -477,9 +475,8 @@ void prepare_tail(Context& ctx, Prepared& P, bool need_orientation) {
     EFG_LAUNCH(k_sort_small, std::min<int64_t>(ceil_div(groups * 32, B), 16 * ctx.num_sms), B, 0, s, g.offsets,
                P.dplus, n, P.deg_by_rank, P.adjj, P.adjd, scratch);
   }
-  P.ps = ctx.buf("ps").as<int64_t>(m2);
   P.pc = ctx.buf("pc").as<int32_t>(m2);
-  EFG_LAUNCH(k_slot_plus, ceil_div(m2, B), B, 0, s, g.nbr, m2, g.offsets, P.dplus, P.ps, P.pc);
+  EFG_LAUNCH(k_slot_plus, ceil_div(m2, B), B, 0, s, g.nbr, m2, P.dplus, P.pc);
   EFG_CUDA_CHECK(cudaStreamWaitEvent(s, ctx.side_ev[1], 0));  // join: rows sorted
 }
 

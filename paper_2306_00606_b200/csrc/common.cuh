@@ -99,4 +99,37 @@ void prof_end(Profiler*, cudaStream_t s);
     ++::efg::g_lib_calls;                                                           \
   } while (0)
 
+// Warp bitonic sort of 32*I keys, I per lane in blocked order, ascending
+// (within-lane stages are register min/max, cross-lane stages shuffles).
+template <int I>
+__device__ __forceinline__ void warp_bitonic(uint32_t (&x)[I], int lane) {
+#pragma unroll
+  for (int k = 2; k <= 32 * I; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j < I) {
+#pragma unroll
+        for (int i = 0; i < I; ++i) {
+          const int pi = i ^ j;
+          if (pi > i) {
+            const bool up = ((lane * I + i) & k) == 0;
+            const uint32_t lo = min(x[i], x[pi]), hi = max(x[i], x[pi]);
+            x[i] = up ? lo : hi;
+            x[pi] = up ? hi : lo;
+          }
+        }
+      } else {
+        const int lj = j / I;
+        const bool lower = (lane & lj) == 0;
+#pragma unroll
+        for (int i = 0; i < I; ++i) {
+          const uint32_t y = __shfl_xor_sync(0xffffffffu, x[i], lj);
+          const bool up = ((lane * I + i) & k) == 0;
+          x[i] = (lower == up) ? min(x[i], y) : max(x[i], y);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace efg

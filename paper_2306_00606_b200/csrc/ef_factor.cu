@@ -115,6 +115,59 @@ __global__ void k_hist_warp(const int32_t* __restrict__ rows, int64_t count, con
 
 // 32 < d <= THREADS*ITEMS: CTA per row, radix sort in shared memory over the
 // bits degrees actually use (keys < 2^bits; padding = 2^bits - 1 sorts last).
+// 32 < d <= 256: warp per row, the neighbour degrees sorted in registers
+// (32x8 bitonic), run heads by comparison with the left neighbour, their
+// positions compacted by a warp scan; counts = distance to the next head.
+constexpr int kHistW8Warps = 8;
+__global__ void __launch_bounds__(kHistW8Warps * 32)
+k_hist_warp8(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
+             const int32_t* __restrict__ nd, int32_t* __restrict__ hkey, int32_t* __restrict__ hcnt,
+             int32_t* __restrict__ dcnt) {
+  __shared__ int32_t hpos[kHistW8Warps][257];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (q >= count) return;
+  const int32_t i = rows[q];
+  const int64_t b = offsets[i];
+  const int d = (int)(offsets[i + 1] - b);
+  uint32_t x[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int p = lane * 8 + u;
+    x[u] = p < d ? (uint32_t)nd[b + p] : 0xffffffffu;
+  }
+  warp_bitonic<8>(x, lane);
+  const uint32_t left = __shfl_up_sync(0xffffffffu, x[7], 1);
+  bool hd[8];
+  int nh = 0;
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int p = lane * 8 + u;
+    const uint32_t prev = u == 0 ? left : x[u > 0 ? u - 1 : 0];
+    hd[u] = p < d && (p == 0 || x[u] != prev);
+    nh += hd[u];
+  }
+  int incl = nh;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  int rank = incl - nh;
+#pragma unroll
+  for (int u = 0; u < 8; ++u)
+    if (hd[u]) {
+      hpos[w][rank] = lane * 8 + u;
+      hkey[b + rank] = (int32_t)x[u];
+      ++rank;
+    }
+  if (lane == 0) hpos[w][total] = d;
+  __syncwarp();
+  for (int r = lane; r < total; r += 32) hcnt[b + r] = hpos[w][r + 1] - hpos[w][r];
+  if (lane == 0) dcnt[i] = total;
+}
+
 constexpr int kHistThreads = 256, kHistItems = 8;
 template <int kHistThreads, int kHistItems>
 __global__ void __launch_bounds__(kHistThreads)
@@ -1833,7 +1886,8 @@ static void build_histograms(Context& ctx, const Prepared& P, const Lists& L, co
   if (small_rows) EFG_LAUNCH(k_hist_warp, ceil_div(nw * 32, B), B, 0, s, L.hw + o, nw, off, P.nd, hkey, hcnt, dcnt);
   int bits = 1;
   while (bits < 31 && (int64_t(1) << bits) <= (int64_t)P.dmax + 1) ++bits;
-  EFG_LAUNCH((k_hist_block<64, 4>), ns, 64, 0, s, L.hs + o, ns, off, P.nd, hkey, hcnt, dcnt, bits);
+  EFG_LAUNCH(k_hist_warp8, ceil_div(ns * 32, kHistW8Warps * 32), kHistW8Warps * 32, 0, s, L.hs + o, ns, off, P.nd,
+             hkey, hcnt, dcnt);
   EFG_LAUNCH((k_hist_block<kHistThreads, kHistItems>), nb, kHistThreads, 0, s, L.hb + o, nb, off, P.nd, hkey, hcnt,
              dcnt, bits);
   if (nl) {

@@ -262,37 +262,6 @@ __global__ void k_rank_scatter(const int32_t* __restrict__ by_rank, int64_t n, c
 // I per lane in blocked order (within-lane stages are register min/max,
 // cross-lane stages shuffles).  Degrees are re-gathered by label afterwards.
 template <int I>
-__device__ __forceinline__ void warp_bitonic(uint32_t (&x)[I], int lane) {
-#pragma unroll
-  for (int k = 2; k <= 32 * I; k <<= 1) {
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j < I) {
-#pragma unroll
-        for (int i = 0; i < I; ++i) {
-          const int pi = i ^ j;
-          if (pi > i) {
-            const bool up = ((lane * I + i) & k) == 0;
-            const uint32_t lo = min(x[i], x[pi]), hi = max(x[i], x[pi]);
-            x[i] = up ? lo : hi;
-            x[pi] = up ? hi : lo;
-          }
-        }
-      } else {
-        const int lj = j / I;
-        const bool lower = (lane & lj) == 0;
-#pragma unroll
-        for (int i = 0; i < I; ++i) {
-          const uint32_t y = __shfl_xor_sync(0xffffffffu, x[i], lj);
-          const bool up = ((lane * I + i) & k) == 0;
-          x[i] = (lower == up) ? min(x[i], y) : max(x[i], y);
-        }
-      }
-    }
-  }
-}
-
-template <int I>
 __device__ __forceinline__ void sort_row(int32_t* __restrict__ row, int32_t* __restrict__ rowd, int p, int lane,
                                          const int32_t* __restrict__ deg_by_rank) {
   uint32_t x[I];

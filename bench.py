@@ -266,8 +266,9 @@ def run_reference(args):
     threads = len(os.sched_getaffinity(0))
     times, est = [], None
     # per-step sample work scaled so the whole K+W run stays within a few
-    # minutes (the default 20+3 steps: ~5 s of sampled CPU work each on a
-    # 16-thread host; 8/(W+K) measured 13.6 s/step, a 5.6 min run)
+    # minutes; the default 20+3 steps measured 11.1 s of sampled CPU work each
+    # on a 16-thread host (4.8 min run; one hub seed of degree > 16384 is the
+    # floor of every step)
     budget = 3.0e9 * min(1.0, 3.0 / max(1, args.warmup + args.steps))
     for step in range(args.warmup + args.steps):
         t_est, sample, sample_s = cpu_port_rate(offsets, neighbors, threads, rng_seed=step, budget=budget)

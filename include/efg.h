@@ -150,6 +150,15 @@ EFG_API int efg_profile_enable(efg_ctx *ctx, int32_t on);
 EFG_API int efg_profile_reset(efg_ctx *ctx);
 EFG_API int efg_profile_report(efg_ctx *ctx, char *buf, int64_t cap);
 
+/* Host-side row formatter of write_ef_csv (expected_force.py:123-130): for
+ * i in [0, n) appends "<orig_ids[i]>,<ef[i] as %.9g>,<cluster_total[i]>\n"
+ * (the reference's f-string format: C's %.9g and Python's format(x, ".9g")
+ * agree -- both correctly rounded) into buf (capacity cap >= 64 n bytes),
+ * rows split over `threads` host threads; *len_out = bytes written.  No
+ * device work; loads and runs without a GPU. */
+EFG_API int efg_format_ef_csv(const int64_t *orig_ids, const double *ef, const int64_t *cluster_total, int64_t n,
+                              int32_t threads, char *buf, int64_t cap, int64_t *len_out);
+
 /* Pinned (page-locked) host memory for zero-staging copies; the Python layer
  * allocates Graph arrays and EF outputs here. */
 EFG_API int efg_host_alloc(int64_t bytes, void **out);

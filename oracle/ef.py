@@ -27,6 +27,8 @@ def _load():
         lib.efo_ef_seeds.argtypes = [ctypes.c_int64, p, p, p, ctypes.c_int64, ctypes.c_int,
                                      p, p, p, p, p]
         lib.efo_ef_seeds.restype = ctypes.c_int
+        lib.efo_ef_seed_threads.argtypes = [ctypes.c_int64, p, p, ctypes.c_int64, ctypes.c_int, p, p, p, p, p]
+        lib.efo_ef_seed_threads.restype = ctypes.c_int
         lib.efo_cluster_count.argtypes = [ctypes.c_int64, p]
         lib.efo_cluster_count.restype = ctypes.c_int64
         _lib = lib
@@ -61,6 +63,24 @@ def ef_seeds(offsets, neighbors, seeds=None, threads: int = 1):
     if rc != 0:
         raise RuntimeError(f"efo_ef_seeds failed rc={rc}")
     return ef, tot, flags, T, W
+
+
+def ef_seed_threads(offsets, neighbors, seed: int, threads: int = 8):
+    """One seed's (ef, cluster_total, flags, T, W) with its cluster walk split
+    over `threads` (exact bitmap membership; same histogram as ef_seeds)."""
+    lib = _load()
+    offsets = np.ascontiguousarray(offsets, dtype=np.int64)
+    neighbors = np.ascontiguousarray(neighbors, dtype=np.int32)
+    ef = np.zeros(1, np.float64)
+    tot = np.zeros(1, np.int64)
+    flags = np.zeros(1, np.uint8)
+    T = np.zeros(1, np.int64)
+    W = np.zeros(1, np.float64)
+    rc = lib.efo_ef_seed_threads(offsets.size - 1, _ptr(offsets), _ptr(neighbors), int(seed), int(threads),
+                                 _ptr(ef), _ptr(tot), _ptr(flags), _ptr(T), _ptr(W))
+    if rc != 0:
+        raise RuntimeError(f"efo_ef_seed_threads failed rc={rc}")
+    return float(ef[0]), int(tot[0]), int(flags[0]), int(T[0]), float(W[0])
 
 
 def cluster_count(offsets) -> int:

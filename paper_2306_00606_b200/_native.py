@@ -33,7 +33,7 @@ EXPORTED = (
     "efg_expected_force", "efg_expected_force_device", "efg_shard_bounds", "efg_ef_partial", "efg_ef_finish",
     "efg_topk",
     "efg_topk_device", "efg_rank_ascending", "efg_ef_bins", "efg_host_alloc", "efg_host_free", "efg_profile_enable", "efg_profile_reset",
-    "efg_profile_report", "efg_rmat_build",
+    "efg_profile_report", "efg_rmat_build", "efg_format_ef_csv",
 )
 
 
@@ -112,6 +112,7 @@ def lib():
             "efg_profile_reset": ([p], ctypes.c_int),
             "efg_profile_report": ([p, ctypes.c_char_p, i64], ctypes.c_int),
             "efg_rmat_build": ([p, i32, i64, p, p, p, P(i32), P(i64), P(i64)], ctypes.c_int),
+            "efg_format_ef_csv": ([p, p, p, i64, i32, p, i64, P(i64)], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
             fn = getattr(L, name)

@@ -3,8 +3,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -246,6 +248,39 @@ int efg_host_alloc(int64_t bytes, void** out) {
 int efg_host_free(void* p) {
   if (p) cudaFreeHost(p);
   return 0;
+}
+
+int efg_format_ef_csv(const int64_t* orig_ids, const double* ef, const int64_t* cluster_total, int64_t n,
+                      int32_t threads, char* buf, int64_t cap, int64_t* len_out) {
+  constexpr int64_t kRowMax = 64;  // 20 + 1 + 24 (%.9g) + 1 + 20 + 1 < 64
+  if (n < 0 || !len_out || (n > 0 && (!orig_ids || !ef || !cluster_total || !buf)) || cap < kRowMax * n)
+    return fail(efg::EFG_INVALID, "bad efg_format_ef_csv arguments (cap must be >= 64 n)");
+  try {
+    const int T = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(threads, 1), (n + 65535) / 65536));
+    std::vector<std::string> part(T);
+    auto work = [&](int t) {
+      const int64_t lo = n * t / T, hi = n * (t + 1) / T;
+      std::string& out = part[t];
+      out.resize((size_t)((hi - lo) * kRowMax));
+      char* p = &out[0];
+      for (int64_t i = lo; i < hi; ++i)
+        p += std::snprintf(p, kRowMax, "%lld,%.9g,%lld\n", (long long)orig_ids[i], ef[i], (long long)cluster_total[i]);
+      out.resize((size_t)(p - &out[0]));
+    };
+    std::vector<std::thread> pool;
+    for (int t = 1; t < T; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& th : pool) th.join();
+    int64_t len = 0;
+    for (auto& s : part) {
+      std::memcpy(buf + len, s.data(), s.size());
+      len += (int64_t)s.size();
+    }
+    *len_out = len;
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(efg::EFG_OOM, std::string("efg_format_ef_csv: ") + e.what());
+  }
 }
 
 int efg_build_graph(efg_ctx* ctx, const int64_t* edges, int64_t k, int64_t* n_out, int64_t* m_out) {

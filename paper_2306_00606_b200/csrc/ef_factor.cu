@@ -75,9 +75,10 @@ struct FArgs {
 // H_i (the histogram of the degrees of Adj(i): distinct values ascending, with
 // counts) is stored in adjacency-slot space: row i occupies hkey/hcnt
 // [offsets[i], offsets[i] + dcnt[i]) (|D_i| <= d_i), so no scan/compaction pass
-// is needed.  Rows by size class: a warp bitonic sort in registers (d <= 32),
-// a CTA radix sort in shared memory (d <= 2048), windowed counting in shared
-// memory for the few larger rows.
+// is needed.  Size classes: d <= 32 a warp per row
+// (bitonic sort, k_hist_warp), 32 < d <= 256 a warp per row (32x8 register
+// bitonic sort, k_hist_warp8), 256 < d <= 2048 a CTA per row (radix sort,
+// k_hist_block), d > 2048 windowed counting (k_hist_count).
 
 // d <= 32: warp per row, 32-lane bitonic sort of the neighbour degrees.
 __global__ void k_hist_warp(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
@@ -113,8 +114,6 @@ __global__ void k_hist_warp(const int32_t* __restrict__ rows, int64_t count, con
   if (lane == 0) dcnt[i] = __popc(heads);
 }
 
-// 32 < d <= THREADS*ITEMS: CTA per row, radix sort in shared memory over the
-// bits degrees actually use (keys < 2^bits; padding = 2^bits - 1 sorts last).
 // 32 < d <= 256: warp per row, the neighbour degrees sorted in registers
 // (32x8 bitonic), run heads by comparison with the left neighbour, their
 // positions compacted by a warp scan; counts = distance to the next head.
@@ -169,6 +168,9 @@ k_hist_warp8(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
 }
 
 constexpr int kHistThreads = 256, kHistItems = 8;
+// 256 < d <= THREADS*ITEMS (2048): CTA per row, radix sort in shared memory
+// over the bits degrees actually use (keys < 2^bits; padding = 2^bits - 1
+// sorts last).
 template <int kHistThreads, int kHistItems>
 __global__ void __launch_bounds__(kHistThreads)
 k_hist_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
@@ -681,15 +683,18 @@ k_small_rows(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
     key = runs[w][lane].x;
     cntk = runs[w][lane].y;
   }
-  // chain table: C_i(key_k) = sum_a h_a F[key_k + di - 4 + x_a] - F[2 key_k + di - 4]
+  // chain table: C_i(key_k) = sum_a h_a F[key_k + di - 4 + x_a] - F[2 key_k + di - 4].
+  // The only negative argument is an isolated edge (di = 1, key = 1: -1), whose
+  // table is exactly 0 (no chain leaves it); clamping to F[0] = 0 keeps it 0
+  // without reading before the table.
   const int64_t base = (int64_t)key + d - 4;
   double c = 0.0;
   for (int a = 0; a < D; ++a) {
     const int32_t xa = __shfl_sync(0xffffffffu, key, a);
     const int32_t ha = __shfl_sync(0xffffffffu, cntk, a);
-    if (lane < D) c += (double)ha * __ldg(F + base + xa);
+    if (lane < D) c += (double)ha * __ldg(F + max(base + xa, (int64_t)0));
   }
-  if (lane < D) c -= __ldg(F + base + key);
+  if (lane < D) c -= __ldg(F + max(base + key, (int64_t)0));
   const double hc = warp_sum(lane < D ? (double)cntk * c : 0.0);
   if (lane == 0) ca.ws[i] = hc;
   // pushes: slot e takes C of its degree's run
@@ -1544,7 +1549,7 @@ struct MidSmem {
 
 template <bool PART, class C>
 __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& tk) {
-  constexpr int kMidThreads = C::kThreads, kMidNB = C::kNB, kMidLgNB = C::kLgNB, kMidMaxP = C::kMaxP,
+  constexpr int kMidThreads = C::kThreads, kMidLgNB = C::kLgNB, kMidMaxP = C::kMaxP,
                 kMidChunk = C::kChunk;
   __shared__ MidSmem<C> sm;
   const uint32_t kb = (uint32_t)__cvta_generic_to_shared(sm.lk), vb = (uint32_t)__cvta_generic_to_shared(sm.lv);

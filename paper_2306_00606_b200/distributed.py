@@ -29,6 +29,41 @@ import numpy as np
 RECORD_BYTES = 17  # f64 ef + i64 cluster_total + u8 flags
 
 
+def _all_reduce_sum(t, group):
+    """All-reduce (sum) of a device tensor: NCCL in place; under gloo (CPU
+    tests, or ranks sharing one GPU) through a host copy."""
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl" or t.device.type == "cpu":
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+        return
+    h = t.cpu()
+    dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+    t.copy_(h)
+
+
+def ef_cluster_centric_distributed(g, group=None, T=None, W=None):
+    """Public multi-GPU entry point: host ``Graph`` in, ``EFResult`` out on every
+    rank (the ef_cluster_centric contract, expected_force.py:138-174, run as
+    one process per GPU).  Each rank copies the CSR from its host arrays to
+    its own GPU (the graph is replicated), runs its part of
+    the whole-graph pass, joins the one all-reduce, finishes every seed and
+    copies the outputs back."""
+    import torch
+
+    from . import device as D
+    from .expected_force import EFResult, _empty_result
+    from .graph import cluster_count
+
+    if g.n == 0:
+        return _empty_result()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dg = D.DeviceGraph.from_host(g, device=dev.index, non_blocking=True)
+    ef, tot, fl = ef_distributed(dg, group=group, T=T, W=W)
+    return EFResult(ef=ef.cpu().numpy(), cluster_total=tot.cpu().numpy(), flags=fl.cpu().numpy(),
+                    clusters_processed=cluster_count(g))
+
+
 def ef_distributed(dg, group=None, partial=None, finish=None, T=None, W=None):
     """EF of every seed of DeviceGraph `dg`, the whole-graph pass split over
     the ranks of `group`; returns (ef, cluster_total, flags) on every rank.
@@ -52,8 +87,8 @@ def ef_distributed(dg, group=None, partial=None, finish=None, T=None, W=None):
         partial(dg, rank, world, words, ws)
     if world > 1:
         # integer words: exact in any order; stars terms: one nonzero per node
-        dist.all_reduce(words, op=dist.ReduceOp.SUM, group=group)
-        dist.all_reduce(ws, op=dist.ReduceOp.SUM, group=group)
+        _all_reduce_sum(words, group)
+        _all_reduce_sum(ws, group)
     ef = torch.empty(n, dtype=torch.float64, device=dev)
     tot = torch.empty(n, dtype=torch.int64, device=dev)
     fl = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -128,8 +163,9 @@ def ef_sharded(dg, engine="factorized", group=None, compute=None, bounds=None):
     if dist.get_backend(group) == "nccl":
         gathered = torch.empty(world * mine.numel(), dtype=torch.uint8, device=dev)
         dist.all_gather_into_tensor(gathered, mine, group=group)  # one NCCL all-gather over NVLink
-    else:  # gloo (CPU tests): list form
-        parts = [torch.empty_like(mine) for _ in range(world)]
-        dist.all_gather(parts, mine, group=group)
-        gathered = torch.cat(parts)
+    else:  # gloo (CPU tests, ranks sharing one GPU): list form through host memory
+        mine_h = mine.cpu()
+        parts = [torch.empty_like(mine_h) for _ in range(world)]
+        dist.all_gather(parts, mine_h, group=group)
+        gathered = torch.cat(parts).to(dev)
     return unpack_all(gathered, bounds, pad_to)

@@ -172,11 +172,22 @@ def ef_vertex_centric(g, workers: int = 1, *, engine: str | None = None, device:
 def write_ef_csv(g, result: EFResult, stream) -> None:
     """``node,ef,cluster_total`` rows, original ids ascending, 9 significant digits
     (expected_force.py:123-130)."""
+    import os
+
     stream.write("node,ef,cluster_total\n")
-    orig = np.asarray(g.orig_ids).tolist()
-    efv = np.asarray(result.ef).tolist()
-    tot = np.asarray(result.cluster_total).tolist()
-    stream.write("".join(f"{o},{e:.9g},{t}\n" for o, e, t in zip(orig, efv, tot)))
+    orig = np.ascontiguousarray(g.orig_ids, dtype=np.int64)
+    efv = np.ascontiguousarray(result.ef, dtype=np.float64)
+    tot = np.ascontiguousarray(result.cluster_total, dtype=np.int64)
+    n = int(efv.size)
+    if n == 0:
+        return
+    # rows formatted by the C ABI's host formatter (%.9g == Python's format(x, ".9g"))
+    buf = np.empty(64 * n, np.uint8)
+    length = ctypes.c_int64()
+    _native.check(_native.lib().efg_format_ef_csv(
+        _native.ptr(orig), _native.ptr(efv), _native.ptr(tot), n, len(os.sched_getaffinity(0)),
+        _native.ptr(buf), buf.size, ctypes.byref(length)))
+    stream.write(buf[: length.value].tobytes().decode("ascii"))
 
 
 def key_nodes(result, k: int | None = None, frac: float | None = None, device: int | None = None) -> np.ndarray:

@@ -9,6 +9,9 @@ import pytest
 ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 GOLDEN = ROOT / "tests" / "golden"
+REF_INSTALL = ROOT / "baseline" / "_ref"  # the unmodified reference (scripts/install_reference.sh)
+if (REF_INSTALL / "efgraph").is_dir():
+    os.environ.setdefault("EFGRAPH_PATH", str(REF_INSTALL))  # the CLI hooks into the reference's CLI
 
 
 def pytest_configure(config):

@@ -1,4 +1,6 @@
-"""CLI end to end on the GPU (reference test_cli.py TestGenerate/TestEf/TestBench)."""
+"""CLI end to end on the GPU: the reference CLI with `--backend gpu` bound
+(paper_2306_00606_b200/cli.py; reference test_cli.py TestGenerate/TestEf/
+TestBench), the added `topk`, and GPU-vs-CPU backend output values."""
 import hashlib
 import json
 import math
@@ -60,3 +62,20 @@ def test_bench_and_topk(tmp_path):
     top = tmp_path / "top.csv"
     assert _run("topk", "--input", inp, "--frac", 0.05, "--output", top) == 0
     assert top.read_text().splitlines()[0] == "rank,node,ef"
+
+
+def test_gpu_backend_values_match_reference_backend(tmp_path):
+    inp = tmp_path / "g.txt"
+    assert _run("generate", "--scale", 9, "--avg-degree", 8, "--seed", 3, "--output", inp) == 0
+    outs = {}
+    for be in ("gpu", "cpu"):
+        out = tmp_path / f"{be}.csv"
+        assert main(["--backend", be, "ef", "--input", str(inp), "--output", str(out)]) == 0
+        rows = [ln.split(",") for ln in out.read_text().strip().splitlines()[1:]]
+        outs[be] = rows
+        m = json.loads((tmp_path / f"{be}.csv.manifest.json").read_text())
+        assert m["status"] == "ok" and m["graph"]["sha256"]
+    assert [r[0] for r in outs["gpu"]] == [r[0] for r in outs["cpu"]]
+    assert [r[2] for r in outs["gpu"]] == [r[2] for r in outs["cpu"]]        # cluster_total exact
+    for a, b in zip(outs["gpu"], outs["cpu"]):                                # %.9g values (ties may round apart)
+        assert float(a[1]) == pytest.approx(float(b[1]), rel=2e-9, abs=1e-12)

@@ -2,6 +2,14 @@
 
 * ER-1M, WS (n=400K) and Chung-Lu (n=2^16, W=2e4): every seed, exact
   cluster_total/flags/T, EF within 1e-9 relative;
+* WS-4M (configs[4] at its stated size): every seed, plus the top-1 % key-node
+  ranking (k = 40,000) equal to np.lexsort((ids, -ef))[:k];
+* Chung-Lu n=2^20, W=2e5 (configs[3] at its stated size, dmax ~ 1e5): a
+  uniform seed sample against the oracle and the top-10 hubs plus seeds of
+  every degree class against committed oracle fixtures;
+* R-MAT22 hubs: the top 40 hubs, every 8th remaining hub of degree > 16384
+  and seeds of every smaller class against committed oracle fixtures
+  (tests/golden/hub_fixtures.json, scripts/make_hub_fixtures.py);
 * R-MAT scale 22 (the bench graph, sha256 equal to the reference generator's):
   a uniform seed sample plus hubs of every size class against the oracle, and
   size-independent invariants over all 2.18 M seeds (mass identity, entropy
@@ -9,6 +17,8 @@
 Both engines are checked where the oracle finishes in seconds.
 """
 import hashlib
+import json
+import os
 
 import numpy as np
 import pytest
@@ -21,6 +31,36 @@ from oracle import ef as O
 
 pytestmark = pytest.mark.gpu
 RMAT22_SHA256 = "2c4b690446b61f1441357f8f4b08d437b12f7885f3375516d3c984b96c831891"
+
+
+def _fingerprint(g):
+    h = hashlib.sha256()
+    h.update(np.int64([g.n, g.m]).tobytes())
+    for a in (g.offsets, g.neighbors, g.orig_ids):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def _hub_fixtures(name):
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "hub_fixtures.json")
+    with open(path) as fh:
+        return json.load(fh)[name]
+
+
+def _check_fixture_seeds(r, rec):
+    """GPU outputs (with T) against the oracle's fixture rows: T, cluster_total,
+    flags exact; EF within 1e-9 relative."""
+    seeds = np.array([x["seed"] for x in rec["seeds"]], np.int64)
+    want_ef = np.array([float(x["ef"]) for x in rec["seeds"]])
+    want_T = np.array([int(x["T"]) for x in rec["seeds"]], np.int64)
+    want_tot = np.array([x["cluster_total"] for x in rec["seeds"]], np.int64)
+    want_fl = np.array([x["flags"] for x in rec["seeds"]], np.uint8)
+    assert np.array_equal(r.stats["T"][seeds], want_T)
+    assert np.array_equal(r.cluster_total[seeds], want_tot)
+    assert np.array_equal(r.flags[seeds], want_fl)
+    rel = np.abs(r.ef[seeds] - want_ef) / np.maximum(np.abs(want_ef), 1e-300)
+    assert ef_close(r.ef[seeds], want_ef), float(rel.max())
+    return seeds
 
 
 def _full_parity(g, engines=("factorized",), threads=16):
@@ -45,6 +85,58 @@ def test_watts_strogatz_every_seed():
     _full_parity(g, engines=("factorized", "direct"))
 
 
+def test_watts_strogatz_4m_every_seed_and_top1pct():
+    g = efg.build_graph(gen.ws_edges())                      # n=4M k=20 p=0.05
+    assert (g.n, g.m) == (4_000_000, 39_999_988)
+    ef, tot, fl, T, W = O.ef_seeds(g.offsets, g.neighbors, threads=len(os.sched_getaffinity(0)))
+    r = _run(g, 0, "factorized", None, want_tw=True)
+    assert np.array_equal(r.cluster_total, tot)
+    assert np.array_equal(r.flags, fl)
+    assert np.array_equal(r.stats["T"], T)
+    assert ef_close(r.ef, ef)
+    assert r.clusters_processed == 761_950_856
+    k = 40_000
+    top = efg.key_nodes(r, frac=0.01)
+    ids = np.arange(g.n)
+    assert top.size == k
+    assert np.array_equal(top, np.lexsort((ids, -r.ef))[:k])      # device top-k = stable ranking of our EF
+    want = np.lexsort((ids, -ef))[:k]                              # ranking of the oracle's EF
+    if not np.array_equal(top, want):  # only swaps among values equal within the EF tolerance are allowed
+        diff = np.flatnonzero(top != want)
+        assert ef_close(ef[top[diff]], ef[want[diff]]), diff[:10]
+    assert float(r.ef[top[-1]]) > float(np.sort(r.ef)[-k - 1])     # no tie across the cut
+
+
+@pytest.fixture(scope="module")
+def chunglu20():
+    g = efg.build_graph(gen.chung_lu_edges(n=1 << 20, max_weight=2e5, seed=0))
+    rec = _hub_fixtures("chunglu")
+    assert (g.n, g.m) == (rec["n"], rec["m"]) and _fingerprint(g) == rec["sha256"]
+    return g, rec
+
+
+def test_chung_lu_2e20_hubs_and_sample(chunglu20):
+    g, rec = chunglu20
+    assert int(np.diff(g.offsets).max()) == rec["dmax"] > 90_000   # the dmax ~ 1e5 regime of configs[3]
+    r = _run(g, 0, "factorized", None, want_tw=True)
+    hubs = _check_fixture_seeds(r, rec)
+    deg = np.diff(g.offsets)
+    assert int(deg[hubs].max()) == rec["dmax"]
+    rng = np.random.default_rng(1)
+    seeds = rng.choice(g.n, 3000, replace=False)
+    ef, tot, fl, T, W = O.ef_seeds(g.offsets, g.neighbors, seeds=seeds, threads=len(os.sched_getaffinity(0)))
+    assert np.array_equal(r.stats["T"][seeds], T)
+    assert np.array_equal(r.cluster_total[seeds], tot)
+    assert np.array_equal(r.flags[seeds], fl)
+    assert ef_close(r.ef[seeds], ef)
+    s1 = np.add.reduceat(deg[g.neighbors], g.offsets[:-1])
+    assert np.array_equal(r.cluster_total, deg * (deg - 1) + s1 - deg)
+    live = r.cluster_total >= 1
+    assert np.all(r.ef >= 0.0) and np.all(r.ef[live] <= np.log(r.cluster_total[live]) + 1e-12)
+    r2 = efg.ef_cluster_centric(g)
+    assert np.array_equal(r.ef, r2.ef)
+
+
 def test_chung_lu_every_seed():
     g = efg.build_graph(gen.chung_lu_edges(n=1 << 16, max_weight=2e4, seed=0))
     _full_parity(g, engines=("factorized", "direct"))
@@ -59,12 +151,8 @@ def rmat22():
 
 def test_rmat22_matches_reference_generator(rmat22):
     g = rmat22
-    h = hashlib.sha256()
-    h.update(np.int64([g.n, g.m]).tobytes())
-    for a in (g.offsets, g.neighbors, g.orig_ids):
-        h.update(np.ascontiguousarray(a).tobytes())
     assert (g.n, g.m) == (2_181_017, 44_040_192)
-    assert h.hexdigest() == RMAT22_SHA256
+    assert _fingerprint(g) == RMAT22_SHA256
 
 
 def test_rmat22_sampled_seeds_and_invariants(rmat22):
@@ -78,8 +166,8 @@ def test_rmat22_sampled_seeds_and_invariants(rmat22):
     live = r.cluster_total >= 1
     assert np.all(r.ef[live] <= np.log(r.cluster_total[live]) + 1e-12)
     assert r.clusters_processed == 127_263_919_491
-    # oracle on a sample: uniform + hubs from every degree class (the largest ones
-    # take minutes on the CPU and are covered by the engine cross-check below)
+    # oracle on a sample: uniform + seeds from every degree class (the largest
+    # hubs: test_rmat22_top_hubs_vs_oracle_fixtures)
     rng = np.random.default_rng(0)
     order = np.argsort(-deg, kind="stable")
     hubs = np.concatenate([order[40:46], order[300:304], order[2000:2004], order[9000:9004]])
@@ -92,6 +180,17 @@ def test_rmat22_sampled_seeds_and_invariants(rmat22):
     # determinism of the full pass
     r2 = efg.ef_cluster_centric(g)
     assert np.array_equal(r.ef, r2.ef)
+
+
+def test_rmat22_top_hubs_vs_oracle_fixtures(rmat22):
+    g = rmat22
+    rec = _hub_fixtures("rmat22")
+    assert rec["sha256"] == RMAT22_SHA256
+    r = _run(g, 0, "factorized", None, want_tw=True)
+    seeds = _check_fixture_seeds(r, rec)
+    deg = np.diff(g.offsets)
+    order = np.lexsort((np.arange(g.n), -deg))
+    assert set(order[:40].tolist()) <= set(seeds.tolist())           # the 40 largest hubs, incl. degree 123,453
 
 
 def test_rmat22_engines_agree_on_every_seed(rmat22):

@@ -113,3 +113,22 @@ def test_ranking_oracle_known_answers():
     with _pytest.raises(ValueError, match="distinct"):
         R.ef_bins([1.0, 1.0, 2.0], k=3)
     assert R.rank_ascending([2.0, 1.0, 2.0, 0.5]).tolist() == [3, 1, 0, 2]
+
+
+def test_threaded_single_seed_walk_equals_per_seed_walk(golden):
+    """efo_ef_seed_threads (the hub-fixture generator, scripts/make_hub_fixtures.py)
+    gives the per-seed walk's outputs bit for bit: same histogram, same order."""
+    checked = 0
+    for name, case in sorted(golden.items()):
+        off, nb = case.get("offsets"), case.get("neighbors")
+        if off is None or case.n < 3:
+            continue
+        ef, tot, fl, T, W = O.ef_seeds(off, nb)
+        deg = np.diff(off)
+        for s in {0, int(np.argmax(deg)), case.n - 1}:
+            got = O.ef_seed_threads(off, nb, s, threads=3)
+            assert got == (ef[s], tot[s], fl[s], T[s], W[s]), (name, s)
+            checked += 1
+        if checked > 120:
+            break
+    assert checked > 60

@@ -13,6 +13,9 @@
 #include "efg_internal.cuh"
 
 namespace efg {
+int check_line_factor();
+int check_line_direct();
+int check_line_prep();
 thread_local int64_t g_launches = 0;
 thread_local int64_t g_lib_calls = 0;
 thread_local Profiler* g_prof = nullptr;
@@ -92,6 +95,15 @@ int guarded(efg_ctx* ctx, F&& body) {
     if (e != cudaSuccess) return fail(efg::EFG_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
     efg::g_prof = ctx->c.prof.on ? &ctx->c.prof : nullptr;
     body(ctx->c);
+#ifdef EFG_BOUNDS_CHECK
+    {  // bounds-checked build: any device index check that failed during the call
+      EFG_CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
+      const int lf = efg::check_line_factor(), ld = efg::check_line_direct(), lp = efg::check_line_prep();
+      if (lf || ld || lp)
+        throw efg::Error(efg::EFG_CUDA, "device bounds check failed: ef_factor.cu:" + std::to_string(lf) +
+                                            " ef_direct.cu:" + std::to_string(ld) + " prep.cu:" + std::to_string(lp));
+    }
+#endif
     if (efg::g_prof && !ctx->c.prof.pending.empty()) {
       EFG_CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
       ctx->c.prof.resolve();
@@ -367,7 +379,24 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
     int32_t* d_nbr = c.buf("h_nbr").as<int32_t>(m2 > 0 ? m2 : 1);
     g.offsets = d_off;
     g.nbr = d_nbr;
-    EFG_CUDA_CHECK(cudaMemcpyAsync(d_off, offsets, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, c.copy_stream));
+    // pageable caller memory (a reference Graph's numpy arrays) goes through
+    // the pinned staging ring (stage.cu); page-locked memory is copied directly
+    const bool stage_off = efg::is_pageable(offsets), stage_nbr = efg::is_pageable(neighbors);
+    struct JoinGuard {  // never leave staging workers running past this call
+      efg::HostStager& s;
+      ~JoinGuard() {
+        for (auto& w : s.workers) w.join();
+        s.workers.clear();
+      }
+    } join_guard{c.stager};
+    c.stager.begin();
+    auto h2d = [&](void* dst, const void* src, size_t bytes, bool staged) {
+      if (staged)
+        c.stager.add(c.copy_stream, dst, src, bytes);
+      else
+        EFG_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c.copy_stream));
+    };
+    h2d(d_off, offsets, (n + 1) * sizeof(int64_t), stage_off);
     EFG_CUDA_CHECK(cudaEventRecord(c.chunk_ev[0], c.copy_stream));
     efg::Staging stg;
     // Two chunks (measured at R-MAT22: 1: 51.8, 2: 50.6, 4: 52.7, 8: 58.7 ms e2e at
@@ -387,13 +416,12 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
     }
     for (int k = 0; k < stg.nchunks; ++k) {
       const int64_t e0 = stg.slot[k], e1 = stg.slot[k + 1];
-      if (e1 > e0)
-        EFG_CUDA_CHECK(cudaMemcpyAsync(d_nbr + e0, neighbors + e0, (e1 - e0) * sizeof(int32_t), cudaMemcpyHostToDevice,
-                                       c.copy_stream));
+      if (e1 > e0) h2d(d_nbr + e0, neighbors + e0, (e1 - e0) * sizeof(int32_t), stage_nbr);
       EFG_CUDA_CHECK(cudaEventRecord(c.chunk_ev[1 + k], c.copy_stream));
       stg.ready[k] = c.chunk_ev[1 + k];
     }
     EFG_CUDA_CHECK(cudaEventRecord(ev[1], c.copy_stream));  // all inputs resident
+    c.stager.start((int)std::max(1u, std::thread::hardware_concurrency() / 2));
     EFG_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.chunk_ev[0], 0));
     double* d_ef = c.buf("o_ef").as<double>(n);
     int64_t* d_tot = c.buf("o_tot").as<int64_t>(n);
@@ -414,6 +442,7 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
     if (W_out) EFG_CUDA_CHECK(cudaMemcpyAsync(W_out, d_W, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
     EFG_CUDA_CHECK(cudaEventRecord(ev[6], c.stream));
     EFG_CUDA_CHECK(cudaEventSynchronize(ev[6]));
+    c.stager.finish();
     st->ms_h2d = elapsed(ev[0], ev[1]);
     st->ms_d2h = elapsed(ev[5], ev[6]);
     st->ms_device = elapsed(ev[0], ev[6]);

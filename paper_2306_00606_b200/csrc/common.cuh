@@ -38,6 +38,33 @@ struct Error : std::runtime_error {
     if (!(cond)) throw ::efg::Error(::efg::EFG_INVALID, (msg));                      \
   } while (0)
 
+// Bounds-checked builds (-DEFG_BOUNDS_CHECK, tools/build_variant.sh checked):
+// the compute-sanitizer is closed on the B200 pool, so the risky device
+// indices (table gathers, shared-map positions, row ranges) are checked in
+// the kernels themselves.  A failed check records its source line in a
+// per-translation-unit device word (first failure wins) and the index is
+// clamped to 0, so the kernel completes without touching memory out of
+// bounds; the C ABI turns a recorded line into a status-2 error after the
+// call (efg_check_failures).  Release builds compile the checks away.
+#ifdef EFG_BOUNDS_CHECK
+static __device__ int efg_check_line = 0;
+#define EFG_DCHECK(cond) ((cond) ? true : (atomicCAS(&efg_check_line, 0, __LINE__), false))
+#define EFG_CLAMP(idx, len) (EFG_DCHECK((int64_t)(idx) >= 0 && (int64_t)(idx) < (int64_t)(len)) ? (idx) : 0)
+// host: read and clear this translation unit's failure line
+#define EFG_CHECK_ACCESSOR(fn)                                                     \
+  int fn() {                                                                       \
+    int v = 0, z = 0;                                                              \
+    cudaMemcpyFromSymbol(&v, efg_check_line, sizeof v);                            \
+    cudaMemcpyToSymbol(efg_check_line, &z, sizeof z);                              \
+    return v;                                                                      \
+  }
+#else
+#define EFG_DCHECK(cond) true
+#define EFG_CLAMP(idx, len) (idx)
+#define EFG_CHECK_ACCESSOR(fn) \
+  int fn() { return 0; }
+#endif
+
 constexpr int kWarp = 32;
 constexpr int kNumSMs = 148;   // B200; queried at runtime as well
 

@@ -46,6 +46,7 @@ struct DArgs {
   int64_t seed_lo;
   int64_t* pT;
   double* pW;
+  int64_t flen;             // F table length (bounds-checked builds)
 };
 
 __device__ __forceinline__ uint32_t hslot(int32_t key) { return ((uint32_t)key * 2654435761u) >> 19; }
@@ -108,7 +109,7 @@ k_direct_task(DArgs a, int64_t ntasks) {
     unrank_pair(q, dv, x, y);
     int64_t d = c + a.nd[ob + x] + a.nd[ob + y];
     T += 2 * d;
-    W += 2.0 * a.F[d];
+    W += 2.0 * a.F[EFG_CLAMP(d, a.flen)];
   }
   // chains: items [max(q0, nstar), q1), warp-cooperative over 32 consecutive items
   const int64_t cs = q0 > nstar ? q0 : nstar;
@@ -139,7 +140,7 @@ k_direct_task(DArgs a, int64_t ntasks) {
       if (k < 32 && b <= r) ++k;
     }
     if (q < q1) {
-      const int64_t x = x0 + k;
+      const int64_t x = EFG_CLAMP(x0 + k, dv);
       const int32_t i = a.nbr[ob + x];
       const int64_t di = a.nd[ob + x];
       const int64_t t = r - a.cp[ob + x];
@@ -159,10 +160,10 @@ k_direct_task(DArgs a, int64_t ntasks) {
         const int64_t D = c + di + dk;
         if (tri) {
           T += (D - 2) - 2;
-          W += 2.0 * a.F[D - 2] - a.F[D];
+          W += 2.0 * a.F[EFG_CLAMP(D - 2, a.flen)] - a.F[EFG_CLAMP(D, a.flen)];
         } else {
           T += D;
-          W += a.F[D];
+          W += a.F[EFG_CLAMP(D, a.flen)];
         }
       }
     }
@@ -329,11 +330,14 @@ void ef_direct(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* tota
   EFG_LAUNCH(k_row_prefix, ceil_div(cnt * 32, B), B, 0, s, P.g.offsets, P.nd, r.lo, r.hi, cp);
   int64_t* pT = ctx.buf("d_pT").as<int64_t>(ntasks);
   double* pW = ctx.buf("d_pW").as<double>(ntasks);
-  DArgs a{P.g.offsets, P.g.nbr, P.nd, P.s1, P.ftab, cp, tstart, task_seed, hub_slot, bitmaps, words, r.lo, pT, pW};
+  DArgs a{P.g.offsets, P.g.nbr, P.nd, P.s1, P.ftab, cp, tstart, task_seed, hub_slot, bitmaps, words, r.lo, pT, pW,
+          P.ftab_len};
   EFG_LAUNCH(k_direct_task, ntasks, kThreads, 0, s, a, ntasks);
   EFG_LAUNCH(k_direct_epilogue, ceil_div(cnt, B), B, 0, s, P.g.offsets, P.s1, tstart, pT, pW, r.lo, cnt, ef, total,
              flags, T_out, W_out);
   if (st) st->terms = ntasks;
 }
+
+EFG_CHECK_ACCESSOR(check_line_direct)
 
 }  // namespace efg

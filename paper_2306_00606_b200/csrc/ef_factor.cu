@@ -47,6 +47,7 @@ struct FArgs {
   const double* F;
   const double* G;         // G[S] = F(S-6) - F(S-4): triangle correction per unit weight
   const int64_t* PT;       // P[S] = rint(G[S] 2^40): triangle sums are exact integers (any order, any path)
+  int64_t flen;            // F / G / PT table length (bounds-checked builds)
   const int32_t* pc;       // [2m] |Adj+(nbr[e])|
   const int32_t* adjj;     // oriented adjacency Adj+ as rank labels
   const int32_t* adjd;     // degree of each Adj+ entry
@@ -346,7 +347,7 @@ template <int G>
 __global__ void k_ctab_group(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
                              const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey,
                              const int32_t* __restrict__ hcnt, const int32_t* __restrict__ deg,
-                             const double* __restrict__ F, double* __restrict__ ctab) {
+                             const double* __restrict__ F, double* __restrict__ ctab, int64_t flen) {
   const int sub = threadIdx.x & (G - 1);
   int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
   if (q >= count) return;
@@ -357,8 +358,9 @@ __global__ void k_ctab_group(const int32_t* __restrict__ rows, int64_t count, co
     int32_t y = hkey[o];
     int64_t base = (int64_t)y + di - 4;
     double acc = 0.0;
-    for (int64_t a = b; a < e; ++a) acc += (double)__ldg(hcnt + a) * __ldg(F + base + __ldg(hkey + a));
-    ctab[o] = acc - __ldg(F + base + y);
+    for (int64_t a = b; a < e; ++a)
+      acc += (double)__ldg(hcnt + a) * __ldg(F + EFG_CLAMP(base + __ldg(hkey + a), flen));
+    ctab[o] = acc - __ldg(F + EFG_CLAMP(base + y, flen));
   }
 }
 
@@ -412,7 +414,7 @@ __global__ void __launch_bounds__(kCtabThreads)
 k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __restrict__ offsets,
              const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey, const int32_t* __restrict__ hcnt,
              const int32_t* __restrict__ deg, const double* __restrict__ F, double* __restrict__ ctab,
-             int exp_min, int exp_min_d) {
+             int exp_min, int exp_min_d, int64_t flen) {
   __shared__ int32_t sx[kCtabStage];
   __shared__ double sh[kCtabStage];
   __shared__ int32_t tbeg[kExpGrid], tend[kExpGrid];
@@ -568,7 +570,7 @@ k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __r
       for (int k = 0; k < kCtabOut; ++k) {
         if (k >= K) break;
         const int64_t Z = base[k] + xc;
-        const double FZ = __ldg(F + Z), t = 1.0 / (double)Z;
+        const double FZ = __ldg(F + EFG_CLAMP(Z, flen)), t = 1.0 / (double)Z;
         double poly = co[1 + kExpK];
 #pragma unroll
         for (int j = kExpK - 1; j >= 1; --j) poly = fma(poly, t, co[1 + j]);
@@ -578,7 +580,7 @@ k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __r
 #pragma unroll
     for (int k = 0; k < kCtabOut; ++k) {
       const int o = o0 + threadIdx.x + k * T;
-      if (o < D) ctab[b + o] = acc[k] - __ldg(F + base[k] + yk[k]);
+      if (o < D) ctab[b + o] = acc[k] - __ldg(F + EFG_CLAMP(base[k] + yk[k], flen));
     }
   }
 }
@@ -645,7 +647,7 @@ __global__ void __launch_bounds__(kSmallWarps * 32)
 k_small_rows(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
                              const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd,
                              const int32_t* __restrict__ deg, const double* __restrict__ F,
-                             const int64_t* __restrict__ s1, ChainAcc ca) {
+                             const int64_t* __restrict__ s1, ChainAcc ca, int64_t flen) {
   const int lane = threadIdx.x & 31;
   const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (q >= count) return;
@@ -692,9 +694,9 @@ k_small_rows(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
   for (int a = 0; a < D; ++a) {
     const int32_t xa = __shfl_sync(0xffffffffu, key, a);
     const int32_t ha = __shfl_sync(0xffffffffu, cntk, a);
-    if (lane < D) c += (double)ha * __ldg(F + max(base + xa, (int64_t)0));
+    if (lane < D) c += (double)ha * __ldg(F + EFG_CLAMP(max(base + xa, (int64_t)0), flen));
   }
-  if (lane < D) c -= __ldg(F + max(base + key, (int64_t)0));
+  if (lane < D) c -= __ldg(F + EFG_CLAMP(max(base + key, (int64_t)0), flen));
   const double hc = warp_sum(lane < D ? (double)cntk * c : 0.0);
   if (lane == 0) ca.ws[i] = hc;
   // pushes: slot e takes C of its degree's run
@@ -897,7 +899,7 @@ __device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restric
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) dj[u] = tag[u] >= 0 ? map.finish(j[u], tag[u], dd[u]) : -1;
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) g[u] = dj[u] >= 0 ? __ldg(a.PT + s0 + dj[u]) : 0;
+      for (int u = 0; u < kUnroll; ++u) g[u] = dj[u] >= 0 ? __ldg(a.PT + EFG_CLAMP(s0 + dj[u], a.flen)) : 0;
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         if (dj[u] >= 0) {
@@ -911,7 +913,7 @@ __device__ __forceinline__ void tri_row(const FArgs& a, const int32_t* __restric
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         if (dj[u] >= 0) {
-          Wt.add(__ldg(a.PT + s0 + dj[u]));
+          Wt.add(__ldg(a.PT + EFG_CLAMP(s0 + dj[u], a.flen)));
           ++tri;
         }
       }
@@ -1026,7 +1028,7 @@ k_tri_warp(const int32_t* __restrict__ seeds, int64_t count, FArgs a) {
     const int64_t psx = __shfl_sync(0xffffffffu, myps, x);
     const int32_t dx = __shfl_sync(0xffffffffu, myd, x);
     if (lane < dv && lane != x && rowhash_has(a.rowhash + 2 * psx, rowhash_lg(pcx), myl)) {
-      Wt.add(__ldg(a.PT + dv + dx + myd));
+      Wt.add(__ldg(a.PT + EFG_CLAMP(dv + dx + myd, a.flen)));
       ++tri;
     }
   }
@@ -1156,18 +1158,20 @@ __global__ void k_hub_count(const int32_t* __restrict__ hubs, const int64_t* __r
   }
 }
 
-// Triangle probes of each hub (sort key for the hub order), warp per hub.
-__global__ void k_hub_work(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ offsets,
-                           const int32_t* __restrict__ pc, int64_t* __restrict__ work) {
-  const int lane = threadIdx.x & 31;
-  for (int64_t h = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; h < nhubs;
-       h += ((int64_t)gridDim.x * blockDim.x) >> 5) {
-    const int32_t v = hubs[h];
-    int64_t w = 0;
-    for (int64_t p = offsets[v] + lane; p < offsets[v + 1]; p += 32) w += pc[p];
-    w = warp_sum(w);
-    if (lane == 0) work[h] = w;
-  }
+// Triangle probes of each hub (sort key for the hub order).
+__global__ void __launch_bounds__(256) k_hub_work(const int32_t* __restrict__ hubs, int64_t nhubs,
+                                                  const int64_t* __restrict__ offsets,
+                                                  const int32_t* __restrict__ nbr, const int32_t* __restrict__ dplus,
+                                                  int64_t* __restrict__ work) {
+  // a CTA per hub: sum of |Adj+(u)| over the hub's row (dplus gathers, L2-resident)
+  __shared__ int64_t red[8];
+  const int64_t h = blockIdx.x;
+  if (h >= nhubs) return;
+  const int32_t v = hubs[h];
+  int64_t w = 0;
+  for (int64_t p = offsets[v] + threadIdx.x; p < offsets[v + 1]; p += 256) w += __ldg(dplus + __ldg(nbr + p));
+  w = block_sum<256>(w, red);
+  if (threadIdx.x == 0) work[h] = w;
 }
 
 __global__ void k_hub_ntasks(const int32_t* __restrict__ hubs, int64_t nhubs, const int64_t* __restrict__ offsets,
@@ -1245,10 +1249,18 @@ constexpr int kMidNB = 512;         // shared map of Adj+(v): <= 1024 keys at lo
 constexpr int kMidLgNB = 9;
 constexpr int kMidMaxP = 1024;      // longer Adj+(v) are processed in parts of this size
 constexpr int kMidChunk = 256;     // rows between entry flushes: 32-bit entry words cannot overflow
-// probe-loop unroll (entries per lane per step), measured per loop: k_mid_warp 2
+// probe-loop unroll (entries per lane per step), measured per loop: bitmap scan with
+// the 8-byte word+prefix entries 4 (k_mid_big 12.05 ms vs 12.39 at 2, r02); k_mid_warp 2
 // (0.85 vs 0.95 ms at 4), bitmap 2 (12.6 vs 13.2 ms), hash 4 in big CTAs, 2 in small
 constexpr int kMidUnroll = 2;
-constexpr int kMidUnrollBm = 2;
+#ifndef EFG_MID_UNROLL_BM
+#define EFG_MID_UNROLL_BM 4
+#endif
+#ifndef EFG_MID_BIG_MINB
+#define EFG_MID_BIG_MINB 5
+#endif
+constexpr int kMidUnrollBm = EFG_MID_UNROLL_BM;
+
 constexpr int kMidSmallDeg = 256;  // middle vertices of degree <= this run in small CTAs
 
 // CTA shapes of k_mid_block: big (hub tasks and degree > kMidSmallDeg) and
@@ -1270,7 +1282,6 @@ struct MArgs {
   const int64_t* offsets;
   const int32_t* nbr;
   const int32_t* nd;
-  const int32_t* pc;  // per slot: |Adj+(u)|
   const int32_t* dplus;     // |Adj+(v)|: Adj+(v) at adjj[offsets[v], offsets[v] + dplus[v])
   const int32_t* adjj;
   const int32_t* adjd;
@@ -1278,6 +1289,7 @@ struct MArgs {
   const int32_t* by_rank;
   const int32_t* deg_by_rank;
   const int64_t* PT;        // fixed-point G
+  int64_t flen;             // PT length (bounds-checked builds)
   unsigned long long* acc;  // [4 n] per node: (hi, lo, count, pad)
   int64_t n, n32;           // labels < n32: degree > 32
   int64_t nhubs, ntasks;    // labels < nhubs come as ntasks row-range tasks
@@ -1385,7 +1397,8 @@ __device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu
       }
     }
 #pragma unroll
-    for (int k = 0; k < U; ++k) g[k] = y[k] >= 0 ? __ldg(pt + (uint32_t)d[k]) : 0;  // 32-bit index off a row base
+    for (int k = 0; k < U; ++k)
+      g[k] = y[k] >= 0 ? __ldg(pt + EFG_CLAMP((uint32_t)d[k], a.flen - s0)) : 0;  // 32-bit index off a row base
 #pragma unroll
     for (int k = 0; k < U; ++k)
       if (y[k] >= 0) hit(y[k], j[k], g[k]);
@@ -1418,6 +1431,11 @@ __device__ __forceinline__ int32_t lds32(uint32_t addr) {
   asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ int32_t lds_s16(uint32_t addr) {
   short v;
   asm("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(addr));
@@ -1426,6 +1444,42 @@ __device__ __forceinline__ int32_t lds_s16(uint32_t addr) {
 
 __device__ __forceinline__ void reds_add(uint32_t addr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+// The bitmap form of mid_scan (labels < lim <= 32 kBmWords): a running row
+// pointer and the row's G-table base stay in registers; one 8-byte shared
+// load per entry gives membership and, with a popcount, the position in
+// Adj+(v); w's degree (shared) and the G gather are predicated on the hit.
+template <int U, class Hit>
+__device__ __forceinline__ void mid_scan_bm(const int32_t* __restrict__ row, int32_t pu, int32_t lim,
+                                            const int64_t* __restrict__ PT, uint32_t s0, uint32_t bmb, uint32_t db,
+                                            int lane, Hit hit, int64_t flen = 0) {
+  const int32_t* __restrict__ rp = row + lane;
+  for (int32_t q = lane; q - lane < pu; q += 32 * U, rp += 32 * U) {
+    int32_t j[U], y[U];
+    int64_t g[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) j[k] = q + 32 * k < pu ? __ldg(rp + 32 * k) : INT32_MAX;
+    bool past = false;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const bool in = j[k] < lim;
+      past |= !in;
+      const uint32_t key = in ? (uint32_t)j[k] : 0u;
+      const uint2 wp = lds64(bmb + 8u * (key >> 5));
+      const uint32_t bit = 1u << (key & 31);
+      y[k] = (in && (wp.x & bit)) ? (int32_t)(wp.y + __popc(wp.x & (bit - 1))) : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint32_t d = (uint32_t)lds32(db + 4u * (uint32_t)max(y[k], 0));
+      g[k] = y[k] >= 0 ? __ldg(PT + EFG_CLAMP(s0 + d, flen)) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (y[k] >= 0) hit(y[k], j[k], g[k]);
+    if (__any_sync(0xffffffffu, past)) break;
+  }
 }
 
 // position of key in the shared map (keys at kb: NB = 2^lg buckets of 4; int16
@@ -1473,7 +1527,7 @@ k_mid_warp(MArgs a) {
     u = __ldg(a.nbr + ob + lane);
     du = __ldg(a.nd + ob + lane);
     up = above(du, u, dv, v);
-    pu = __ldg(a.pc + ob + lane);
+    pu = __ldg(a.dplus + u);
     psu = __ldg(a.offsets + u);  // Adj+(u) starts at u's own row (slot space)
   }
   sK[w][lane] = make_int4(-1, -1, -1, -1);
@@ -1526,18 +1580,17 @@ k_mid_warp(MArgs a) {
 // bits, count), flushed every kMidChunk rows.
 template <class C>
 struct MidSmem {
-  // Adj+(v) as a map label -> position: a bitmap over labels [0, rank(v)) with
-  // per-word prefix counts (positions are label ranks: Adj+ rows are sorted)
-  // when rank(v) is small enough, else a bucketed hash
+  // Adj+(v) as a map label -> position: a bitmap over labels [0, rank(v)),
+  // each 32-bit word stored beside the popcount of the words before it (one
+  // 8-byte shared load answers both membership and position: positions are
+  // label ranks, Adj+ rows are sorted), when rank(v) is small enough, else a
+  // bucketed hash
   union {
     struct {
       int4 lk[C::kNB];
       int16_t lv[4 * C::kNB];
     };
-    struct {
-      uint32_t bm[C::kBmWords > 0 ? C::kBmWords : 1];
-      int16_t bpre[C::kBmWords > 0 ? C::kBmWords : 1];
-    };
+    uint2 bmp[C::kBmWords > 0 ? C::kBmWords : 1];  // {bitmap word, popcount of the words before it}
   };
   int64_t rps[C::kChunk];  // compacted rows of the current chunk: Adj+(u) start,
   int32_t ru[C::kChunk], rdu[C::kChunk], rpu[C::kChunk];  // u, du, |Adj+(u)|
@@ -1589,14 +1642,14 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
     const int nbw = use_bm ? (lim + 31) >> 5 : 0;
     __syncthreads();
     if (use_bm) {
-      for (int b = threadIdx.x; b < nbw; b += blockDim.x) sm.bm[b] = 0u;
+      for (int b = threadIdx.x; b < nbw; b += blockDim.x) sm.bmp[b] = make_uint2(0u, 0u);
     } else {
       for (int b = threadIdx.x; b < (1 << lgl); b += blockDim.x) sm.lk[b] = make_int4(-1, -1, -1, -1);
     }
     __syncthreads();
     for (int t = threadIdx.x; t < np; t += blockDim.x) {
       const int32_t l = __ldg(a.adjj + pb + q0 + t);
-      if (use_bm) atomicOr(&sm.bm[l >> 5], 1u << (l & 31));
+      if (use_bm) atomicOr(&sm.bmp[l >> 5].x, 1u << (l & 31));
       else smap_insert(sm.lk, sm.lv, lgl, l, t);
       sm.node[t] = __ldg(a.by_rank + l);
       sm.edeg[t] = __ldg(a.deg_by_rank + l);
@@ -1612,7 +1665,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
 #pragma unroll
       for (int k = 0; k < per; ++k) {
         const int wi = threadIdx.x * per + k;
-        tot += wi < nbw ? __popc(sm.bm[wi]) : 0;
+        tot += wi < nbw ? __popc(sm.bmp[wi].x) : 0;
       }
       int incl = tot;
 #pragma unroll
@@ -1628,12 +1681,12 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
       for (int k = 0; k < per; ++k) {
         const int wi = threadIdx.x * per + k;
         if (wi < nbw) {
-          sm.bpre[wi] = (int16_t)base;
-          base += __popc(sm.bm[wi]);
+          sm.bmp[wi].y = (uint32_t)base;
+          base += __popc(sm.bmp[wi].x);
         }
       }
     }
-    const uint32_t bmb = (uint32_t)__cvta_generic_to_shared(sm.bm), bpb = (uint32_t)__cvta_generic_to_shared(sm.bpre);
+    const uint32_t bmb = (uint32_t)__cvta_generic_to_shared(sm.bmp);
     for (int32_t c0 = x0; c0 < x1; c0 += kMidChunk) {
       // compact the chunk's rows (lower-ranked u with |Adj+(u)| >= 2) into shared memory
       __syncthreads();
@@ -1642,7 +1695,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
       for (int32_t x = c0 + threadIdx.x; x < min(x1, c0 + kMidChunk); x += blockDim.x) {
         const int64_t e = ob + x;
         const int32_t u = __ldg(a.nbr + e), du = __ldg(a.nd + e);
-        const int32_t pu = above(du, u, dv, v) ? 0 : __ldg(a.pc + e);
+        const int32_t pu = above(du, u, dv, v) ? 0 : __ldg(a.dplus + u);
         const bool keep = pu >= 2;
         const unsigned m = __ballot_sync(__activemask(), keep);
         int base = 0;
@@ -1675,13 +1728,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
         };
         // the map kind is block-uniform: one loop per kind, no branch in the probe
         if (use_bm)
-          mid_scan<kMidUnrollBm, true>(
-              a, psu, pu, lim, dv + du, lane,
-              [&](int32_t key) {
-                const uint32_t word = (uint32_t)lds32(bmb + 4 * (key >> 5)), bit = 1u << (key & 31);
-                return word & bit ? lds_s16(bpb + 2 * (key >> 5)) + __popc(word & (bit - 1)) : -1;
-              },
-              degree, hit);
+          mid_scan_bm<kMidUnrollBm>(a.adjj + psu, pu, lim, a.PT, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
         else
           mid_scan<C::kUnrollHash, true>(
               a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); }, degree, hit);
@@ -1720,7 +1767,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
 // Launch shapes: 5 CTAs per SM for the big instantiation (<= 51 registers:
 // measured 14.6 ms against 15.6 at 63 registers / 4 CTAs), 12 for the small.
 template <bool PART>
-__global__ void __launch_bounds__(MidBig::kThreads, 5) k_mid_big(MArgs a, HubTasks tk) {
+__global__ void __launch_bounds__(MidBig::kThreads, EFG_MID_BIG_MINB) k_mid_big(MArgs a, HubTasks tk) {
   mid_block_body<PART, MidBig>(a, tk);
 }
 template <bool PART>
@@ -1976,13 +2023,13 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     // rows with d <= 32: histogram, chain table and pushes fused in registers
     const int64_t nsm = c[cslot(kHW, k)];
     EFG_LAUNCH(k_small_rows, ceil_div(nsm, kSmallWarps), kSmallWarps * 32, 0, s, L.hw + stg.row[k], nsm, g.offsets,
-               g.nbr, P.nd, P.deg, P.ftab, P.s1, ca);
+               g.nbr, P.nd, P.deg, P.ftab, P.s1, ca, P.ftab_len);
     // chain tables C_i(y): rows with 32 < d <= 64 by 8-lane groups, the rest by CTAs
     const int64_t o = stg.row[k], ng = c[cslot(kCG, k)], nb = c[cslot(kCB, k)];
     EFG_LAUNCH(k_ctab_group<8>, ceil_div(ng * 8, B), B, 0, s, L.cg + o, ng, g.offsets, dcnt, hkey, hcnt, P.deg,
-               P.ftab, ctab);
+               P.ftab, ctab, P.ftab_len);
     EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab,
-               kExpMin, kExpMinD);
+               kExpMin, kExpMinD, P.ftab_len);
     // chains pushed from the rows whose tables are now complete
     const int64_t ps1 = c[cslot(kHS, k)], pb = c[cslot(kHB, k)], pl = c[cslot(kHL, k)];
     EFG_LAUNCH(k_push_warp256, ceil_div(ps1, kPushWarps), kPushWarps * 32, 0, s, L.hs + o, ps1, g.offsets, g.nbr,
@@ -2002,7 +2049,10 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     ctx.total_sent = true;
     total = nullptr;
   }
-  prepare_tail(ctx, P, true);
+  // whole-graph passes list triangles (they gather |Adj+(u)| from dplus); the
+  // per-seed triangle path reads it per slot from the slot table
+  const bool listing = dp || (r.lo == 0 && r.hi == n && P.dmax <= kListMaxDeg);
+  prepare_tail(ctx, P, true, !listing);
   if (st) EFG_CUDA_CHECK(cudaEventRecord(ctx.ev[3], s));
   const PrepInfo info{P.dmax, P.sum_c2};
   if (cnt <= 0 && !dp) return info;
@@ -2012,6 +2062,7 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   a.nd = P.nd;
   a.s1 = P.s1;
   a.F = P.ftab;
+  a.flen = P.ftab_len;
   a.G = P.gtab;
   a.pc = P.pc;
   a.adjj = P.adjj;
@@ -2039,14 +2090,13 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   }
   // 2. triangles: listed once each for whole-graph passes, else per seed (the long kernels first)
   const int64_t nhubs = c[kHubs], ntasks = c[kNTasks];
-  const bool listing = dp || (r.lo == 0 && r.hi == n && P.dmax <= kListMaxDeg);
   // hub tasks (hubs in descending work order, kHubRows rows each) serve both triangle paths
   HubTasks tk{};
   int64_t* tstart = nullptr;
   int32_t* hs = nullptr;
   if (nhubs) {
     int64_t* hw = ctx.buf("f_hub_work").as<int64_t>(2 * nhubs + 2);
-    EFG_LAUNCH(k_hub_work, 8 * ctx.num_sms, 256, 0, s, L.hub, nhubs, g.offsets, P.pc, hw);
+    EFG_LAUNCH(k_hub_work, nhubs, 256, 0, s, L.hub, nhubs, g.offsets, g.nbr, P.dplus, hw);
     int64_t* hw_sorted = hw + nhubs;
     hs = ctx.buf("f_hub_sorted").as<int32_t>(nhubs);
     EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, hw, hw_sorted, L.hub, hs, nhubs, 0, 64, s));
@@ -2075,7 +2125,6 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     ma.offsets = P.g.offsets;
     ma.nbr = P.g.nbr;
     ma.nd = P.nd;
-    ma.pc = P.pc;
     ma.dplus = P.dplus;
     ma.adjj = P.adjj;
     ma.adjd = P.adjd;
@@ -2083,6 +2132,7 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     ma.by_rank = P.by_rank;
     ma.deg_by_rank = P.deg_by_rank;
     ma.PT = a.PT;
+    ma.flen = P.ftab_len;
     ma.acc = acc;
     ma.n = n;
     ma.n32 = c[kTr1] + c[kTr2] + c[kTr3] + c[kHubs];  // whole-graph pass: nodes of degree > 32
@@ -2189,5 +2239,7 @@ void ef_finish(Context& ctx, const CSRView& g, SeedRange r, const unsigned long 
   EFG_LAUNCH(k_list_out, ceil_div(cnt, B), B, 0, s, words + 3 * n, a, cnt);
   EFG_LAUNCH(k_epilogue, ceil_div(cnt, B), B, 0, s, a, cnt, ef, total, flags, T_out, W_out);
 }
+
+EFG_CHECK_ACCESSOR(check_line_factor)
 
 }  // namespace efg

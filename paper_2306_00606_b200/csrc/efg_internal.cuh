@@ -1,8 +1,11 @@
 // Internal (C++) interfaces between the efg translation units.
 #pragma once
+#include <condition_variable>
+#include <deque>
 #include <map>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -39,6 +42,42 @@ struct Profiler {
   ~Profiler();
 };
 
+// Pageable host -> device copies through a ring of pinned buffers filled by
+// host worker threads (stage.cu).  add() enqueues a range's pieces on a
+// stream (gate callback + copy + event each); start() launches the workers;
+// finish() joins them (call once every gate has been enqueued).
+struct HostStager {
+  static constexpr size_t kPiece = size_t(8) << 20;
+  static constexpr int kRing = 16;
+  struct Piece {
+    const char* src;
+    char* dst;
+    size_t bytes;
+  };
+  struct Gate {
+    HostStager* owner;
+    int64_t idx;
+  };
+  std::vector<char*> bufs;        // kRing pinned buffers of kPiece bytes
+  std::vector<cudaEvent_t> ev;    // per piece: its device copy done
+  std::vector<Piece> pieces;
+  std::deque<Gate> gates;         // stable addresses (callback arguments)
+  std::deque<uint8_t> ready;      // guarded by mu
+  std::mutex mu;
+  std::condition_variable cv;
+  std::vector<std::thread> workers;
+  bool failed = false;
+  void begin();
+  void add(cudaStream_t s, void* dst, const void* src, size_t bytes);
+  void start(int threads);
+  void finish();
+  ~HostStager();
+
+ private:
+  void ensure(size_t npieces);
+};
+bool is_pageable(const void* p);
+
 struct Context {
   int device = 0;
   int num_sms = kNumSMs;
@@ -63,6 +102,7 @@ struct Context {
   cudaEvent_t side_ev[2] = {};          // fork / join of side_stream
   bool total_sent = false;              // set by the engine when it queued that read-back
   Profiler prof;
+  HostStager stager;  // pageable inputs of efg_expected_force
   DeviceCSR csr;  // resident graph of efg_build_graph / efg_rmat_build
   DevBuf& buf(const std::string& name) { return bufs[name]; }
   ~Context();
@@ -112,7 +152,9 @@ void rmat_build_device(Context& ctx, int scale, int64_t avg_degree, const double
 void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P);
 void prepare_head(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P);
 void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t e0, int64_t e1);
-void prepare_tail(Context& ctx, Prepared& P, bool need_orientation);
+// need_slot_table: the per-slot |Adj+(i)| table P.pc (K2 work, per-seed
+// triangle paths); whole-graph listing passes gather it from dplus instead
+void prepare_tail(Context& ctx, Prepared& P, bool need_orientation, bool need_slot_table);
 
 // Host inputs arriving on a copy stream in row chunks (efg_expected_force):
 // work on the rows of chunk k may start once ready[k] has fired (null event:

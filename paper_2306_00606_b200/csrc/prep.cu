@@ -113,7 +113,7 @@ __device__ __forceinline__ void row_sums_big(const int64_t* __restrict__ offsets
 #pragma unroll
       for (int k = 0; k < U; ++k)
         if (take[k]) {
-          const int64_t o = out + before[k] + __popc(msk[k] & ((1u << lane) - 1));
+          const int64_t o = EFG_CLAMP(out + before[k] + __popc(msk[k] & ((1u << lane) - 1)), e);
           adjj[o] = lab[k];
           adjd[o] = dj[k];
         }
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kRowThreads) k_row_sums(
     for (int k = 0; k < U; ++k) {
       const unsigned mask = __ballot_sync(0xffffffffu, take[k]);
       if (take[k] && adjj) {
-        const int64_t o = out + __popc(mask & ((1u << lane) - 1));
+        const int64_t o = EFG_CLAMP(out + __popc(mask & ((1u << lane) - 1)), e);
         adjj[o] = lab[k];
         adjd[o] = dj[k];
       }
@@ -424,7 +424,7 @@ void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t, in
 }
 
 // Everything that needs all neighbours: the label-sorted orientation.
-void prepare_tail(Context& ctx, Prepared& P, bool need_orientation) {
+void prepare_tail(Context& ctx, Prepared& P, bool need_orientation, bool need_slot_table) {
   if (!need_orientation) return;
   cudaStream_t s = ctx.stream;
   const int B = 256;
@@ -444,15 +444,19 @@ void prepare_tail(Context& ctx, Prepared& P, bool need_orientation) {
     EFG_LAUNCH(k_sort_small, std::min<int64_t>(ceil_div(groups * 32, B), 16 * ctx.num_sms), B, 0, s, g.offsets,
                P.dplus, n, P.deg_by_rank, P.adjj, P.adjd, scratch);
   }
-  P.pc = ctx.buf("pc").as<int32_t>(m2);
-  EFG_LAUNCH(k_slot_plus, ceil_div(m2, B), B, 0, s, g.nbr, m2, P.dplus, P.pc);
+  if (need_slot_table) {
+    P.pc = ctx.buf("pc").as<int32_t>(m2);
+    EFG_LAUNCH(k_slot_plus, ceil_div(m2, B), B, 0, s, g.nbr, m2, P.dplus, P.pc);
+  }
   EFG_CUDA_CHECK(cudaStreamWaitEvent(s, ctx.side_ev[1], 0));  // join: rows sorted
 }
 
 void prepare(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P) {
   prepare_head(ctx, g, need_orientation, P);
   prepare_rows(ctx, P, 0, g.n, 0, g.m2);
-  prepare_tail(ctx, P, need_orientation);
+  prepare_tail(ctx, P, need_orientation, true);
 }
+
+EFG_CHECK_ACCESSOR(check_line_prep)
 
 }  // namespace efg

@@ -567,10 +567,18 @@ def main():
     ctx.profile_reset()
     ctx.profile(True)
     torch.cuda.synchronize()
-    if distributed:
+    if distributed:  # this rank's rows phase, the row exchange, its listing phase (the timed step's kernels)
+        from paper_2306_00606_b200.distributed import exchange_rows
         words = torch.empty(D.DIST_WORDS * n, dtype=torch.int64, device=dev)
         ws = torch.empty(n, dtype=torch.float64, device=dev)
-        st = D.ef_partial(dg, rank, world, words, ws, stats=True)
+        adjp = torch.empty(2 * m, dtype=torch.int32, device=dev)
+        dplus = torch.empty(n, dtype=torch.int32, device=dev)
+        pb = D.part_bounds(dg, world)
+        st = D.ef_partial_rows(dg, rank, world, pb, adjp, dplus, words, ws, stats=True)
+        exchange_rows(adjp, dplus, dg.offsets[torch.as_tensor(pb, device=dev)].cpu().numpy(), pb)
+        st2 = D.ef_partial_tables(dg, rank, world, pb, words, ws, stats=True)
+        st3 = D.ef_partial_list(dg, rank, world, pb, adjp, dplus, words, ws, stats=True)
+        st["launches"] += st2["launches"] + st3["launches"]
     else:
         lo, hi = int(bounds[rank]), int(bounds[rank + 1])
         pe = torch.empty(hi - lo, dtype=torch.float64, device=dev)
@@ -579,8 +587,8 @@ def main():
         st = D.ef_range(dg, lo, hi, pe, pt, pf, engine=args.engine, stats=True)
     ctx.profile(False)
     kernels = ctx.profile_report()
-    if distributed:  # the finish kernels of the step (k_list_out, k_epilogue), outside the part's stats call
-        n_launch_finish = 2
+    if distributed:  # the finish kernels of the step (head + k_list_out, k_epilogue), outside the parts' stats calls
+        n_launch_finish = 9
     else:
         n_launch_finish = 0
 
@@ -687,7 +695,8 @@ def main():
         "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f64+int64", "data": "synthetic",
         "config": {"workload": CONFIGS[args.config], "n": n, "m": m, "engine": args.engine,
-                   "parallelism": (f"whole-graph pass in {world} parts + 1 all-reduce ({backend})" if distributed
+                   "parallelism": (f"whole-graph pass in {world} parts: rows per part, Adj+ row exchange "
+                                   f"({world} broadcasts), listing per part, 1 all-reduce ({backend})" if distributed
                                    else f"seed-sharded x{world}"),
                    "l2": "flushed between timed steps (256 MB write)",
                    "graph_sha256_matches_reference": sha_ok},

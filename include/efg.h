@@ -110,19 +110,48 @@ EFG_API int efg_expected_force_device(efg_ctx *ctx, const int64_t *d_offsets, co
 EFG_API int efg_shard_bounds(efg_ctx *ctx, const int64_t *d_offsets, const int32_t *d_neighbors, int64_t n,
                      int32_t engine, int32_t parts, int64_t *bounds_out);
 
-/* Distributed whole-graph pass (factorized engine, one part per device):
- * efg_ef_partial computes part `part` of `nparts` -- the chain tables and
- * pushes of the nodes v % nparts == part and the triangles listed by every
- * nparts-th work unit -- into d_words (uint64[EFG_DIST_WORDS * n], exact
- * integer sums) and d_ws (f64[n], nonzero only at the part's nodes).  The
+/* Distributed whole-graph pass (factorized engine, one part per device; no
+ * reference counterpart -- it replaces the reference's thread-pool merge,
+ * expected_force.py:158-172).  Part p owns the contiguous
+ * node range [bounds[p], bounds[p+1]) of efg_part_bounds (balanced by row
+ * work; identical on every rank): its rows' neighbour degrees, S1/S2,
+ * label-sorted Adj+ rows, chain tables and pushes.  The triangle listing is
+ * split by work unit (every nparts-th).  Every part writes EFG_DIST_WORDS
+ * uint64 words per node (d_words[EFG_DIST_WORDS * n]: exact integer sums, own
+ * rows / own units only) and f64 stars terms (d_ws[n], own rows only); the
  * caller sums both over all parts (one all-reduce: integer addition and
- * disjoint supports, so the sum is exact and order-free), then
- * efg_ef_finish turns the sums into the outputs of seeds [seed_lo, seed_hi).
- * The result equals efg_expected_force_device bitwise.  No reference
- * counterpart. */
-#define EFG_DIST_WORDS 7
+ * disjoint supports, so exact and order-free), then efg_ef_finish produces
+ * the outputs of seeds [seed_lo, seed_hi).  Bitwise equal to
+ * efg_expected_force_device for any nparts.
+ *
+ * Row-partitioned form (per-rank work ~ 1/nparts of the whole pass), three
+ * calls on one context:
+ *   efg_ef_partial_rows -- the part's rows: neighbour degrees, S1/S2, its
+ *     label-sorted Adj+ rows into the caller's slot-space buffer d_adjp[2m]
+ *     (row v at [offsets[v], offsets[v] + dplus[v])) and |Adj+(v)| into
+ *     d_dplus[n]; clears the words;
+ *   (caller: every part broadcasts its slot range [offsets[bounds[p]],
+ *    offsets[bounds[p+1]]) of d_adjp and node range of d_dplus, so that every
+ *    rank holds all rows -- asynchronously, while the next call runs)
+ *   efg_ef_partial_tables -- the part's histograms, chain tables and pushes;
+ *   efg_ef_partial_list -- the part's listing units on the exchanged rows.
+ * The tables and listing calls add into the words the rows call cleared.
+ * Self-contained form: efg_ef_partial runs both with every row's orientation
+ * prepared locally (no exchange; more work per rank). */
+#define EFG_DIST_WORDS 9
+EFG_API int efg_part_bounds(efg_ctx *ctx, const int64_t *d_offsets, const int32_t *d_neighbors, int64_t n,
+                            int32_t nparts, int64_t *bounds_out);
 EFG_API int efg_ef_partial(efg_ctx *ctx, const int64_t *d_offsets, const int32_t *d_neighbors, int64_t n,
                            int32_t part, int32_t nparts, uint64_t *d_words, double *d_ws, efg_stats *stats);
+EFG_API int efg_ef_partial_rows(efg_ctx *ctx, const int64_t *d_offsets, const int32_t *d_neighbors, int64_t n,
+                                int32_t part, int32_t nparts, const int64_t *bounds, int32_t *d_adjp,
+                                int32_t *d_dplus, uint64_t *d_words, double *d_ws, efg_stats *stats);
+EFG_API int efg_ef_partial_tables(efg_ctx *ctx, const int64_t *d_offsets, const int32_t *d_neighbors, int64_t n,
+                                  int32_t part, int32_t nparts, const int64_t *bounds, uint64_t *d_words,
+                                  double *d_ws, efg_stats *stats);
+EFG_API int efg_ef_partial_list(efg_ctx *ctx, const int64_t *d_offsets, const int32_t *d_neighbors, int64_t n,
+                                int32_t part, int32_t nparts, const int64_t *bounds, int32_t *d_adjp,
+                                int32_t *d_dplus, uint64_t *d_words, double *d_ws, efg_stats *stats);
 EFG_API int efg_ef_finish(efg_ctx *ctx, const int64_t *d_offsets, const int32_t *d_neighbors, int64_t n,
                           int64_t seed_lo, int64_t seed_hi, const uint64_t *d_words, const double *d_ws,
                           double *d_ef, int64_t *d_cluster_total, uint8_t *d_flags, int64_t *d_T, double *d_W);

@@ -30,7 +30,9 @@ ENGINES = {"auto": ENGINE_AUTO, "factorized": ENGINE_FACTORIZED, "direct": ENGIN
 EXPORTED = (
     "efg_abi_version", "efg_last_error", "efg_create", "efg_destroy", "efg_set_stream",
     "efg_synchronize", "efg_build_graph", "efg_fetch_graph", "efg_graph_device",
-    "efg_expected_force", "efg_expected_force_device", "efg_shard_bounds", "efg_ef_partial", "efg_ef_finish",
+    "efg_expected_force", "efg_expected_force_device", "efg_shard_bounds", "efg_part_bounds", "efg_ef_partial", "efg_ef_partial_rows", "efg_ef_partial_tables",
+    "efg_ef_partial_list",
+    "efg_ef_finish",
     "efg_topk",
     "efg_topk_device", "efg_rank_ascending", "efg_ef_bins", "efg_host_alloc", "efg_host_free", "efg_profile_enable", "efg_profile_reset",
     "efg_profile_report", "efg_rmat_build", "efg_format_ef_csv",
@@ -100,7 +102,11 @@ def lib():
             "efg_expected_force": ([p, p, p, i64, i32, i32, p, p, p, P(i64), p, p, P(Stats)], ctypes.c_int),
             "efg_expected_force_device": ([p, p, p, i64, i64, i64, i32, p, p, p, p, p, P(Stats)], ctypes.c_int),
             "efg_shard_bounds": ([p, p, p, i64, i32, i32, p], ctypes.c_int),
+            "efg_part_bounds": ([p, p, p, i64, i32, p], ctypes.c_int),
             "efg_ef_partial": ([p, p, p, i64, i32, i32, p, p, P(Stats)], ctypes.c_int),
+            "efg_ef_partial_rows": ([p, p, p, i64, i32, i32, p, p, p, p, p, P(Stats)], ctypes.c_int),
+            "efg_ef_partial_tables": ([p, p, p, i64, i32, i32, p, p, p, P(Stats)], ctypes.c_int),
+            "efg_ef_partial_list": ([p, p, p, i64, i32, i32, p, p, p, p, p, P(Stats)], ctypes.c_int),
             "efg_ef_finish": ([p, p, p, i64, i64, i64, p, p, p, p, p, p, p], ctypes.c_int),
             "efg_topk": ([p, p, i64, i64, p], ctypes.c_int),
             "efg_topk_device": ([p, p, i64, i64, p], ctypes.c_int),

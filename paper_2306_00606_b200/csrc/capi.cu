@@ -485,10 +485,21 @@ int efg_expected_force_device(efg_ctx* ctx, const int64_t* d_offsets, const int3
   });
 }
 
-int efg_ef_partial(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n, int32_t part,
-                   int32_t nparts, uint64_t* d_words, double* d_ws, efg_stats* stats) {
+namespace {
+// One distributed part: validate, view the graph, run ef_factorized in `mode`.
+int run_part(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n, int32_t part,
+             int32_t nparts, const int64_t* bounds, int mode, int32_t* d_adjp, int32_t* d_dplus, uint64_t* d_words,
+             double* d_ws, efg_stats* stats) {
   if (n < 0 || nparts < 1 || part < 0 || part >= nparts) return fail(efg::EFG_INVALID, "bad part");
   if (n > 0 && (!d_words || !d_ws)) return fail(efg::EFG_INVALID, "null output array");
+  if (mode != efg::kDistRepl && n > 0 && !bounds) return fail(efg::EFG_INVALID, "row-partitioned part needs bounds");
+  if ((mode == efg::kDistRows || mode == efg::kDistList) && n > 0 && (!d_adjp || !d_dplus))
+    return fail(efg::EFG_INVALID, "rows / listing parts need d_adjp and d_dplus");
+  if (bounds) {
+    if (bounds[0] != 0 || bounds[nparts] != n) return fail(efg::EFG_INVALID, "bounds must run from 0 to n");
+    for (int p = 0; p < nparts; ++p)
+      if (bounds[p + 1] < bounds[p]) return fail(efg::EFG_INVALID, "bounds must be non-decreasing");
+  }
   static_assert(EFG_DIST_WORDS == efg::kDistWords, "word count");
   return guarded(ctx, [&](Context& c) {
     efg::g_launches = 0;
@@ -497,16 +508,24 @@ int efg_ef_partial(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neig
     int64_t off_n = 0;
     EFG_CUDA_CHECK(cudaMemcpyAsync(&off_n, d_offsets + n, sizeof off_n, cudaMemcpyDeviceToHost, c.stream));
     EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
-    efg::CSRView g;
-    g.n = n;
-    g.m2 = off_n;
-    g.offsets = d_offsets;
-    g.nbr = d_neighbors;
+    efg::CSRView g{n, off_n, d_offsets, d_neighbors};
     efg::DistPart dp;
     dp.part = part;
     dp.nparts = nparts;
+    dp.mode = mode;
+    if (bounds) {
+      dp.node_lo = bounds[part];
+      dp.node_hi = bounds[part + 1];
+    } else {
+      std::vector<int64_t> b(nparts + 1);
+      efg::part_bounds(c, g, nparts, b.data());
+      dp.node_lo = b[part];
+      dp.node_hi = b[part + 1];
+    }
     dp.words = reinterpret_cast<unsigned long long*>(d_words);
     dp.ws = d_ws;
+    dp.adjp = d_adjp;
+    dp.dplus = d_dplus;
     if (stats) EFG_CUDA_CHECK(cudaEventRecord(c.ev[0], c.stream));
     efg::ef_factorized(c, g, resident(g), efg::SeedRange{0, n}, nullptr, nullptr, nullptr, nullptr, nullptr, stats,
                        &dp);
@@ -518,6 +537,49 @@ int efg_ef_partial(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neig
       stats->engine = EFG_ENGINE_FACTORIZED;
     }
   });
+}
+}  // namespace
+
+int efg_part_bounds(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n, int32_t nparts,
+                    int64_t* bounds_out) {
+  if (n < 0 || nparts < 1 || !bounds_out) return fail(efg::EFG_INVALID, "bad part-bounds arguments");
+  return guarded(ctx, [&](Context& c) {
+    bounds_out[0] = 0;
+    for (int p = 1; p <= nparts; ++p) bounds_out[p] = n;
+    if (n == 0) return;
+    int64_t off_n = 0;
+    EFG_CUDA_CHECK(cudaMemcpyAsync(&off_n, d_offsets + n, sizeof off_n, cudaMemcpyDeviceToHost, c.stream));
+    EFG_CUDA_CHECK(cudaStreamSynchronize(c.stream));
+    efg::CSRView g{n, off_n, d_offsets, d_neighbors};
+    efg::part_bounds(c, g, nparts, bounds_out);
+  });
+}
+
+int efg_ef_partial(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n, int32_t part,
+                   int32_t nparts, uint64_t* d_words, double* d_ws, efg_stats* stats) {
+  return run_part(ctx, d_offsets, d_neighbors, n, part, nparts, nullptr, efg::kDistRepl, nullptr, nullptr, d_words,
+                  d_ws, stats);
+}
+
+int efg_ef_partial_rows(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n, int32_t part,
+                        int32_t nparts, const int64_t* bounds, int32_t* d_adjp, int32_t* d_dplus, uint64_t* d_words,
+                        double* d_ws, efg_stats* stats) {
+  return run_part(ctx, d_offsets, d_neighbors, n, part, nparts, bounds, efg::kDistRows, d_adjp, d_dplus, d_words,
+                  d_ws, stats);
+}
+
+int efg_ef_partial_tables(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n,
+                          int32_t part, int32_t nparts, const int64_t* bounds, uint64_t* d_words, double* d_ws,
+                          efg_stats* stats) {
+  return run_part(ctx, d_offsets, d_neighbors, n, part, nparts, bounds, efg::kDistTables, nullptr, nullptr, d_words,
+                  d_ws, stats);
+}
+
+int efg_ef_partial_list(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n, int32_t part,
+                        int32_t nparts, const int64_t* bounds, int32_t* d_adjp, int32_t* d_dplus, uint64_t* d_words,
+                        double* d_ws, efg_stats* stats) {
+  return run_part(ctx, d_offsets, d_neighbors, n, part, nparts, bounds, efg::kDistList, d_adjp, d_dplus, d_words,
+                  d_ws, stats);
 }
 
 int efg_ef_finish(efg_ctx* ctx, const int64_t* d_offsets, const int32_t* d_neighbors, int64_t n, int64_t seed_lo,

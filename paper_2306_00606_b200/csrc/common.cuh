@@ -107,9 +107,11 @@ extern thread_local Profiler* g_prof;
 void prof_begin(Profiler*, const char* name, cudaStream_t s);
 void prof_end(Profiler*, cudaStream_t s);
 
+inline int64_t grid_count(int64_t g) { return g; }
+inline int64_t grid_count(dim3 g) { return (int64_t)g.x * g.y * g.z; }
 #define EFG_LAUNCH(kernel, grid, block, smem, stream, ...)                         \
   do {                                                                              \
-    if ((grid) > 0) {                                                               \
+    if (::efg::grid_count(grid) > 0) {                                              \
       if (::efg::g_prof) ::efg::prof_begin(::efg::g_prof, #kernel, (stream));       \
       kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                   \
       EFG_CUDA_CHECK(cudaGetLastError());                                           \

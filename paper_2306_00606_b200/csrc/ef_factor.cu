@@ -711,7 +711,7 @@ k_small_rows(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
 // located through a direct-mapped shared table (key -> position; only keys
 // present are ever read, so it needs no clearing), larger ones by binary
 // search over H_i's keys (shared memory, global beyond kPushKeys).
-constexpr int kPushThreads = 128, kPushKeys = 4096, kPushDirect = 4096;
+constexpr int kPushThreads = 128, kPushKeys = 4096, kPushDirect = 4096, kPushSlices = 16;
 __global__ void __launch_bounds__(kPushThreads)
 k_push_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
              const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd, const int32_t* __restrict__ dcnt,
@@ -727,18 +727,21 @@ k_push_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
   const int d = (int)(offsets[i + 1] - b);
   const int D = dcnt[i];
   const int32_t* keys = D <= kPushKeys ? sk : hkey + b;
+  // the row's slots in gridDim.y slices (long hub rows spread over CTAs);
+  // slice 0 also forms the stars term
+  const int p0 = (int)((int64_t)d * blockIdx.y / gridDim.y), p1 = (int)((int64_t)d * (blockIdx.y + 1) / gridDim.y);
   double hc = 0.0;
   for (int k = threadIdx.x; k < D; k += kPushThreads) {
     const int32_t kk = hkey[b + k];
     if (D <= kPushKeys) sk[k] = kk;
     if (kk < kPushDirect && k < 32768) pos[kk] = (int16_t)k;
-    hc += (double)hcnt[b + k] * ctab[b + k];
+    if (blockIdx.y == 0) hc += (double)hcnt[b + k] * ctab[b + k];
   }
   hc = block_sum<kPushThreads>(hc, red);  // syncs: the tables are complete afterwards
-  if (threadIdx.x == 0) ca.ws[i] = hc;
+  if (threadIdx.x == 0 && blockIdx.y == 0) ca.ws[i] = hc;
   __syncthreads();
   const int64_t s1i = s1[i];
-  for (int p = threadIdx.x; p < d; p += kPushThreads) {
+  for (int p = p0 + threadIdx.x; p < p1; p += kPushThreads) {
     const int32_t y = nd[b + p];
     int lo;
     if (y < kPushDirect && D <= 32768) {
@@ -1158,6 +1161,36 @@ __global__ void k_hub_count(const int32_t* __restrict__ hubs, const int64_t* __r
   }
 }
 
+// Class counts of a listing pass from the rank order (labels are in
+// descending degree order, so "degree > T" is a label prefix): the triangle
+// classes' sizes and the hub task count, straight into the count slots.
+__device__ __forceinline__ int64_t ranks_above_deg(const int32_t* __restrict__ deg_by_rank, int64_t n, int32_t t) {
+  int64_t lo = 0, hi = n;  // first rank of degree <= t
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (deg_by_rank[mid] > t) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+__global__ void k_list_counts(const int32_t* __restrict__ deg_by_rank, int64_t n, int64_t* __restrict__ c,
+                              int slot_s, int slot_1, int slot_2, int slot_3, int slot_hub, int slot_tasks) {
+  __shared__ int64_t red[8];
+  const int64_t g32 = ranks_above_deg(deg_by_rank, n, 32), g256 = ranks_above_deg(deg_by_rank, n, 256),
+                g1024 = ranks_above_deg(deg_by_rank, n, 1024), ghub = ranks_above_deg(deg_by_rank, n, kHashMaxDeg);
+  int64_t t = 0;
+  for (int64_t r = threadIdx.x; r < ghub; r += blockDim.x) t += ceil_div(deg_by_rank[r], kHubRows);
+  t = block_sum<256>(t, red);
+  if (threadIdx.x == 0) {
+    c[slot_s] = n - g32;
+    c[slot_1] = g32 - g256;
+    c[slot_2] = g256 - g1024;
+    c[slot_3] = g1024 - ghub;
+    c[slot_hub] = ghub;
+    c[slot_tasks] = t;
+  }
+}
+
 // Triangle probes of each hub (sort key for the hub order).
 __global__ void __launch_bounds__(256) k_hub_work(const int32_t* __restrict__ hubs, int64_t nhubs,
                                                   const int64_t* __restrict__ offsets,
@@ -1281,7 +1314,8 @@ constexpr int64_t kListMaxDeg = 1000000;  // |G(3 dmax)| < 32
 struct MArgs {
   const int64_t* offsets;
   const int32_t* nbr;
-  const int32_t* nd;
+  const int32_t* nd;        // degree per slot, or null: gathered from deg (distributed listing: other parts' rows)
+  const int32_t* deg;
   const int32_t* dplus;     // |Adj+(v)|: Adj+(v) at adjj[offsets[v], offsets[v] + dplus[v])
   const int32_t* adjj;
   const int32_t* adjd;
@@ -1525,7 +1559,7 @@ k_mid_warp(MArgs a) {
   bool up = false;
   if (lane < dv) {
     u = __ldg(a.nbr + ob + lane);
-    du = __ldg(a.nd + ob + lane);
+    du = a.nd ? __ldg(a.nd + ob + lane) : __ldg(a.deg + u);
     up = above(du, u, dv, v);
     pu = __ldg(a.dplus + u);
     psu = __ldg(a.offsets + u);  // Adj+(u) starts at u's own row (slot space)
@@ -1694,7 +1728,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
       __syncthreads();
       for (int32_t x = c0 + threadIdx.x; x < min(x1, c0 + kMidChunk); x += blockDim.x) {
         const int64_t e = ob + x;
-        const int32_t u = __ldg(a.nbr + e), du = __ldg(a.nd + e);
+        const int32_t u = __ldg(a.nbr + e), du = a.nd ? __ldg(a.nd + e) : __ldg(a.deg + u);
         const int32_t pu = above(du, u, dv, v) ? 0 : __ldg(a.dplus + u);
         const bool keep = pu >= 2;
         const unsigned m = __ballot_sync(__activemask(), keep);
@@ -1831,10 +1865,9 @@ __global__ void k_mass(const int64_t* __restrict__ offsets, const int64_t* __res
 struct DegRange {
   const int64_t* offsets;
   int64_t lo, hi;           // lo < dv <= hi
-  int32_t nparts = 1, part = 0;  // and v % nparts == part
   __host__ __device__ bool operator()(const int32_t& v) const {
     int64_t d = offsets[v + 1] - offsets[v];
-    return d > lo && d <= hi && v % nparts == part;
+    return d > lo && d <= hi;
   }
 };
 
@@ -1866,7 +1899,66 @@ __global__ void k_seed_work(const int64_t* __restrict__ offsets, const int32_t* 
   }
 }
 
+// The part's S1 / S2 into its words (nodes [lo, hi); zeros elsewhere).
+__global__ void k_part_s12(const int64_t* __restrict__ s1, const int64_t* __restrict__ s2, int64_t lo, int64_t hi,
+                           unsigned long long* __restrict__ w1, unsigned long long* __restrict__ w2) {
+  const int64_t v = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= hi) return;
+  w1[v] = (unsigned long long)s1[v];
+  w2[v] = (unsigned long long)s2[v];
+}
+
+// Row work of the distributed pass per node, in units of a quarter adjacency
+// slot: a per-row cost (launch share, histogram, small-row table), the slots
+// (neighbour degrees, orientation, sort, pushes) and the chain table (~ |D_i|^2,
+// |D_i| <= d, capped where the far-field expansion takes over).  Weights fitted
+// to measured per-part times on R-MAT22 (tools/dist_estimate.py, N = 4 and 8:
+// per row 0.73 ns, per slot 0.072 ns, per capped d^2 5.1e-5 ns).
+__global__ void k_part_weight(const int64_t* __restrict__ offsets, int64_t n, int64_t* __restrict__ w) {
+  const int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  const int64_t d = offsets[v + 1] - offsets[v], dc = d < 1024 ? d : 1024;
+  w[v] = 40 + 4 * d + dc * dc / 350;
+}
+
+// bounds[p] = first node whose inclusive work prefix reaches p * total / nparts
+__global__ void k_part_search(const int64_t* __restrict__ prefix, int64_t n, int32_t nparts,
+                              int64_t* __restrict__ bounds) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > nparts) return;
+  if (p == 0 || p == nparts) {
+    bounds[p] = p == 0 ? 0 : n;
+    return;
+  }
+  const long double target = (long double)prefix[n - 1] * p / nparts;
+  int64_t lo = 0, hi = n;  // first v with prefix[v] >= target, cut after it
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((long double)prefix[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  bounds[p] = lo + 1 < n ? lo + 1 : n;
+}
+
 }  // namespace
+
+void part_bounds(Context& ctx, const CSRView& g, int32_t nparts, int64_t* bounds) {
+  cudaStream_t s = ctx.stream;
+  const int64_t n = g.n;
+  const int B = 256;
+  int64_t* w = ctx.buf("pb_w").as<int64_t>(2 * n + nparts + 1);
+  int64_t* pre = w + n;
+  int64_t* db = w + 2 * n;
+  EFG_LAUNCH(k_part_weight, ceil_div(n, B), B, 0, s, g.offsets, n, w);
+  size_t tmp = 0;
+  EFG_CUDA_CHECK(cub::DeviceScan::InclusiveSum(nullptr, tmp, w, pre, n, s));
+  EFG_REGION("cub::DeviceScan::InclusiveSum", s,
+             EFG_CUDA_CHECK(cub::DeviceScan::InclusiveSum(ctx.buf("cub").get(tmp), tmp, w, pre, n, s)));
+  EFG_LAUNCH(k_part_search, 1, 64 * ceil_div(nparts + 1, 64), 0, s, pre, n, nparts, db);
+  EFG_CUDA_CHECK(cudaMemcpyAsync(bounds, db, (nparts + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  EFG_CUDA_CHECK(cudaStreamSynchronize(s));
+  for (int p = 1; p <= nparts; ++p) bounds[p] = std::max(bounds[p], bounds[p - 1]);
+}
 
 // Segment bounds of listed rows (CUB segmented sort over non-contiguous rows).
 
@@ -1888,12 +1980,15 @@ constexpr int64_t kHistWarpMax = 32, kHistBlockMax = kHistThreads * kHistItems, 
 // Node-class lists.  Histogram and chain-table classes are selected per row
 // chunk (chunk k's part of list X starts at X + row[k]), so their kernels can
 // run on a chunk as soon as its neighbours are resident.
+// row_lists: the per-chunk histogram / chain-table classes; tri_lists (with
+// seeds): the triangle classes and the hub list.
 static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, SeedRange r, int64_t* cdev, bool seeds,
-                        int32_t nparts = 1, int32_t part = 0) {
+                        bool row_lists = true, bool tri_lists = true) {
   const int64_t n = P.g.n, cnt = r.hi - r.lo;
   auto list = [&](const char* name, int64_t len) { return ctx.buf(name).as<int32_t>(len > 0 ? len : 1); };
   const int64_t* off = P.g.offsets;
   Lists L{};
+  if (row_lists) {
   L.hw = list("f_l_hw", n);
   L.hs = list("f_l_hs", n);
   L.hb = list("f_l_hb", n);
@@ -1905,15 +2000,16 @@ static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, See
   for (int k = 0; k < stg.nchunks; ++k) {
     const SeedRange ch{stg.row[k], stg.row[k + 1]};
     const int64_t o = stg.row[k];
-    select_seeds(ctx, ch, DegRange{off, -1, kHistWarpMax, nparts, part}, L.hw + o, cdev + cslot(kHW, k));
-    select_seeds(ctx, ch, DegRange{off, kHistWarpMax, 256, nparts, part}, L.hs + o, cdev + cslot(kHS, k));
-    select_seeds(ctx, ch, DegRange{off, 256, kHistBlockMax, nparts, part}, L.hb + o, cdev + cslot(kHB, k));
-    select_seeds(ctx, ch, DegRange{off, kHistBlockMax, INT64_MAX, nparts, part}, L.hl + o, cdev + cslot(kHL, k));
+    select_seeds(ctx, ch, DegRange{off, -1, kHistWarpMax}, L.hw + o, cdev + cslot(kHW, k));
+    select_seeds(ctx, ch, DegRange{off, kHistWarpMax, 256}, L.hs + o, cdev + cslot(kHS, k));
+    select_seeds(ctx, ch, DegRange{off, 256, kHistBlockMax}, L.hb + o, cdev + cslot(kHB, k));
+    select_seeds(ctx, ch, DegRange{off, kHistBlockMax, INT64_MAX}, L.hl + o, cdev + cslot(kHL, k));
     if (!seeds) continue;
-    select_seeds(ctx, ch, DegRange{off, kHistWarpMax, kCtabGroupMax, nparts, part}, L.cg + o, cdev + cslot(kCG, k));
-    select_seeds(ctx, ch, DegRange{off, kCtabGroupMax, INT64_MAX, nparts, part}, L.cb + o, cdev + cslot(kCB, k));
+    select_seeds(ctx, ch, DegRange{off, kHistWarpMax, kCtabGroupMax}, L.cg + o, cdev + cslot(kCG, k));
+    select_seeds(ctx, ch, DegRange{off, kCtabGroupMax, INT64_MAX}, L.cb + o, cdev + cslot(kCB, k));
   }
-  if (!seeds) return L;
+  }
+  if (!seeds || !tri_lists) return L;
   L.trs = list("f_l_trs", cnt);
   L.tr1 = list("f_l_tr1", cnt);
   L.tr2 = list("f_l_tr2", cnt);
@@ -1986,73 +2082,127 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   const int64_t cnt = r.hi - r.lo;
   Prepared P;
   if (st) EFG_CUDA_CHECK(cudaEventRecord(ctx.ev[2], s));
-  prepare_head(ctx, g, true, P);
+  const int dmode = dp ? dp->mode : -1;
+  auto& dh = ctx.dist_head;
+  if ((dmode == kDistList || dmode == kDistTables) && dh.valid && dh.P.g.offsets == g.offsets && dh.P.g.nbr == g.nbr && dh.P.g.n == n &&
+      dh.P.g.m2 == g.m2) {
+    P = dh.P;  // the rows part's degrees, tables and rank labels on this graph are still resident
+  } else {
+    prepare_head(ctx, g, true, P);
+  }
+  // distributed parts work on their node range, as one resident chunk
+  Staging own;
+  if (dp) {
+    own.nchunks = 1;
+    own.row[0] = dp->node_lo;
+    own.row[1] = dp->node_hi;
+    if (dmode != kDistRepl) {  // the caller's (exchanged) Adj+ rows and |Adj+|
+      P.adjj = dp->adjp;
+      P.dplus = dp->dplus;
+    }
+  }
+  const Staging& rows = dp ? own : stg;
   // ---- phase 1: class lists and counts on the device, one read-back
   int64_t* cdev = ctx.buf("f_counts").as<int64_t>(kNCounts);
   EFG_CUDA_CHECK(cudaMemsetAsync(cdev, 0, kNCounts * sizeof(int64_t), s));
-  Lists L = make_lists(ctx, P, stg, r, cdev, true, dp ? dp->nparts : 1, dp ? dp->part : 0);
-  if (dp) {
-    EFG_REQUIRE(P.dmax <= kListMaxDeg, "distributed pass: maximum degree above the listing bound");
-    EFG_CUDA_CHECK(cudaMemsetAsync(dp->words, 0, kDistWords * n * sizeof(unsigned long long), s));
-    EFG_CUDA_CHECK(cudaMemsetAsync(dp->ws, 0, n * sizeof(double), s));
-  }
-  EFG_LAUNCH(k_hub_count, 2 * ctx.num_sms, 256, 0, s, L.hub, cdev + kHubs, g.offsets,
-             reinterpret_cast<unsigned long long*>(cdev + kNTasks));
-  int64_t c[kNCounts];
-  read_counts(ctx, cdev, c);
-  // ---- phase 2: no further host synchronisation; per row chunk as it arrives
-  int32_t* hkey = ctx.buf("f_hkey").as<int32_t>(m2);
-  int32_t* hcnt = ctx.buf("f_hcnt").as<int32_t>(m2);
-  int32_t* dcnt = ctx.buf("f_dcnt").as<int32_t>(n);
-  double* ctab = ctx.buf("f_ctab").as<double>(m2);
-  ChainAcc ca;
-  {
-    unsigned long long* acc = dp ? dp->words : ctx.buf("f_chain_acc").as<unsigned long long>(3 * n);
-    if (!dp) EFG_CUDA_CHECK(cudaMemsetAsync(acc, 0, 3 * n * sizeof(unsigned long long), s));
-    ca.wh = acc;
-    ca.wl = acc + n;
-    ca.p2 = acc + 2 * n;
-    ca.ws = dp ? dp->ws : ctx.buf("f_chain_ws").as<double>(n);
-    const double d3 = 3.0 * (P.dmax > 1 ? P.dmax : 1);
-    ca.c0 = (P.dmax > 1 ? P.dmax : 1) * d3 * log(d3);
-  }
-  for (int k = 0; k < stg.nchunks; ++k) {
-    if (stg.ready[k]) EFG_CUDA_CHECK(cudaStreamWaitEvent(s, stg.ready[k], 0));
-    prepare_rows(ctx, P, stg.row[k], stg.row[k + 1], stg.slot[k], stg.slot[k + 1]);
-    build_histograms(ctx, P, L, c, stg, k, hkey, hcnt, dcnt, false);
-    // rows with d <= 32: histogram, chain table and pushes fused in registers
-    const int64_t nsm = c[cslot(kHW, k)];
-    EFG_LAUNCH(k_small_rows, ceil_div(nsm, kSmallWarps), kSmallWarps * 32, 0, s, L.hw + stg.row[k], nsm, g.offsets,
-               g.nbr, P.nd, P.deg, P.ftab, P.s1, ca, P.ftab_len);
-    // chain tables C_i(y): rows with 32 < d <= 64 by 8-lane groups, the rest by CTAs
-    const int64_t o = stg.row[k], ng = c[cslot(kCG, k)], nb = c[cslot(kCB, k)];
-    EFG_LAUNCH(k_ctab_group<8>, ceil_div(ng * 8, B), B, 0, s, L.cg + o, ng, g.offsets, dcnt, hkey, hcnt, P.deg,
-               P.ftab, ctab, P.ftab_len);
-    EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab, ctab,
-               kExpMin, kExpMinD, P.ftab_len);
-    // chains pushed from the rows whose tables are now complete
-    const int64_t ps1 = c[cslot(kHS, k)], pb = c[cslot(kHB, k)], pl = c[cslot(kHL, k)];
-    EFG_LAUNCH(k_push_warp256, ceil_div(ps1, kPushWarps), kPushWarps * 32, 0, s, L.hs + o, ps1, g.offsets, g.nbr,
-               P.nd, dcnt, hkey, hcnt, ctab, P.s1, ca);
-    EFG_LAUNCH(k_push_block, pb, kPushThreads, 0, s, L.hb + o, pb, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,
-               P.s1, ca);
-    EFG_LAUNCH(k_push_block, pl, kPushThreads, 0, s, L.hl + o, pl, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,
-               P.s1, ca);
-  }
-  if (stg.total_host && !dp && r.lo == 0 && r.hi == n && n > 0) {
-    // S1 is complete: cluster totals now, their read-back overlaps the listing
-    EFG_LAUNCH(k_mass, ceil_div(n, B), B, 0, s, g.offsets, P.s1, n, total);
-    EFG_CUDA_CHECK(cudaEventRecord(ctx.aux_ev[0], s));
-    EFG_CUDA_CHECK(cudaStreamWaitEvent(ctx.copy_stream, ctx.aux_ev[0], 0));
-    EFG_CUDA_CHECK(cudaMemcpyAsync(stg.total_host, total, n * sizeof(int64_t), cudaMemcpyDeviceToHost, ctx.copy_stream));
-    EFG_CUDA_CHECK(cudaEventRecord(ctx.aux_ev[1], ctx.copy_stream));
-    ctx.total_sent = true;
-    total = nullptr;
-  }
   // whole-graph passes list triangles (they gather |Adj+(u)| from dplus); the
   // per-seed triangle path reads it per slot from the slot table
   const bool listing = dp || (r.lo == 0 && r.hi == n && P.dmax <= kListMaxDeg);
-  prepare_tail(ctx, P, true, !listing);
+  const bool tables = dmode == -1 || dmode == kDistRepl || dmode == kDistTables;  // chain tables and pushes here
+  Lists L = make_lists(ctx, P, rows, r, cdev, true, tables, !listing);
+  if (dp) {
+    EFG_REQUIRE(P.dmax <= kListMaxDeg, "distributed pass: maximum degree above the listing bound");
+    if (dmode == kDistRepl || dmode == kDistRows) {  // the tables / listing parts add into these words
+      EFG_CUDA_CHECK(cudaMemsetAsync(dp->words, 0, kDistWords * n * sizeof(unsigned long long), s));
+      EFG_CUDA_CHECK(cudaMemsetAsync(dp->ws, 0, n * sizeof(double), s));
+    }
+  }
+  if (!listing)
+    EFG_LAUNCH(k_hub_count, 2 * ctx.num_sms, 256, 0, s, L.hub, cdev + kHubs, g.offsets,
+               reinterpret_cast<unsigned long long*>(cdev + kNTasks));
+  else if (dmode != kDistRows && dmode != kDistTables)
+    EFG_LAUNCH(k_list_counts, 1, 256, 0, s, P.deg_by_rank, n, cdev, kTrS, kTr1, kTr2, kTr3, kHubs, kNTasks);
+  int64_t c[kNCounts];
+  read_counts(ctx, cdev, c);
+  // ---- phase 2: no further host synchronisation; per row chunk as it arrives
+  int32_t* dcnt = ctx.buf("f_dcnt").as<int32_t>(n);
+  int32_t* hkey = nullptr;
+  int32_t* hcnt = nullptr;
+  ChainAcc ca{};
+  if (dmode != kDistList) {
+    double* ctab = nullptr;
+    if (tables) {
+      hkey = ctx.buf("f_hkey").as<int32_t>(m2);
+      hcnt = ctx.buf("f_hcnt").as<int32_t>(m2);
+      ctab = ctx.buf("f_ctab").as<double>(m2);
+      unsigned long long* acc = dp ? dp->words : ctx.buf("f_chain_acc").as<unsigned long long>(3 * n);
+      if (!dp) EFG_CUDA_CHECK(cudaMemsetAsync(acc, 0, 3 * n * sizeof(unsigned long long), s));
+      ca.wh = acc;
+      ca.wl = acc + n;
+      ca.p2 = acc + 2 * n;
+      ca.ws = dp ? dp->ws : ctx.buf("f_chain_ws").as<double>(n);
+      const double d3 = 3.0 * (P.dmax > 1 ? P.dmax : 1);
+      ca.c0 = (P.dmax > 1 ? P.dmax : 1) * d3 * log(d3);
+    }
+    if (dmode == kDistRepl) prepare_rows(ctx, P, 0, n, 0, g.m2);  // every row's orientation, no exchange
+    for (int k = 0; k < rows.nchunks; ++k) {
+      if (!dp && stg.ready[k]) EFG_CUDA_CHECK(cudaStreamWaitEvent(s, stg.ready[k], 0));
+      if (dmode == -1 || dmode == kDistRows)
+        prepare_rows(ctx, P, rows.row[k], rows.row[k + 1], rows.slot[k], rows.slot[k + 1]);
+      if (!tables) continue;
+      build_histograms(ctx, P, L, c, rows, k, hkey, hcnt, dcnt, false);
+      // rows with d <= 32: histogram, chain table and pushes fused in registers
+      const int64_t nsm = c[cslot(kHW, k)];
+      EFG_LAUNCH(k_small_rows, ceil_div(nsm, kSmallWarps), kSmallWarps * 32, 0, s, L.hw + rows.row[k], nsm,
+                 g.offsets, g.nbr, P.nd, P.deg, P.ftab, P.s1, ca, P.ftab_len);
+      // chain tables C_i(y): rows with 32 < d <= 64 by 8-lane groups, the rest by CTAs
+      const int64_t o = rows.row[k], ng = c[cslot(kCG, k)], nb = c[cslot(kCB, k)];
+      EFG_LAUNCH(k_ctab_group<8>, ceil_div(ng * 8, B), B, 0, s, L.cg + o, ng, g.offsets, dcnt, hkey, hcnt, P.deg,
+                 P.ftab, ctab, P.ftab_len);
+      EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab,
+                 ctab, kExpMin, kExpMinD, P.ftab_len);
+      // chains pushed from the rows whose tables are now complete
+      const int64_t ps1 = c[cslot(kHS, k)], pb = c[cslot(kHB, k)], pl = c[cslot(kHL, k)];
+      EFG_LAUNCH(k_push_warp256, ceil_div(ps1, kPushWarps), kPushWarps * 32, 0, s, L.hs + o, ps1, g.offsets, g.nbr,
+                 P.nd, dcnt, hkey, hcnt, ctab, P.s1, ca);
+      EFG_LAUNCH(k_push_block, pb, kPushThreads, 0, s, L.hb + o, pb, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,
+                 P.s1, ca);
+      // rows of degree > 2048 in kPushSlices slices each (a hub row is one CTA's long serial loop otherwise)
+      EFG_LAUNCH(k_push_block, dim3((unsigned)pl, kPushSlices), kPushThreads, 0, s, L.hl + o, pl, g.offsets, g.nbr,
+                 P.nd, dcnt, hkey, hcnt, ctab, P.s1, ca);
+    }
+    if (dmode == kDistRepl || dmode == kDistRows) {  // the part's S1 / S2 into the words (the finish needs them)
+      const int64_t cntp = dp->node_hi - dp->node_lo;
+      if (cntp > 0)
+        EFG_LAUNCH(k_part_s12, ceil_div(cntp, B), B, 0, s, P.s1, P.s2, dp->node_lo, dp->node_hi,
+                   dp->words + 7 * n, dp->words + 8 * n);
+    }
+    if (stg.total_host && !dp && r.lo == 0 && r.hi == n && n > 0) {
+      // S1 is complete: cluster totals now, their read-back overlaps the listing
+      EFG_LAUNCH(k_mass, ceil_div(n, B), B, 0, s, g.offsets, P.s1, n, total);
+      EFG_CUDA_CHECK(cudaEventRecord(ctx.aux_ev[0], s));
+      EFG_CUDA_CHECK(cudaStreamWaitEvent(ctx.copy_stream, ctx.aux_ev[0], 0));
+      EFG_CUDA_CHECK(cudaMemcpyAsync(stg.total_host, total, n * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                     ctx.copy_stream));
+      EFG_CUDA_CHECK(cudaEventRecord(ctx.aux_ev[1], ctx.copy_stream));
+      ctx.total_sent = true;
+      total = nullptr;
+    }
+    if (dmode == kDistRows) {
+      // the part's rows sorted; the caller exchanges Adj+ rows and |Adj+| (overlapping the tables part),
+      // then runs the listing part
+      prepare_tail(ctx, P, true, false, dp->node_lo, dp->node_hi);
+      if (st) EFG_CUDA_CHECK(cudaEventRecord(ctx.ev[3], s));
+      dh.P = P;
+      dh.valid = true;
+      return PrepInfo{P.dmax, P.sum_c2};
+    }
+    if (dmode == kDistTables) {
+      if (st) EFG_CUDA_CHECK(cudaEventRecord(ctx.ev[3], s));
+      return PrepInfo{P.dmax, P.sum_c2};
+    }
+    prepare_tail(ctx, P, true, !listing);
+  }
   if (st) EFG_CUDA_CHECK(cudaEventRecord(ctx.ev[3], s));
   const PrepInfo info{P.dmax, P.sum_c2};
   if (cnt <= 0 && !dp) return info;
@@ -2095,14 +2245,19 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   int64_t* tstart = nullptr;
   int32_t* hs = nullptr;
   if (nhubs) {
-    int64_t* hw = ctx.buf("f_hub_work").as<int64_t>(2 * nhubs + 2);
-    EFG_LAUNCH(k_hub_work, nhubs, 256, 0, s, L.hub, nhubs, g.offsets, g.nbr, P.dplus, hw);
-    int64_t* hw_sorted = hw + nhubs;
-    hs = ctx.buf("f_hub_sorted").as<int32_t>(nhubs);
-    EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, hw, hw_sorted, L.hub, hs, nhubs, 0, 64, s));
-    EFG_REGION("cub::DeviceRadixSort::SortPairsDescending", s,
-               EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(ctx.buf("cub").get(tmp), tmp, hw, hw_sorted,
-                                                                        L.hub, hs, nhubs, 0, 64, s)));
+    if (listing) {
+      hs = P.by_rank;  // hubs in descending degree order: labels [0, nhubs)
+    } else {           // hubs in descending triangle-probe order
+      int64_t* hw = ctx.buf("f_hub_work").as<int64_t>(2 * nhubs + 2);
+      EFG_LAUNCH(k_hub_work, nhubs, 256, 0, s, L.hub, nhubs, g.offsets, g.nbr, P.dplus, hw);
+      int64_t* hw_sorted = hw + nhubs;
+      hs = ctx.buf("f_hub_sorted").as<int32_t>(nhubs);
+      EFG_CUDA_CHECK(
+          cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, hw, hw_sorted, L.hub, hs, nhubs, 0, 64, s));
+      EFG_REGION("cub::DeviceRadixSort::SortPairsDescending", s,
+                 EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(ctx.buf("cub").get(tmp), tmp, hw,
+                                                                          hw_sorted, L.hub, hs, nhubs, 0, 64, s)));
+    }
     int64_t* hnt = ctx.buf("f_hub_nt").as<int64_t>(nhubs + 1);
     tstart = ctx.buf("f_hub_tstart").as<int64_t>(nhubs + 1);
     EFG_LAUNCH(k_hub_ntasks, ceil_div(nhubs + 1, B), B, 0, s, hs, nhubs, P.g.offsets, hnt);
@@ -2124,7 +2279,8 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     if (!dp) EFG_CUDA_CHECK(cudaMemsetAsync(acc, 0, 4 * n * sizeof(unsigned long long), s));
     ma.offsets = P.g.offsets;
     ma.nbr = P.g.nbr;
-    ma.nd = P.nd;
+    ma.nd = dp && dp->mode == kDistList ? nullptr : P.nd;
+    ma.deg = P.deg;
     ma.dplus = P.dplus;
     ma.adjj = P.adjj;
     ma.adjd = P.adjd;
@@ -2156,15 +2312,7 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
       EFG_LAUNCH(k_mid_small<false>, ms.nunits, MidSmall::kThreads, 0, s, ms, tk);
     }
     EFG_LAUNCH(k_mid_warp, ceil_div(ceil_div(n - ma.n32, ma.nparts), kMidWarps), kMidWarps * 32, 0, s, ma);
-    if (dp) {  // the caller reduces the words over all parts, then ef_finish (which reuses S1/S2)
-      ctx.part_cache.offsets = g.offsets;
-      ctx.part_cache.nbr = g.nbr;
-      ctx.part_cache.n = n;
-      ctx.part_cache.m2 = g.m2;
-      ctx.part_cache.dmax = P.dmax;
-      ctx.part_cache.valid = true;
-      return info;
-    }
+    if (dp) return info;  // the caller reduces the words over all parts, then ef_finish
     EFG_LAUNCH(k_list_out, ceil_div(cnt, B), B, 0, s, acc, a, cnt);
   } else if (nhubs) {
     // exact bitmaps over rank labels, per-task partials merged in task order
@@ -2211,17 +2359,16 @@ void ef_finish(Context& ctx, const CSRView& g, SeedRange r, const unsigned long 
   const int B = 256;
   const int64_t n = g.n, cnt = r.hi - r.lo;
   if (cnt <= 0) return;
-  const auto& pc = ctx.part_cache;
+  // S1 / S2 arrive in the reduced words (every part wrote its own rows');
+  // dmax (the chain words' fixed-point scale) from the degrees
   Prepared P;
-  if (pc.valid && pc.offsets == g.offsets && pc.nbr == g.nbr && pc.n == n && pc.m2 == g.m2) {
-    // S1/S2 of the preceding ef_partial on this graph are still resident
-    P.s1 = ctx.buf("s1").as<int64_t>(n);
-    P.s2 = ctx.buf("s2").as<int64_t>(n);
-    P.dmax = pc.dmax;
-  } else {
+  const auto& dh = ctx.dist_head;
+  if (dh.valid && dh.P.g.offsets == g.offsets && dh.P.g.nbr == g.nbr && dh.P.g.n == n && dh.P.g.m2 == g.m2)
+    P = dh.P;  // the distributed parts' head on this graph
+  else
     prepare_head(ctx, g, false, P);
-    prepare_rows(ctx, P, 0, n, 0, g.m2);
-  }
+  P.s1 = const_cast<int64_t*>(reinterpret_cast<const int64_t*>(words + 7 * n));
+  P.s2 = const_cast<int64_t*>(reinterpret_cast<const int64_t*>(words + 8 * n));
   FArgs a{};
   a.offsets = g.offsets;
   a.s1 = P.s1;

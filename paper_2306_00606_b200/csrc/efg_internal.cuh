@@ -78,36 +78,6 @@ struct HostStager {
 };
 bool is_pageable(const void* p);
 
-struct Context {
-  int device = 0;
-  int num_sms = kNumSMs;
-  cudaStream_t stream = nullptr;
-  bool own_stream = false;
-  std::map<std::string, DevBuf> bufs;
-  std::mutex mu;
-  cudaEvent_t ev[16] = {};
-  // S1/S2/dmax of the last distributed part (ef_partial) for the ef_finish that
-  // follows on the same graph; any other preparation invalidates it
-  struct {
-    const int64_t* offsets = nullptr;
-    const int32_t* nbr = nullptr;
-    int64_t n = -1, m2 = -1;
-    int32_t dmax = 0;
-    bool valid = false;
-  } part_cache;
-  cudaStream_t copy_stream = nullptr;   // host->device staging of efg_expected_force inputs
-  cudaEvent_t chunk_ev[9] = {};         // offsets + neighbour chunks resident (kMaxChunks + 1)
-  cudaEvent_t aux_ev[2] = {};           // early cluster-total read-back: totals written / copied
-  cudaStream_t side_stream = nullptr;   // independent preparation kernels run beside the main stream
-  cudaEvent_t side_ev[2] = {};          // fork / join of side_stream
-  bool total_sent = false;              // set by the engine when it queued that read-back
-  Profiler prof;
-  HostStager stager;  // pageable inputs of efg_expected_force
-  DeviceCSR csr;  // resident graph of efg_build_graph / efg_rmat_build
-  DevBuf& buf(const std::string& name) { return bufs[name]; }
-  ~Context();
-};
-
 // Read-only view of a CSR that some caller owns (device pointers).
 struct CSRView {
   int64_t n = 0, m2 = 0;                 // m2 = 2m adjacency entries
@@ -137,6 +107,34 @@ struct Prepared {
   int32_t* pc = nullptr;        // [2m] per slot (v->i): |Adj+(i)|
 };
 
+struct Context {
+  int device = 0;
+  int num_sms = kNumSMs;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::map<std::string, DevBuf> bufs;
+  std::mutex mu;
+  cudaEvent_t ev[16] = {};
+  cudaStream_t copy_stream = nullptr;   // host->device staging of efg_expected_force inputs
+  cudaEvent_t chunk_ev[9] = {};         // offsets + neighbour chunks resident (kMaxChunks + 1)
+  cudaEvent_t aux_ev[2] = {};           // early cluster-total read-back: totals written / copied
+  cudaStream_t side_stream = nullptr;   // independent preparation kernels run beside the main stream
+  cudaEvent_t side_ev[2] = {};          // fork / join of side_stream
+  bool total_sent = false;              // set by the engine when it queued that read-back
+  Profiler prof;
+  // degrees, F/G tables and rank labels of the last distributed rows part,
+  // reused by the listing part that follows on the same graph
+  // (prepare_head invalidates it)
+  struct {
+    Prepared P;
+    bool valid = false;
+  } dist_head;
+  HostStager stager;  // pageable inputs of efg_expected_force
+  DeviceCSR csr;  // resident graph of efg_build_graph / efg_rmat_build
+  DevBuf& buf(const std::string& name) { return bufs[name]; }
+  ~Context();
+};
+
 struct SeedRange {
   int64_t lo = 0, hi = 0;
 };
@@ -154,7 +152,8 @@ void prepare_head(Context& ctx, const CSRView& g, bool need_orientation, Prepare
 void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t e0, int64_t e1);
 // need_slot_table: the per-slot |Adj+(i)| table P.pc (K2 work, per-seed
 // triangle paths); whole-graph listing passes gather it from dplus instead
-void prepare_tail(Context& ctx, Prepared& P, bool need_orientation, bool need_slot_table);
+void prepare_tail(Context& ctx, Prepared& P, bool need_orientation, bool need_slot_table, int64_t r0 = 0,
+                  int64_t r1 = -1);  // sorts the Adj+ rows of nodes [r0, r1) (r1 < 0: all)
 
 // Host inputs arriving on a copy stream in row chunks (efg_expected_force):
 // work on the rows of chunk k may start once ready[k] has fired (null event:
@@ -176,17 +175,38 @@ struct PrepInfo {
   int32_t dmax = 0;
   int64_t sum_c2 = 0;
 };
-// One part of a distributed whole-graph pass (efg_ef_partial): the part
-// builds the chain tables and pushes of the rows v % nparts == part and lists
-// the triangles of every nparts-th work unit; its integer words (planar chain
-// hi / lo / S1 sums, then per node triangle hi / lo / count / pad) and stars
-// terms are summed over all parts by the caller before ef_finish.
-constexpr int kDistWords = 7;  // u64 words per node
+// One part of a distributed whole-graph pass.  Part p owns the node range
+// [node_lo, node_hi) (efg_part_bounds: contiguous, balanced by row work): its
+// rows' neighbour degrees, S1/S2, label-sorted Adj+ rows, chain tables and
+// pushes; and it lists the triangles of every nparts-th listing work unit.
+// Integer words per node (planar): chain hi / lo / S1 sums [0, 3n), triangle
+// hi / lo / count / pad [3n, 7n), S1 [7n, 8n), S2 [8n, 9n) (own rows only);
+// the caller sums them over all parts (integer addition, disjoint supports:
+// exact in any order) before ef_finish.  Modes:
+//   kDistRepl -- efg_ef_partial: every rank prepares ALL rows' orientation
+//                itself (no exchange), tables / pushes of its range only;
+//   kDistRows -- efg_ef_partial_rows: its range's rows only (neighbour
+//                degrees, S1/S2, label-sorted Adj+ rows into the caller's
+//                slot-space buffer adjp, |Adj+| into dplus); the caller then
+//                exchanges adjp / dplus (each part broadcasts its slot / node
+//                range) so that every rank holds all rows;
+//   kDistTables -- efg_ef_partial_tables: its range's histograms, chain
+//                tables and pushes (runs while the exchange is in flight);
+//   kDistList -- efg_ef_partial_list: the listing on the exchanged adjp /
+//                dplus (the preceding kDistRows call cleared the words).
+constexpr int kDistWords = 9;  // u64 words per node
+enum DistMode { kDistRepl = 0, kDistRows = 1, kDistList = 2, kDistTables = 3 };
 struct DistPart {
   int32_t part = 0, nparts = 1;
+  int mode = kDistRepl;
+  int64_t node_lo = 0, node_hi = 0;
   unsigned long long* words = nullptr;  // [kDistWords n]
   double* ws = nullptr;                 // [n]
+  int32_t* adjp = nullptr;              // [2m] slot-space Adj+ rows (kDistRows out / kDistList in)
+  int32_t* dplus = nullptr;             // [n] |Adj+(v)| (same)
 };
+// Balanced contiguous node ranges of the distributed pass (bounds[nparts+1], host).
+void part_bounds(Context& ctx, const CSRView& g, int32_t nparts, int64_t* bounds);
 PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedRange r, double* ef, int64_t* total,
                        uint8_t* flags, int64_t* T_out, double* W_out, efg_stats* st, const DistPart* dp = nullptr);
 void ef_finish(Context& ctx, const CSRView& g, SeedRange r, const unsigned long long* words, const double* ws,

@@ -316,22 +316,22 @@ __device__ __forceinline__ void sort_one(int64_t b, int pv, int lane, const int3
   __syncwarp();
 }
 
-// Rows of 2..256 entries: a warp per group of 32 nodes sorts the group's rows.
-__global__ void k_sort_small(const int64_t* __restrict__ offsets, const int32_t* __restrict__ dplus, int64_t n,
+// Rows of 2..256 entries of nodes [r0, r1): a warp per group of 32 nodes sorts the group's rows.
+__global__ void k_sort_small(const int64_t* __restrict__ offsets, const int32_t* __restrict__ dplus, int64_t r0, int64_t r1,
                              const int32_t* __restrict__ deg_by_rank, int32_t* __restrict__ adjj,
                              int32_t* __restrict__ adjd, int32_t* __restrict__ scratch) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; g * 32 < n; g += nw) {
-    const int64_t mine = g * 32 + lane;
+  for (int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r0 + g * 32 < r1; g += nw) {
+    const int64_t mine = r0 + g * 32 + lane;
     int p = 0;
-    if (mine < n) p = dplus[mine];
+    if (mine < r1) p = dplus[mine];
     unsigned todo = __ballot_sync(0xffffffffu, p >= 2 && p <= 256);
     while (todo) {
       const int x = __ffs(todo) - 1;
       todo &= todo - 1;
       const int pv = __shfl_sync(0xffffffffu, p, x);
-      sort_one<true>(offsets[g * 32 + x], pv, lane, deg_by_rank, adjj, adjd, scratch);
+      sort_one<true>(offsets[r0 + g * 32 + x], pv, lane, deg_by_rank, adjj, adjd, scratch);
     }
   }
 }
@@ -341,12 +341,14 @@ __global__ void k_sort_small(const int64_t* __restrict__ offsets, const int32_t*
 // low ids in R-MAT graphs -- spread over all warps.
 __global__ void k_sort_large(const int64_t* __restrict__ offsets, const int32_t* __restrict__ dplus, int64_t n,
                              const int32_t* __restrict__ by_rank, const int32_t* __restrict__ deg_by_rank,
-                             int32_t* __restrict__ adjj, int32_t* __restrict__ adjd, int32_t* __restrict__ scratch) {
+                             int32_t* __restrict__ adjj, int32_t* __restrict__ adjd, int32_t* __restrict__ scratch,
+                             int64_t r0, int64_t r1) {
   const int lane = threadIdx.x & 31;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; r < n; r += nw) {
     if (deg_by_rank[r] <= 256) break;
     const int32_t v = by_rank[r];
+    if (v < r0 || v >= r1) continue;  // another part's row
     const int pv = dplus[v];
     if (pv > 256) sort_one<false>(offsets[v], pv, lane, deg_by_rank, adjj, adjd, scratch);
   }
@@ -361,7 +363,7 @@ struct Choose2 {
 // Offsets-only part: degrees, dmax (the one host sync), the F/G tables and
 // the rank labels.  Runs while the neighbour arrays may still be in flight.
 void prepare_head(Context& ctx, const CSRView& g, bool need_orientation, Prepared& P) {
-  ctx.part_cache.valid = false;  // the s1/s2/deg buffers are about to be rewritten
+  ctx.dist_head.valid = false;  // its buffers are about to be rewritten
   cudaStream_t s = ctx.stream;
   const int B = 256;
   P.g = g;
@@ -416,7 +418,7 @@ void prepare_head(Context& ctx, const CSRView& g, bool need_orientation, Prepare
 // degrees, S1, S2 and (with the orientation) Adj+ in slot space.
 void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t, int64_t) {
   cudaStream_t s = ctx.stream;
-  P.dplus = ctx.buf("dplus").as<int32_t>(P.g.n > 0 ? P.g.n : 1);
+  if (!P.dplus) P.dplus = ctx.buf("dplus").as<int32_t>(P.g.n > 0 ? P.g.n : 1);  // (or the caller's buffer)
   const int32_t nbig = P.rank_of ? kRowBigBlocks : 0;  // hub CTAs need the rank order
   EFG_LAUNCH(k_row_sums, nbig + ceil_div((r1 - r0) * 32, kRowThreads), kRowThreads, 0, s, P.g.offsets, P.g.nbr, P.nd,
              P.deg, r0, r1, P.s1, P.s2, P.dplus, P.rank_of, P.rank_of ? P.adjj : nullptr, P.adjd, P.by_rank, P.deg_by_rank,
@@ -424,7 +426,7 @@ void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t, in
 }
 
 // Everything that needs all neighbours: the label-sorted orientation.
-void prepare_tail(Context& ctx, Prepared& P, bool need_orientation, bool need_slot_table) {
+void prepare_tail(Context& ctx, Prepared& P, bool need_orientation, bool need_slot_table, int64_t r0, int64_t r1) {
   if (!need_orientation) return;
   cudaStream_t s = ctx.stream;
   const int B = 256;
@@ -433,16 +435,17 @@ void prepare_tail(Context& ctx, Prepared& P, bool need_orientation, bool need_sl
   {
     // rows sorted by label: a row scan for a higher-ranked v can stop at v (triangle listing)
     int32_t* scratch = ctx.buf("adjj_scratch").as<int32_t>(m2 > 0 ? m2 : 1);
-    const int64_t groups = ceil_div(n, 32);
+    if (r1 < 0) r1 = n;
+    const int64_t groups = ceil_div(r1 - r0, 32);
     // the few long rows (> 256 entries, a warp each for a long time) sort on
     // the side stream while the short rows and the slot table fill the GPU
     EFG_CUDA_CHECK(cudaEventRecord(ctx.side_ev[0], s));
     EFG_CUDA_CHECK(cudaStreamWaitEvent(ctx.side_stream, ctx.side_ev[0], 0));
     EFG_LAUNCH(k_sort_large, 4 * ctx.num_sms, B, 0, ctx.side_stream, g.offsets, P.dplus, n, P.by_rank,
-               P.deg_by_rank, P.adjj, P.adjd, scratch);
+               P.deg_by_rank, P.adjj, P.adjd, scratch, r0, r1);
     EFG_CUDA_CHECK(cudaEventRecord(ctx.side_ev[1], ctx.side_stream));
     EFG_LAUNCH(k_sort_small, std::min<int64_t>(ceil_div(groups * 32, B), 16 * ctx.num_sms), B, 0, s, g.offsets,
-               P.dplus, n, P.deg_by_rank, P.adjj, P.adjd, scratch);
+               P.dplus, r0, r1, P.deg_by_rank, P.adjj, P.adjd, scratch);
   }
   if (need_slot_table) {
     P.pc = ctx.buf("pc").as<int32_t>(m2);

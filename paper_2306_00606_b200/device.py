@@ -71,13 +71,26 @@ def ef_range(dg: DeviceGraph, lo: int, hi: int, out_ef, out_total, out_flags, en
     return st.as_dict() if st is not None else None
 
 
-DIST_WORDS = 7  # EFG_DIST_WORDS: uint64 words per node of a distributed pass
+DIST_WORDS = 9  # EFG_DIST_WORDS: uint64 words per node of a distributed pass
+
+
+def part_bounds(dg: DeviceGraph, nparts: int) -> np.ndarray:
+    """Contiguous node ranges of the distributed pass, balanced by row work
+    (efg_part_bounds; identical on every rank: it depends only on the degrees)."""
+    import torch
+
+    ctx = _ctx_for(dg.offsets)
+    _bind_stream(ctx, torch.cuda.current_stream(dg.offsets.device))
+    out = np.zeros(nparts + 1, np.int64)
+    _native.check(_native.lib().efg_part_bounds(ctx.handle, _dptr(dg.offsets), _dptr(dg.neighbors), dg.n,
+                                                int(nparts), _native.ptr(out)))
+    return out
 
 
 def ef_partial(dg: DeviceGraph, part: int, nparts: int, words, ws, stats: bool = False):
-    """One part of a distributed whole-graph pass (efg_ef_partial): integer
-    words int64[DIST_WORDS * n] and stars terms f64[n] of part `part` of
-    `nparts`; sum both over all parts, then ef_finish."""
+    """One self-contained part of a distributed whole-graph pass (efg_ef_partial):
+    integer words int64[DIST_WORDS * n] and stars terms f64[n] of part `part`
+    of `nparts`; sum both over all parts, then ef_finish."""
     import torch
 
     ctx = _ctx_for(dg.offsets)
@@ -86,6 +99,53 @@ def ef_partial(dg: DeviceGraph, part: int, nparts: int, words, ws, stats: bool =
     st = _native.Stats() if stats else None
     _native.check(L.efg_ef_partial(ctx.handle, _dptr(dg.offsets), _dptr(dg.neighbors), dg.n, int(part), int(nparts),
                                    _dptr(words), _dptr(ws), ctypes.byref(st) if st is not None else None))
+    return st.as_dict() if st is not None else None
+
+
+def ef_partial_rows(dg: DeviceGraph, part: int, nparts: int, bounds, adjp, dplus, words, ws, stats: bool = False):
+    """The rows phase of a row-partitioned part (efg_ef_partial_rows): the part's
+    neighbour degrees and S1/S2 (into words), its label-sorted Adj+ rows into
+    adjp (int32[2m], slot space) and |Adj+| into dplus (int32[n])."""
+    import torch
+
+    ctx = _ctx_for(dg.offsets)
+    _bind_stream(ctx, torch.cuda.current_stream(dg.offsets.device))
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    st = _native.Stats() if stats else None
+    _native.check(_native.lib().efg_ef_partial_rows(
+        ctx.handle, _dptr(dg.offsets), _dptr(dg.neighbors), dg.n, int(part), int(nparts), _native.ptr(b),
+        _dptr(adjp), _dptr(dplus), _dptr(words), _dptr(ws), ctypes.byref(st) if st is not None else None))
+    return st.as_dict() if st is not None else None
+
+
+def ef_partial_tables(dg: DeviceGraph, part: int, nparts: int, bounds, words, ws, stats: bool = False):
+    """The tables phase of a row-partitioned part (efg_ef_partial_tables): the
+    part's histograms, chain tables and pushes into words / ws (after its rows
+    phase on the same context; runs while the Adj+ row exchange is in flight)."""
+    import torch
+
+    ctx = _ctx_for(dg.offsets)
+    _bind_stream(ctx, torch.cuda.current_stream(dg.offsets.device))
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    st = _native.Stats() if stats else None
+    _native.check(_native.lib().efg_ef_partial_tables(
+        ctx.handle, _dptr(dg.offsets), _dptr(dg.neighbors), dg.n, int(part), int(nparts), _native.ptr(b),
+        _dptr(words), _dptr(ws), ctypes.byref(st) if st is not None else None))
+    return st.as_dict() if st is not None else None
+
+
+def ef_partial_list(dg: DeviceGraph, part: int, nparts: int, bounds, adjp, dplus, words, ws, stats: bool = False):
+    """The listing phase of a row-partitioned part (efg_ef_partial_list) on the
+    exchanged adjp / dplus; adds the part's triangle words into words."""
+    import torch
+
+    ctx = _ctx_for(dg.offsets)
+    _bind_stream(ctx, torch.cuda.current_stream(dg.offsets.device))
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    st = _native.Stats() if stats else None
+    _native.check(_native.lib().efg_ef_partial_list(
+        ctx.handle, _dptr(dg.offsets), _dptr(dg.neighbors), dg.n, int(part), int(nparts), _native.ptr(b),
+        _dptr(adjp), _dptr(dplus), _dptr(words), _dptr(ws), ctypes.byref(st) if st is not None else None))
     return st.as_dict() if st is not None else None
 
 

@@ -3,13 +3,15 @@
 Two schemes, both one process per GPU (torch.distributed, NCCL over NVLink on
 B200 boxes) with the full CSR replicated in every rank's HBM:
 
-* ``ef_distributed`` (whole-graph passes, the default of bench.py): every
-  rank runs one part of the factorized pass -- the chain tables / pushes of
-  its nodes and the triangles listed by its share of work units
-  (efg_ef_partial) -- and ONE all-reduce sums the per-node integer words and
-  stars terms; every rank then finishes all seeds locally (efg_ef_finish).
-  Integer sums and disjoint supports make the result bitwise identical to the
-  single-GPU pass for any world size.
+* ``ef_distributed`` (whole-graph passes, the default of bench.py): rank p
+  prepares the rows of its node range only (neighbour degrees, S1/S2, the
+  label-sorted Adj+ rows, chain tables and pushes: efg_ef_partial_rows), the
+  ranks exchange their Adj+ rows (one broadcast per part), rank p lists the
+  triangles of its share of work units (efg_ef_partial_list), and ONE
+  all-reduce sums the per-node integer words and stars terms; every rank then
+  finishes all seeds locally (efg_ef_finish).  Integer sums and disjoint
+  supports make the result bitwise identical to the single-GPU pass for any
+  world size.
 * ``ef_sharded`` (seed shards; the direct engine and explicit seed ranges):
   K2 cuts the seed range into contiguous shards of equal engine work
   (`shard_bounds`, the same bounds on every rank because they depend only on
@@ -29,17 +31,19 @@ import numpy as np
 RECORD_BYTES = 17  # f64 ef + i64 cluster_total + u8 flags
 
 
-def _all_reduce_sum(t, group):
-    """All-reduce (sum) of a device tensor: NCCL in place; under gloo (CPU
-    tests, or ranks sharing one GPU) through a host copy."""
+def _all_reduce_sum(t, group, async_op=False):
+    """All-reduce (sum) of a device tensor: NCCL in place (asynchronous on
+    request: the work handle is returned); under gloo (CPU tests, or ranks
+    sharing one GPU) through a host copy, synchronously."""
     import torch.distributed as dist
 
     if dist.get_backend(group) == "nccl" or t.device.type == "cpu":
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
-        return
+        return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group,
+                               async_op=async_op and dist.get_backend(group) == "nccl")
     h = t.cpu()
     dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
     t.copy_(h)
+    return None
 
 
 def ef_cluster_centric_distributed(g, group=None, T=None, W=None):
@@ -64,12 +68,48 @@ def ef_cluster_centric_distributed(g, group=None, T=None, W=None):
                     clusters_processed=cluster_count(g))
 
 
-def ef_distributed(dg, group=None, partial=None, finish=None, T=None, W=None):
+def exchange_rows(adjp, dplus, slot_bounds, node_bounds, group=None, async_op=False):
+    """Every part's slot range of adjp and node range of dplus to every rank:
+    one broadcast per part, rooted at the part's rank, in place (NCCL over
+    NVLink; under gloo through host memory).  With async_op (NCCL) the
+    broadcasts are queued on NCCL's stream and their work handles returned:
+    the caller overlaps them with the tables phase and waits before listing."""
+    import torch.distributed as dist
+
+    world = len(node_bounds) - 1
+    nccl = dist.get_backend(group) == "nccl"
+    works = []
+    for p in range(world):
+        for buf, lo, hi in ((adjp, slot_bounds[p], slot_bounds[p + 1]), (dplus, node_bounds[p], node_bounds[p + 1])):
+            lo, hi = int(lo), int(hi)
+            if hi <= lo:
+                continue
+            view = buf[lo:hi]
+            if nccl or view.device.type == "cpu":
+                w = dist.broadcast(view, src=p, group=group, async_op=async_op and nccl)
+                if w is not None:
+                    works.append(w)
+            else:
+                h = view.cpu()
+                dist.broadcast(h, src=p, group=group)
+                view.copy_(h)
+    return works
+
+
+def ef_distributed(dg, group=None, rows=None, tables=None, listing=None, finish=None, T=None, W=None):
     """EF of every seed of DeviceGraph `dg`, the whole-graph pass split over
     the ranks of `group`; returns (ef, cluster_total, flags) on every rank.
-    `partial(dg, part, nparts, words, ws)` / `finish(dg, words, ws, ef, tot,
-    fl)` default to the GPU library (device.ef_partial / ef_finish); tests
-    substitute CPU stand-ins under gloo."""
+
+    Rank p prepares only its node range's rows (efg_ef_partial_rows: neighbour
+    degrees, S1/S2, label-sorted Adj+ rows), the ranks exchange the Adj+ rows
+    (one broadcast per part, exchange_rows, asynchronous under NCCL) while
+    rank p builds its rows' chain tables and pushes (efg_ef_partial_tables),
+    rank p lists the triangles of its work units (efg_ef_partial_list), ONE
+    all-reduce sums the integer words and stars terms, and every rank
+    finishes all seeds (efg_ef_finish).  `rows(dg, part, nparts, bounds, adjp,
+    dplus, words, ws)` / `tables(dg, part, nparts, bounds, words, ws)` /
+    `listing(...)` / `finish(dg, words, ws, ef, tot, fl)` default to the GPU
+    library; tests substitute CPU stand-ins under gloo."""
     import torch
     import torch.distributed as dist
 
@@ -79,16 +119,37 @@ def ef_distributed(dg, group=None, partial=None, finish=None, T=None, W=None):
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     dev = dg.offsets.device
     n = dg.n
+    bounds = D.part_bounds(dg, world) if rows is None else np.linspace(0, n, world + 1).astype(np.int64)
     words = torch.empty(D.DIST_WORDS * n, dtype=torch.int64, device=dev)
     ws = torch.empty(n, dtype=torch.float64, device=dev)
-    if partial is None:
-        D.ef_partial(dg, rank, world, words, ws)
-    else:
-        partial(dg, rank, world, words, ws)
+    adjp = torch.empty(max(1, dg.neighbors.numel()), dtype=torch.int32, device=dev)
+    dplus = torch.empty(max(1, n), dtype=torch.int32, device=dev)
+    (rows or D.ef_partial_rows)(dg, rank, world, bounds, adjp, dplus, words, ws)
+    works = []
     if world > 1:
-        # integer words: exact in any order; stars terms: one nonzero per node
-        _all_reduce_sum(words, group)
-        _all_reduce_sum(ws, group)
+        slot_bounds = dg.offsets[torch.as_tensor(bounds, device=dev)].cpu().numpy()
+        works = exchange_rows(adjp, dplus, slot_bounds, bounds, group, async_op=True)
+    if tables is not None:
+        tables(dg, rank, world, bounds, words, ws)
+    elif rows is None:
+        D.ef_partial_tables(dg, rank, world, bounds, words, ws)
+    for w in works:  # the listing reads every part's rows
+        w.wait()
+    # integer words: exact in any order; stars terms: one nonzero per node.  The
+    # chain / S1 / S2 words and the stars terms are final after the tables
+    # phase: their all-reduce runs while the listing does; the triangle words
+    # [3n, 7n) follow it
+    early = []
+    if world > 1:
+        early = [_all_reduce_sum(words[: 3 * n], group, async_op=True),
+                 _all_reduce_sum(words[7 * n:], group, async_op=True),
+                 _all_reduce_sum(ws, group, async_op=True)]
+    (listing or D.ef_partial_list)(dg, rank, world, bounds, adjp, dplus, words, ws)
+    if world > 1:
+        _all_reduce_sum(words[3 * n: 7 * n], group)
+        for w in early:
+            if w is not None:
+                w.wait()
     ef = torch.empty(n, dtype=torch.float64, device=dev)
     tot = torch.empty(n, dtype=torch.int64, device=dev)
     fl = torch.empty(n, dtype=torch.uint8, device=dev)

@@ -1,7 +1,11 @@
-"""N>1 path on CPU: two gloo ranks shard the seeds, compute their shard
-(CPU oracle standing in for the GPU engine), exchange with the packed
-all-gather of distributed.ef_sharded, and must reproduce the single-pass
-result bitwise."""
+"""N>1 paths on CPU (gloo, world 2 and 3):
+
+* ef_sharded: the ranks shard the seeds, compute their shard (CPU oracle
+  standing in for the GPU engine), exchange with the packed all-gather, and
+  must reproduce the single-pass result bitwise;
+* ef_distributed: row-partitioned parts write their node range's Adj+ rows,
+  exchange_rows (one broadcast per part) must assemble every row on every
+  rank, and the one all-reduce of the integer words must be exact."""
 import os
 import socket
 
@@ -87,22 +91,42 @@ def test_pack_unpack_roundtrip():
     assert fl.tolist() == [0, 0, 0, 2, 2, 2, 2]
 
 
-# --- ef_distributed: parts of the whole-graph pass + one all-reduce --------
-def _split_partial(T, W):
-    """Stand-in for efg_ef_partial: part p holds an arbitrary (seeded) integer
-    split of every node's T in word 0 (negative pieces exercise wrap-free
-    int64 sums) and W of the nodes v % nparts == p (disjoint supports)."""
-    def partial(dg, part, nparts, words, ws):
+# --- ef_distributed: row-partitioned parts, row exchange, one all-reduce ----
+def _expected_rows(dg):
+    m2 = dg.neighbors.numel()
+    adjp = (np.arange(m2, dtype=np.int64) * 7 + 3) % (2**31 - 1)
+    dplus = np.arange(dg.n, dtype=np.int64) * 3 + 1
+    return adjp.astype(np.int32), dplus.astype(np.int32)
+
+
+def _split_rows(T, W):
+    """Stand-in for efg_ef_partial_rows: part p writes its node range's rows
+    (a known pattern) into adjp / dplus, an arbitrary (seeded) integer split of
+    every node's T into word 0 (negative pieces exercise wrap-free int64 sums)
+    and W of its node range (disjoint supports)."""
+    def rows(dg, part, nparts, bounds, adjp, dplus, words, ws):
         n = dg.n
+        lo, hi = int(bounds[part]), int(bounds[part + 1])
+        ea, ed = _expected_rows(dg)
+        so, se = int(dg.offsets[lo]), int(dg.offsets[hi])
+        adjp[so:se] = torch.from_numpy(ea[so:se])
+        dplus[lo:hi] = torch.from_numpy(ed[lo:hi])
         rng = np.random.default_rng(1234)  # same draws on every rank
         pieces = rng.integers(-2**40, 2**40, size=(nparts, n))
         pieces[-1] = T - pieces[:-1].sum(axis=0)
         w = np.zeros(words.numel(), np.int64)
         w[:n] = pieces[part]
         words.copy_(torch.from_numpy(w))
-        s = np.where(np.arange(n) % nparts == part, W, 0.0)
+        s = np.where((np.arange(n) >= lo) & (np.arange(n) < hi), W, 0.0)
         ws.copy_(torch.from_numpy(s))
-    return partial
+    return rows
+
+
+def _check_listing(dg, part, nparts, bounds, adjp, dplus, words, ws):
+    """Stand-in for efg_ef_partial_list: the exchanged rows must be complete."""
+    ea, ed = _expected_rows(dg)
+    assert np.array_equal(adjp.numpy(), ea), "Adj+ row exchange incomplete"
+    assert np.array_equal(dplus.numpy(), ed), "|Adj+| exchange incomplete"
 
 
 def _finish(dg, words, ws, ef, tot, fl):
@@ -120,7 +144,7 @@ def _dist_worker(rank, world, port, offsets, neighbors, T, W, out_path):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         dg = HostGraph(offsets, neighbors)
-        ef, tot, fl = Dist.ef_distributed(dg, partial=_split_partial(T, W), finish=_finish)
+        ef, tot, fl = Dist.ef_distributed(dg, rows=_split_rows(T, W), listing=_check_listing, finish=_finish)
         np.savez(f"{out_path}.{rank}.npz", ef=ef.numpy(), tot=tot.numpy())
     finally:
         dist.destroy_process_group()

@@ -166,6 +166,41 @@ def test_distributed_parts_bitwise(rmat18, nparts):
         assert torch.equal(x, y)
 
 
+@pytest.mark.parametrize("nparts", [2, 3, 8])
+def test_row_partitioned_parts_bitwise(rmat18, nparts):
+    # the row-partitioned distributed pass emulated on one GPU: every part's
+    # rows phase writes its node range's Adj+ rows into one shared buffer (the
+    # union is what the broadcast exchange assembles on every rank), then each
+    # part lists its units; words summed as the all-reduce would: bitwise equal
+    # to the single-GPU pass
+    import torch
+    from paper_2306_00606_b200 import device as D
+
+    dg = D.DeviceGraph.from_host(rmat18)
+    n = rmat18.n
+    full = [torch.empty(n, dtype=t, device="cuda") for t in (torch.float64, torch.int64, torch.uint8)]
+    D.ef_range(dg, 0, n, *full)
+    bounds = D.part_bounds(dg, nparts)
+    assert bounds[0] == 0 and bounds[-1] == n and np.all(np.diff(bounds) >= 0)
+    adjp = torch.empty(dg.neighbors.numel(), dtype=torch.int32, device="cuda")
+    dplus = torch.empty(n, dtype=torch.int32, device="cuda")
+    words = [torch.empty(D.DIST_WORDS * n, dtype=torch.int64, device="cuda") for _ in range(nparts)]
+    wss = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(nparts)]
+    for p in range(nparts):
+        D.ef_partial_rows(dg, p, nparts, bounds, adjp, dplus, words[p], wss[p])
+    for p in range(nparts):
+        D.ef_partial_tables(dg, p, nparts, bounds, words[p], wss[p])
+    for p in range(nparts):
+        D.ef_partial_list(dg, p, nparts, bounds, adjp, dplus, words[p], wss[p])
+    tot_w = torch.stack(words).sum(0)
+    tot_s = torch.stack(wss).sum(0)
+    out = [torch.empty(n, dtype=t, device="cuda") for t in (torch.float64, torch.int64, torch.uint8)]
+    D.ef_finish(dg, 0, n, tot_w, tot_s, *out)
+    torch.cuda.synchronize()
+    for x, y in zip(full, out):
+        assert torch.equal(x, y)
+
+
 def test_star_beyond_listing_bound():
     # a star with more than 10^6 leaves: maximum degree above the listing's
     # fixed-point bound, so the whole-graph pass takes the per-seed triangle

@@ -70,7 +70,7 @@ def main():
     ws = torch.zeros(n, dtype=torch.float64, device="cuda")
     w, s = torch.empty_like(words), torch.empty_like(ws)
     for p in range(2):
-        D.ef_partial(dg, p, 2, w, s)
+        D.ef_partial(dg, p, 2, w, s)  # self-contained parts (efg_ef_partial)
         words += w
         ws += s
     D.ef_finish(dg, 0, n, words, ws, *out)

@@ -37,7 +37,8 @@ enum { EFG_MODE_CLUSTER_CENTRIC = 0, EFG_MODE_VERTEX_CENTRIC = 1 };
 /* engine: which device algorithm evaluates the per-seed cluster sums.
  *  FACTORIZED -- degree-histogram factorisation + triangle corrections (default)
  *  DIRECT     -- per-seed enumeration of every star and chain (original formulation)
- *  ALG1       -- Algorithm-1 middle-triplet scatter, cross-check */
+ *  ALG1       -- Algorithm-1 middle-triplet scatter, an independent
+ *                cross-check (fp64 W summed by atomics: EF may vary in the last bits) */
 enum { EFG_ENGINE_AUTO = 0, EFG_ENGINE_FACTORIZED = 1, EFG_ENGINE_DIRECT = 2, EFG_ENGINE_ALG1 = 3 };
 
 typedef struct efg_stats {

@@ -24,7 +24,8 @@ MODE_VERTEX_CENTRIC = 1
 ENGINE_AUTO = 0
 ENGINE_FACTORIZED = 1
 ENGINE_DIRECT = 2
-ENGINES = {"auto": ENGINE_AUTO, "factorized": ENGINE_FACTORIZED, "direct": ENGINE_DIRECT}
+ENGINE_ALG1 = 3
+ENGINES = {"auto": ENGINE_AUTO, "factorized": ENGINE_FACTORIZED, "direct": ENGINE_DIRECT, "alg1": ENGINE_ALG1}
 
 # every symbol include/efg.h declares (checked by tests/test_native.py)
 EXPORTED = (

@@ -16,6 +16,7 @@ namespace efg {
 int check_line_factor();
 int check_line_direct();
 int check_line_prep();
+int check_line_alg1();
 thread_local int64_t g_launches = 0;
 thread_local int64_t g_lib_calls = 0;
 thread_local Profiler* g_prof = nullptr;
@@ -98,10 +99,12 @@ int guarded(efg_ctx* ctx, F&& body) {
 #ifdef EFG_BOUNDS_CHECK
     {  // bounds-checked build: any device index check that failed during the call
       EFG_CUDA_CHECK(cudaStreamSynchronize(ctx->c.stream));
-      const int lf = efg::check_line_factor(), ld = efg::check_line_direct(), lp = efg::check_line_prep();
-      if (lf || ld || lp)
+      const int lf = efg::check_line_factor(), ld = efg::check_line_direct(), lp = efg::check_line_prep(),
+                la = efg::check_line_alg1();
+      if (lf || ld || lp || la)
         throw efg::Error(efg::EFG_CUDA, "device bounds check failed: ef_factor.cu:" + std::to_string(lf) +
-                                            " ef_direct.cu:" + std::to_string(ld) + " prep.cu:" + std::to_string(lp));
+                                            " ef_direct.cu:" + std::to_string(ld) + " prep.cu:" + std::to_string(lp) +
+                                            " ef_alg1.cu:" + std::to_string(la));
     }
 #endif
     if (efg::g_prof && !ctx->c.prof.pending.empty()) {
@@ -138,7 +141,7 @@ int resolve_engine(int mode, int engine) {
 // Run one EF pass over device CSR `g` for seeds r; outputs device, index = seed - r.lo.
 void run_engine(Context& c, const efg::CSRView& g, const efg::Staging& stg, efg::SeedRange r, int engine, double* ef,
                 int64_t* tot, uint8_t* fl, int64_t* T, double* W, efg_stats* st) {
-  EFG_REQUIRE(engine == EFG_ENGINE_FACTORIZED || engine == EFG_ENGINE_DIRECT,
+  EFG_REQUIRE(engine == EFG_ENGINE_FACTORIZED || engine == EFG_ENGINE_DIRECT || engine == EFG_ENGINE_ALG1,
               "unknown engine " + std::to_string(engine));
   cudaEvent_t* ev = c.ev;
   efg::PrepInfo info;
@@ -152,7 +155,10 @@ void run_engine(Context& c, const efg::CSRView& g, const efg::Staging& stg, efg:
     if (st) EFG_CUDA_CHECK(cudaEventRecord(ev[2], c.stream));
     efg::prepare(c, g, false, P);
     if (st) EFG_CUDA_CHECK(cudaEventRecord(ev[3], c.stream));
-    efg::ef_direct(c, P, r, ef, tot, fl, T, W, st);
+    if (engine == EFG_ENGINE_ALG1)
+      efg::ef_alg1(c, P, r, ef, tot, fl, T, W, st);
+    else
+      efg::ef_direct(c, P, r, ef, tot, fl, T, W, st);
     info.dmax = P.dmax;
     info.sum_c2 = P.sum_c2;
   }

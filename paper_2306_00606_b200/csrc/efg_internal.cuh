@@ -216,6 +216,10 @@ void ef_finish(Context& ctx, const CSRView& g, SeedRange r, const unsigned long 
 void ef_direct(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* total, uint8_t* flags,
                int64_t* T_out, double* W_out, efg_stats* st);
 
+// ef_alg1.cu -- Algorithm 1 of the paper (middle-triplet scatter), cross-check engine
+void ef_alg1(Context& ctx, Prepared& P, SeedRange r, double* ef, int64_t* total, uint8_t* flags, int64_t* T_out,
+             double* W_out, efg_stats* st);
+
 // K2 -- per-seed work estimates (int64 [n]) used for balanced sharding
 void factorized_work(Context& ctx, Prepared& P, int64_t* d_work);
 void direct_work(Context& ctx, Prepared& P, int64_t* d_work);

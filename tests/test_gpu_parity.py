@@ -155,3 +155,25 @@ def test_device_rmat_edge_cases():
         n, mm, off, nb, orig = OG.build_csr(e)
         assert trunc == t2 and (g.n, g.m) == (n, mm), params
         assert np.array_equal(g.offsets, off) and np.array_equal(g.neighbors, nb), params
+
+
+def test_algorithm1_engine_matches_reference_golden(golden):
+    """K3b: the paper's Algorithm 1 (middle-triplet scatter),
+    the third independent engine: exact mass / T / flags and EF within 1e-9
+    on every reference-run fixture (its fp64 W is summed by atomics, so it is
+    not bitwise reproducible; the tolerance covers that)."""
+    for name, case in golden.items():
+        if case.n == 0:
+            continue
+        g = graph_of(case)
+        r = _run(g, 0, "alg1", None, want_tw=True)
+        assert np.array_equal(r.cluster_total, case.get("cluster_total")), name
+        assert np.array_equal(r.flags, case.get("flags")), name
+        assert ef_close(r.ef, case.get("ef")), (name, float(np.max(np.abs(r.ef - case.get("ef")))))
+        assert r.clusters_processed == case.meta["cluster_count"], name
+    for name in ("ba2000", "rmat_12_8_3", "rmat_14_16_1", "k6"):
+        case = golden[name]
+        r = _run(graph_of(case), 0, "alg1", None, want_tw=True)
+        _, _, _, T, W = O.ef_seeds(case.get("offsets"), case.get("neighbors"), threads=4)
+        assert np.array_equal(r.stats["T"], T), name
+        assert ef_close(r.stats["W"], W, rtol=1e-12, atol=1e-9), name

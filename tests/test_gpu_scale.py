@@ -201,6 +201,17 @@ def test_row_partitioned_parts_bitwise(rmat18, nparts):
         assert torch.equal(x, y)
 
 
+def test_algorithm1_cross_checks_every_seed(rmat18):
+    # three independent decompositions (degree classes + listing, per-seed
+    # walks, the paper's middle-triplet scatter) agree on every seed
+    a = _run(rmat18, 0, "factorized", None, want_tw=True)
+    b = _run(rmat18, 0, "alg1", None, want_tw=True)
+    assert np.array_equal(a.stats["T"], b.stats["T"])
+    assert np.array_equal(a.cluster_total, b.cluster_total)
+    assert np.array_equal(a.flags, b.flags)
+    assert ef_close(a.ef, b.ef)  # the parity bar; alg1's W is an fp64 atomic sum (order varies)
+
+
 def test_star_beyond_listing_bound():
     # a star with more than 10^6 leaves: maximum degree above the listing's
     # fixed-point bound, so the whole-graph pass takes the per-seed triangle

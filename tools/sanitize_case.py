@@ -38,7 +38,7 @@ def check(name, g, engines=("factorized", "direct"), seeds=None):
 def main():
     check("ba2000", efg.build_graph(gen.ba_edges(2000, 3, seed=0)))
     g, _ = efg.generate_rmat(efg.RmatParams(scale=12, avg_degree=8, seed=3))
-    r = check("rmat_12_8_3", g)
+    r = check("rmat_12_8_3", g, engines=("factorized", "direct", "alg1"))
     top = efg.key_nodes(r, frac=0.05)
     assert np.array_equal(top, np.lexsort((np.arange(g.n), -r.ef))[: top.size])
     efg.ef_bins(r, 8)

@@ -1294,6 +1294,7 @@ constexpr int kMidUnroll = 2;
 #endif
 constexpr int kMidUnrollBm = EFG_MID_UNROLL_BM;
 
+
 constexpr int kMidSmallDeg = 256;  // middle vertices of degree <= this run in small CTAs
 
 // CTA shapes of k_mid_block: big (hub tasks and degree > kMidSmallDeg) and
@@ -1930,11 +1931,11 @@ __global__ void k_part_search(const int64_t* __restrict__ prefix, int64_t n, int
     bounds[p] = p == 0 ? 0 : n;
     return;
   }
-  const long double target = (long double)prefix[n - 1] * p / nparts;
+  const double target = (double)prefix[n - 1] * p / nparts;
   int64_t lo = 0, hi = n;  // first v with prefix[v] >= target, cut after it
   while (lo < hi) {
     const int64_t mid = (lo + hi) >> 1;
-    if ((long double)prefix[mid] < target) lo = mid + 1;
+    if ((double)prefix[mid] < target) lo = mid + 1;
     else hi = mid;
   }
   bounds[p] = lo + 1 < n ? lo + 1 : n;
@@ -2245,18 +2246,18 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   int64_t* tstart = nullptr;
   int32_t* hs = nullptr;
   if (nhubs) {
-    if (listing) {
-      hs = P.by_rank;  // hubs in descending degree order: labels [0, nhubs)
-    } else {           // hubs in descending triangle-probe order
+    {  // hubs in descending triangle-probe order (the longest hub tasks start first); a listing
+       // pass takes the hub list from the rank order (labels [0, nhubs) are the hubs)
+      const int32_t* hubs = listing ? P.by_rank : L.hub;
       int64_t* hw = ctx.buf("f_hub_work").as<int64_t>(2 * nhubs + 2);
-      EFG_LAUNCH(k_hub_work, nhubs, 256, 0, s, L.hub, nhubs, g.offsets, g.nbr, P.dplus, hw);
+      EFG_LAUNCH(k_hub_work, nhubs, 256, 0, s, hubs, nhubs, g.offsets, g.nbr, P.dplus, hw);
       int64_t* hw_sorted = hw + nhubs;
       hs = ctx.buf("f_hub_sorted").as<int32_t>(nhubs);
       EFG_CUDA_CHECK(
-          cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, hw, hw_sorted, L.hub, hs, nhubs, 0, 64, s));
+          cub::DeviceRadixSort::SortPairsDescending(nullptr, tmp, hw, hw_sorted, hubs, hs, nhubs, 0, 64, s));
       EFG_REGION("cub::DeviceRadixSort::SortPairsDescending", s,
                  EFG_CUDA_CHECK(cub::DeviceRadixSort::SortPairsDescending(ctx.buf("cub").get(tmp), tmp, hw,
-                                                                          hw_sorted, L.hub, hs, nhubs, 0, 64, s)));
+                                                                          hw_sorted, hubs, hs, nhubs, 0, 64, s)));
     }
     int64_t* hnt = ctx.buf("f_hub_nt").as<int64_t>(nhubs + 1);
     tstart = ctx.buf("f_hub_tstart").as<int64_t>(nhubs + 1);

@@ -707,6 +707,70 @@ k_small_rows(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
   if (lane < d) chain_push(ca, nbr[b + lane], y, val, s1[i]);
 }
 
+// d <= 8 (1.46 M of R-MAT22's 2.18 M rows): the same fused histogram / table /
+// pushes with 8 lanes per row, four rows per warp.  The table values and the
+// stars term are those of k_small_rows bit for bit (same per-output order;
+// the 32-lane reduction tree only adds zeros beyond lane 8).
+__global__ void __launch_bounds__(kSmallWarps * 32)
+k_small_rows8(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
+              const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd, const double* __restrict__ F,
+              const int64_t* __restrict__ s1, ChainAcc ca, int64_t flen) {
+  const int lane = threadIdx.x & 31, g = lane >> 3, t = lane & 7, w = threadIdx.x >> 5;
+  const int64_t q0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 4;
+  if (q0 >= count) return;  // warp-uniform
+  const int64_t q = q0 + g;
+  const bool valid = q < count;
+  const int32_t i = valid ? rows[q] : 0;
+  const int64_t b = valid ? offsets[i] : 0;
+  const int d = valid ? (int)(offsets[i + 1] - b) : 0;
+  const int32_t y = t < d ? nd[b + t] : 0x7fffffff;
+  int32_t x = y;
+#pragma unroll
+  for (int k = 2; k <= 8; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      const int32_t o = __shfl_xor_sync(0xffffffffu, x, j);
+      const bool up = (t & k) == 0;
+      const bool lower = (t & j) == 0;
+      x = (lower == up) ? min(x, o) : max(x, o);
+    }
+  }
+  const int32_t prev = __shfl_up_sync(0xffffffffu, x, 1);
+  const bool head = t < d && (t == 0 || x != prev);
+  const unsigned heads = (__ballot_sync(0xffffffffu, head) >> (8 * g)) & 0xffu;
+  const int D = __popc(heads);
+  __shared__ int2 runs[kSmallWarps][32];
+  if (head) {
+    const unsigned after = heads & ~((2u << t) - 1);
+    const int nxt = after ? __ffs(after) - 1 : d;
+    runs[w][8 * g + __popc(heads & ((1u << t) - 1))] = make_int2(x, nxt - t);
+  }
+  __syncwarp();
+  int32_t key = 0x7fffffff, cntk = 0;
+  if (t < D) {
+    key = runs[w][8 * g + t].x;
+    cntk = runs[w][8 * g + t].y;
+  }
+  const int64_t base = (int64_t)key + d - 4;
+  double c = 0.0;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int32_t xa = __shfl_sync(0xffffffffu, key, 8 * g + a);
+    const int32_t ha = __shfl_sync(0xffffffffu, cntk, 8 * g + a);
+    if (t < D && a < D) c += (double)ha * __ldg(F + EFG_CLAMP(max(base + xa, (int64_t)0), flen));
+  }
+  if (t < D) c -= __ldg(F + EFG_CLAMP(max(base + key, (int64_t)0), flen));
+  double hc = t < D ? (double)cntk * c : 0.0;
+  for (int o = 4; o; o >>= 1) hc += __shfl_xor_sync(0xffffffffu, hc, o);
+  if (t == 0 && valid) ca.ws[i] = hc;
+  int idx = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k)
+    if (__shfl_sync(0xffffffffu, key, 8 * g + k) == y && k < D) idx = k;
+  const double val = __shfl_sync(0xffffffffu, c, 8 * g + idx);
+  if (t < d) chain_push(ca, nbr[b + t], y, val, s1[i]);
+}
+
 // d > 32: CTA per row.  Keys below kPushDirect (most neighbour degrees) are
 // located through a direct-mapped shared table (key -> position; only keys
 // present are ever read, so it needs no clearing), larger ones by binary
@@ -1285,7 +1349,10 @@ constexpr int kMidChunk = 256;     // rows between entry flushes: 32-bit entry w
 // probe-loop unroll (entries per lane per step), measured per loop: bitmap scan with
 // the 8-byte word+prefix entries 4 (k_mid_big 12.05 ms vs 12.39 at 2, r02); k_mid_warp 2
 // (0.85 vs 0.95 ms at 4), bitmap 2 (12.6 vs 13.2 ms), hash 4 in big CTAs, 2 in small
-constexpr int kMidUnroll = 2;
+#ifndef EFG_MID_WARP_UNROLL
+#define EFG_MID_WARP_UNROLL 2
+#endif
+constexpr int kMidUnroll = EFG_MID_WARP_UNROLL;
 #ifndef EFG_MID_UNROLL_BM
 #define EFG_MID_UNROLL_BM 4
 #endif
@@ -1540,15 +1607,24 @@ __device__ __forceinline__ bool above(int32_t dj, int32_t j, int32_t dv, int32_t
 }
 
 // dv <= 32 (labels >= n32): warp per v.  Lane e holds slot e of v's row;
-// Adj+(v) is the set of lanes whose neighbour ranks above v.  A row's hits
-// are distinct entries, so the per-warp entry sums need no atomics.
+// Adj+(v) is the set of lanes whose neighbour ranks above v (a shared hash
+// label -> lane).  The rows (lower-ranked neighbours u) are short here
+// (|Adj+(u)| <= du <= dv <= 32), so they are scanned FLAT: the warp lays all
+// rows' entries end to end (exclusive scan of |Adj+(u)|, each flat position
+// tagged with its row in shared memory) and probes 32 of them per step,
+// whatever row they belong to -- a row-at-a-time scan left most lanes idle
+// (WS-4M: ~10 rows of ~10 entries per seed against 64-lane steps).  Entries
+// at or past v's own label (Adj+(u) is label-sorted) fail the `< rank(v)`
+// test.  u's and w's sums go to shared 32-bit pieces of Q = -P (at most 32
+// hits per row and per entry: no overflow), v's stay in registers.
+constexpr int kMidFlat = 1024;  // 32 rows x 32 entries
 __global__ void __launch_bounds__(kMidWarps * 32)
 k_mid_warp(MArgs a) {
   __shared__ int4 sK[kMidWarps][32];
   __shared__ int8_t sV[kMidWarps][128];
-  __shared__ int64_t sP[kMidWarps][32];
-  __shared__ uint32_t sC[kMidWarps][32];
   __shared__ int32_t sE[kMidWarps][32];  // degree of each slot's neighbour (entries of Adj+(v) among them)
+  __shared__ uint32_t sQ[kMidWarps][6][32];  // per lane: row pieces lo / hi / count, entry pieces lo / hi / count
+  __shared__ int8_t sRow[kMidWarps][kMidFlat];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t r = a.n32 + ((int64_t)blockIdx.x * kMidWarps + w) * a.nparts + a.part;
   if (r >= a.n) return;
@@ -1565,48 +1641,67 @@ k_mid_warp(MArgs a) {
     pu = __ldg(a.dplus + u);
     psu = __ldg(a.offsets + u);  // Adj+(u) starts at u's own row (slot space)
   }
+  if (__ballot_sync(0xffffffffu, up) == 0) return;  // Adj+(v) empty: no triangle has v in the middle
   sK[w][lane] = make_int4(-1, -1, -1, -1);
-  sP[w][lane] = 0;
-  sC[w][lane] = 0;
   sE[w][lane] = du;
+#pragma unroll
+  for (int k = 0; k < 6; ++k) sQ[w][k][lane] = 0;
+  // flat layout of the rows' entries
+  const int32_t len = lane < dv && !up && pu >= 2 ? pu : 0;
+  int32_t incl = len;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const int32_t st = incl - len, total = __shfl_sync(0xffffffffu, incl, 31);
+  for (int32_t p = 0; p < len; ++p) sRow[w][EFG_CLAMP(st + p, kMidFlat)] = (int8_t)lane;
   __syncwarp();
   if (up) smap_insert(sK[w], sV[w], 5, __ldg(a.rank_of + u), lane);
   __syncwarp();
+  const uint32_t qb = (uint32_t)__cvta_generic_to_shared(&sQ[w][0][0]);
+  const int32_t lim = (int32_t)r;
   Acc2 av;
-  unsigned todo = __ballot_sync(0xffffffffu, lane < dv && !up && pu >= 2);
-  if (__ballot_sync(0xffffffffu, up) == 0) todo = 0;  // Adj+(v) empty: no triangle has v in the middle
-  while (todo) {
-    const int x = __ffs(todo) - 1;
-    todo &= todo - 1;
-    const int32_t ux = __shfl_sync(0xffffffffu, u, x);
-    const int32_t pux = __shfl_sync(0xffffffffu, pu, x);
-    const int64_t psx = __shfl_sync(0xffffffffu, psu, x);
-    const int32_t s0 = dv + __shfl_sync(0xffffffffu, du, x);
-    int64_t rs = 0;
-    uint32_t rc = 0;
-    mid_scan<kMidUnroll>(
-        a, psx, pux, (int32_t)r, s0, lane, [&](int32_t key) { return smap_find(sK[w], sV[w], 5, key); },
-        [&](int32_t y, int32_t) { return sE[w][y]; },
-        [&](int32_t y, int32_t, int64_t g) {
-          rs += g;
-          ++rc;
-          sP[w][y] += g;
-          sC[w][y] += 1;
-        });
-    rc = warp_count(rc);
-    if (rc) {
-      rs = warp_sum64(rs);
-      av.add_row(rs, rc);
-      if (lane == 0) red_node(a.acc, ux, rs, rc);
+  for (int32_t f0 = 0; f0 < total; f0 += 32) {
+    const int32_t f = f0 + lane;
+    const bool valid = f < total;
+    const int32_t rr = valid ? (int32_t)sRow[w][f] : 0;
+    const int32_t st_r = __shfl_sync(0xffffffffu, st, rr);
+    const int64_t ps_r = __shfl_sync(0xffffffffu, psu, rr);
+    const int32_t s0_r = dv + __shfl_sync(0xffffffffu, du, rr);
+    const int32_t j = valid ? __ldg(a.adjj + ps_r + (f - st_r)) : INT32_MAX;
+    const int32_t y = j < lim ? smap_find(sK[w], sV[w], 5, j) : -1;
+    if (y >= 0) {
+      const int64_t g = __ldg(a.PT + EFG_CLAMP(s0_r + sE[w][y], a.flen));
+      av.add_row(g, 1);
+      const uint64_t Q = (uint64_t)(-g);
+      const uint32_t lo = (uint32_t)(Q & 0x3fffff), hi = (uint32_t)(Q >> 22);
+      reds_add(qb + 4u * (0 * 32 + rr), lo);  // u's share (row rr)
+      reds_add(qb + 4u * (1 * 32 + rr), hi);
+      reds_add(qb + 4u * (2 * 32 + rr), 1u);
+      reds_add(qb + 4u * (3 * 32 + y), lo);   // w's share (entry y)
+      reds_add(qb + 4u * (4 * 32 + y), hi);
+      reds_add(qb + 4u * (5 * 32 + y), 1u);
     }
-    __syncwarp();
   }
-  if (up && sC[w][lane]) red_node(a.acc, u, sP[w][lane], sC[w][lane]);
-  if (lane == 0 && av.c) {
+  __syncwarp();
+  if (lane < dv) {
+    if (sQ[w][2][lane]) {  // a row: u's share
+      const uint64_t Q = ((uint64_t)sQ[w][1][lane] << 22) + sQ[w][0][lane];
+      red_node(a.acc, u, -(int64_t)Q, sQ[w][2][lane]);
+    }
+    if (sQ[w][5][lane]) {  // an entry of Adj+(v): w's share
+      const uint64_t Q = ((uint64_t)sQ[w][4][lane] << 22) + sQ[w][3][lane];
+      red_node(a.acc, u, -(int64_t)Q, sQ[w][5][lane]);
+    }
+  }
+  const int64_t vh = warp_sum(av.hi), vl = warp_sum(av.lo);
+  const uint32_t vc = warp_count(av.c);
+  if (lane == 0 && vc) {
     unsigned long long* q = a.acc + 4 * (int64_t)v;
-    atomicAdd(q, (unsigned long long)av.hi);
-    atomicAdd(q + 1, (unsigned long long)av.lo);
-    atomicAdd(q + 2, (unsigned long long)av.c);
+    atomicAdd(q, (unsigned long long)vh);
+    atomicAdd(q + 1, (unsigned long long)vl);
+    atomicAdd(q + 2, (unsigned long long)vc);
   }
 }
 
@@ -1965,15 +2060,15 @@ void part_bounds(Context& ctx, const CSRView& g, int32_t nparts, int64_t* bounds
 
 // Class lists by degree (all known before any histogram is built).
 struct Lists {
-  int32_t *hw, *hs, *hb, *hl;     // histogram rows: d <= 32, <= 256, <= 2048, > 2048 (all nodes)
+  int32_t *hw8, *hw, *hs, *hb, *hl;  // histogram rows: d <= 8, <= 32, <= 256, <= 2048, > 2048 (all nodes)
   int32_t *cg, *cb;               // chain tables: d <= 64, > 64 (all nodes)
   int32_t *trs, *tr1, *tr2, *tr3, *hub;  // triangles
 };
 enum Slot {
-  kHW, kHS, kHB, kHL, kCG, kCB, kTrS, kTr1, kTr2, kTr3, kHubs, kNTasks, kNSlots
+  kHW8, kHW, kHS, kHB, kHL, kCG, kCB, kTrS, kTr1, kTr2, kTr3, kHubs, kNTasks, kNSlots
 };
 // per-chunk counts of the node-class lists (histograms, chain tables): class
-// c in [kHW, kCB], chunk k -> kNSlots + c * kMaxChunks + k
+// c in [kHW8, kCB], chunk k -> kNSlots + c * kMaxChunks + k
 constexpr int kNCounts = kNSlots + (kCB + 1) * kMaxChunks;
 __host__ __device__ constexpr int cslot(int c, int k) { return kNSlots + c * kMaxChunks + k; }
 constexpr int64_t kHistWarpMax = 32, kHistBlockMax = kHistThreads * kHistItems, kCtabGroupMax = 64;
@@ -1990,6 +2085,7 @@ static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, See
   const int64_t* off = P.g.offsets;
   Lists L{};
   if (row_lists) {
+  L.hw8 = list("f_l_hw8", n);
   L.hw = list("f_l_hw", n);
   L.hs = list("f_l_hs", n);
   L.hb = list("f_l_hb", n);
@@ -2001,7 +2097,8 @@ static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, See
   for (int k = 0; k < stg.nchunks; ++k) {
     const SeedRange ch{stg.row[k], stg.row[k + 1]};
     const int64_t o = stg.row[k];
-    select_seeds(ctx, ch, DegRange{off, -1, kHistWarpMax}, L.hw + o, cdev + cslot(kHW, k));
+    select_seeds(ctx, ch, DegRange{off, -1, 8}, L.hw8 + o, cdev + cslot(kHW8, k));
+    select_seeds(ctx, ch, DegRange{off, 8, kHistWarpMax}, L.hw + o, cdev + cslot(kHW, k));
     select_seeds(ctx, ch, DegRange{off, kHistWarpMax, 256}, L.hs + o, cdev + cslot(kHS, k));
     select_seeds(ctx, ch, DegRange{off, 256, kHistBlockMax}, L.hb + o, cdev + cslot(kHB, k));
     select_seeds(ctx, ch, DegRange{off, kHistBlockMax, INT64_MAX}, L.hl + o, cdev + cslot(kHL, k));
@@ -2032,7 +2129,11 @@ static void build_histograms(Context& ctx, const Prepared& P, const Lists& L, co
   const int64_t* off = P.g.offsets;
   const int64_t o = stg.row[k];
   const int64_t nw = c[cslot(kHW, k)], ns = c[cslot(kHS, k)], nb = c[cslot(kHB, k)], nl = c[cslot(kHL, k)];
-  if (small_rows) EFG_LAUNCH(k_hist_warp, ceil_div(nw * 32, B), B, 0, s, L.hw + o, nw, off, P.nd, hkey, hcnt, dcnt);
+  if (small_rows) {
+    const int64_t nw8 = c[cslot(kHW8, k)];
+    EFG_LAUNCH(k_hist_warp, ceil_div(nw8 * 32, B), B, 0, s, L.hw8 + o, nw8, off, P.nd, hkey, hcnt, dcnt);
+    EFG_LAUNCH(k_hist_warp, ceil_div(nw * 32, B), B, 0, s, L.hw + o, nw, off, P.nd, hkey, hcnt, dcnt);
+  }
   int bits = 1;
   while (bits < 31 && (int64_t(1) << bits) <= (int64_t)P.dmax + 1) ++bits;
   EFG_LAUNCH(k_hist_warp8, ceil_div(ns * 32, kHistW8Warps * 32), kHistW8Warps * 32, 0, s, L.hs + o, ns, off, P.nd,
@@ -2153,7 +2254,10 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
       if (!tables) continue;
       build_histograms(ctx, P, L, c, rows, k, hkey, hcnt, dcnt, false);
       // rows with d <= 32: histogram, chain table and pushes fused in registers
-      const int64_t nsm = c[cslot(kHW, k)];
+      // (d <= 8: four rows per warp)
+      const int64_t nsm8 = c[cslot(kHW8, k)], nsm = c[cslot(kHW, k)];
+      EFG_LAUNCH(k_small_rows8, ceil_div(ceil_div(nsm8, 4), kSmallWarps), kSmallWarps * 32, 0, s,
+                 L.hw8 + rows.row[k], nsm8, g.offsets, g.nbr, P.nd, P.ftab, P.s1, ca, P.ftab_len);
       EFG_LAUNCH(k_small_rows, ceil_div(nsm, kSmallWarps), kSmallWarps * 32, 0, s, L.hw + rows.row[k], nsm,
                  g.offsets, g.nbr, P.nd, P.deg, P.ftab, P.s1, ca, P.ftab_len);
       // chain tables C_i(y): rows with 32 < d <= 64 by 8-lane groups, the rest by CTAs

@@ -143,21 +143,14 @@ __device__ __forceinline__ void row_sums_big(const int64_t* __restrict__ offsets
   }
 }
 
-__global__ void __launch_bounds__(kRowThreads) k_row_sums(
-    const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr, int32_t* __restrict__ nd,
-    const int32_t* __restrict__ deg, int64_t r0, int64_t r1, int64_t* __restrict__ s1, int64_t* __restrict__ s2, int32_t* __restrict__ dplus,
-    const int32_t* __restrict__ rank_of, int32_t* __restrict__ adjj, int32_t* __restrict__ adjd,
-    const int32_t* __restrict__ by_rank, const int32_t* __restrict__ deg_by_rank, int64_t n, int32_t nbig) {
-  if ((int32_t)blockIdx.x < nbig) {
-    row_sums_big(offsets, nbr, nd, deg, r0, r1, s1, s2, dplus, rank_of, adjj, adjd, by_rank, deg_by_rank, n, nbig);
-    return;
-  }
-  const int lane = threadIdx.x & 31;
-  int64_t v = r0 + (((blockIdx.x - nbig) * (int64_t)blockDim.x + threadIdx.x) >> 5);
-  if (v >= r1) return;
+// One row by the whole warp: neighbour degrees, S1 / S2, Adj+ (slot space).
+__device__ __forceinline__ void row_sums_warp(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
+                                              int32_t* __restrict__ nd, const int32_t* __restrict__ deg, int64_t v,
+                                              int64_t* __restrict__ s1, int64_t* __restrict__ s2,
+                                              int32_t* __restrict__ dplus, const int32_t* __restrict__ rank_of,
+                                              int32_t* __restrict__ adjj, int32_t* __restrict__ adjd, int lane) {
   int64_t b = offsets[v], e = offsets[v + 1];
   int32_t dv = (int32_t)(e - b);
-  if (nbig > 0 && dv > kRowBig) return;  // a hub: one of the first nbig CTAs has it
   int64_t s = 0, q = 0;
   int64_t out = b;
   if (dv <= 32) {  // most rows: one group, no unrolled predicated tail
@@ -225,6 +218,59 @@ __global__ void __launch_bounds__(kRowThreads) k_row_sums(
     s1[v] = s;
     s2[v] = q;
     dplus[v] = (int32_t)(out - b);
+  }
+}
+
+// Rows [r0, r1): four consecutive rows per warp.  A quad whose rows all have
+// degree <= 8 (most rows of a skewed graph: 1.46 M of R-MAT22's 2.18 M) is
+// done by 8-lane groups in one step; other quads take their rows one after
+// another with the whole warp.  Rows of degree > kRowBig belong to the first
+// nbig CTAs (row_sums_big).
+__global__ void __launch_bounds__(kRowThreads) k_row_sums(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr, int32_t* __restrict__ nd,
+    const int32_t* __restrict__ deg, int64_t r0, int64_t r1, int64_t* __restrict__ s1, int64_t* __restrict__ s2, int32_t* __restrict__ dplus,
+    const int32_t* __restrict__ rank_of, int32_t* __restrict__ adjj, int32_t* __restrict__ adjd,
+    const int32_t* __restrict__ by_rank, const int32_t* __restrict__ deg_by_rank, int64_t n, int32_t nbig) {
+  if ((int32_t)blockIdx.x < nbig) {
+    row_sums_big(offsets, nbr, nd, deg, r0, r1, s1, s2, dplus, rank_of, adjj, adjd, by_rank, deg_by_rank, n, nbig);
+    return;
+  }
+  const int lane = threadIdx.x & 31;
+  const int64_t v0 = r0 + 4 * (((blockIdx.x - nbig) * (int64_t)blockDim.x + threadIdx.x) >> 5);
+  if (v0 >= r1) return;
+  const int g = lane >> 3, t = lane & 7;
+  const int64_t vg = v0 + g;
+  const bool valid = vg < r1;
+  const int64_t bg = valid ? offsets[vg] : 0;
+  const int32_t dg = valid ? (int32_t)(offsets[vg + 1] - bg) : 0;
+  if (__all_sync(0xffffffffu, dg <= 8)) {
+    const bool in = t < dg;
+    const int32_t j = in ? nbr[bg + t] : 0, dj = in ? __ldg(deg + j) : 0;
+    const int32_t lab = in && adjj ? __ldg(rank_of + j) : 0;
+    if (in) nd[bg + t] = dj;
+    const bool take = in && ranks_above(dj, j, dg, (int32_t)vg);
+    int64_t sg = dj, qg = (int64_t)dj * dj;
+    for (int o = 4; o; o >>= 1) {  // within the 8-lane group
+      sg += __shfl_xor_sync(0xffffffffu, sg, o);
+      qg += __shfl_xor_sync(0xffffffffu, qg, o);
+    }
+    const unsigned gm = (__ballot_sync(0xffffffffu, take) >> (8 * g)) & 0xffu;
+    if (take && adjj) {
+      const int64_t o = EFG_CLAMP(bg + __popc(gm & ((1u << t) - 1)), bg + dg);
+      adjj[o] = lab;
+      adjd[o] = dj;
+    }
+    if (t == 0 && valid) {
+      s1[vg] = sg;
+      s2[vg] = qg;
+      dplus[vg] = __popc(gm);
+    }
+    return;
+  }
+  for (int k = 0; k < 4 && v0 + k < r1; ++k) {
+    const int64_t v = v0 + k;
+    if (nbig > 0 && offsets[v + 1] - offsets[v] > kRowBig) continue;  // a hub: one of the first nbig CTAs has it
+    row_sums_warp(offsets, nbr, nd, deg, v, s1, s2, dplus, rank_of, adjj, adjd, lane);
   }
 }
 
@@ -420,7 +466,8 @@ void prepare_rows(Context& ctx, Prepared& P, int64_t r0, int64_t r1, int64_t, in
   cudaStream_t s = ctx.stream;
   if (!P.dplus) P.dplus = ctx.buf("dplus").as<int32_t>(P.g.n > 0 ? P.g.n : 1);  // (or the caller's buffer)
   const int32_t nbig = P.rank_of ? kRowBigBlocks : 0;  // hub CTAs need the rank order
-  EFG_LAUNCH(k_row_sums, nbig + ceil_div((r1 - r0) * 32, kRowThreads), kRowThreads, 0, s, P.g.offsets, P.g.nbr, P.nd,
+  EFG_LAUNCH(k_row_sums, nbig + ceil_div(ceil_div(r1 - r0, 4) * 32, kRowThreads), kRowThreads, 0, s, P.g.offsets,
+             P.g.nbr, P.nd,
              P.deg, r0, r1, P.s1, P.s2, P.dplus, P.rank_of, P.rank_of ? P.adjj : nullptr, P.adjd, P.by_rank, P.deg_by_rank,
              P.g.n, nbig);
 }

@@ -1387,7 +1387,9 @@ constexpr int kMidLgNB = 9;
 constexpr int kMidMaxP = 1024;      // longer Adj+(v) are processed in parts of this size
 constexpr int kMidChunk = 256;     // rows between entry flushes: 32-bit entry words cannot overflow
 // probe-loop unroll (entries per lane per step), measured per loop: bitmap scan with
-// the 8-byte word+prefix entries 4 (k_mid_big 12.05 ms vs 12.39 at 2, r02); k_mid_warp 2
+// the 8-byte word+prefix entries 4 for long rows, 2 / 1 for rows whose scan is at most
+// 64 / 32 entries (k_mid_big 12.25 -> 11.80 ms; peeking at labels 31 / 63 of longer
+// rows to shorten their step measured slower: 12.38), r02; k_mid_warp 2
 // (0.85 vs 0.95 ms at 4), bitmap 2 (12.6 vs 13.2 ms), hash 4 in big CTAs, 2 in small
 #ifndef EFG_MID_WARP_UNROLL
 #define EFG_MID_WARP_UNROLL 2
@@ -1400,6 +1402,11 @@ constexpr int kMidUnroll = EFG_MID_WARP_UNROLL;
 #define EFG_MID_BIG_MINB 5
 #endif
 constexpr int kMidUnrollBm = EFG_MID_UNROLL_BM;
+#ifndef EFG_MID_ADAPT_U
+#define EFG_MID_ADAPT_U 1
+#endif
+constexpr bool kMidAdaptU = EFG_MID_ADAPT_U;
+
 
 
 constexpr int kMidSmallDeg = 256;  // middle vertices of degree <= this run in small CTAs
@@ -1897,8 +1904,19 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
           reds_add(eb_c + 4 * y, 1u);
         };
         // the map kind is block-uniform: one loop per kind, no branch in the probe
-        if (use_bm)
+        // the unroll follows the row: the scan covers at most min(|Adj+(u)|, lim) entries
+        // (distinct labels below lim), so short scans take one step of 32 / 64 lanes
+        // instead of a 128-lane step
+        const int32_t span = min(pu, lim);
+        if (use_bm && kMidAdaptU && span <= 32)
+          mid_scan_bm<1>(a.adjj + psu, pu, lim, a.PT, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
+        else if (use_bm && kMidAdaptU && span <= 64)
+          mid_scan_bm<2>(a.adjj + psu, pu, lim, a.PT, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
+        else if (use_bm)
           mid_scan_bm<kMidUnrollBm>(a.adjj + psu, pu, lim, a.PT, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
+        else if (kMidAdaptU && span <= 32)
+          mid_scan<1, true>(a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); },
+                            degree, hit);
         else
           mid_scan<C::kUnrollHash, true>(
               a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); }, degree, hit);

@@ -1649,6 +1649,17 @@ __device__ __forceinline__ int32_t mfind(uint32_t kb, uint32_t vb, uint32_t lg, 
   return k >= 0 ? lds_s16(vb + 2 * (4 * b + k)) : -1;
 }
 
+// first position of a label-sorted Adj+ row (length pu) holding a label >= lim
+__device__ __forceinline__ int32_t row_lower_bound(const int32_t* __restrict__ row, int32_t pu, int32_t lim) {
+  int32_t lo = 0, hi = pu;
+  while (lo < hi) {
+    const int32_t mid = (lo + hi) >> 1;
+    if (__ldg(row + mid) < lim) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
 __device__ __forceinline__ bool above(int32_t dj, int32_t j, int32_t dv, int32_t v) {
   return dj > dv || (dj == dv && j > v);
 }
@@ -1665,6 +1676,10 @@ __device__ __forceinline__ bool above(int32_t dj, int32_t j, int32_t dv, int32_t
 // test.  u's and w's sums go to shared 32-bit pieces of Q = -P (at most 32
 // hits per row and per entry: no overflow), v's stay in registers.
 constexpr int kMidFlat = 1024;  // 32 rows x 32 entries
+#ifndef EFG_MID_WARP_EXACT
+#define EFG_MID_WARP_EXACT 1
+#endif
+constexpr bool kMidWarpExact = EFG_MID_WARP_EXACT;
 __global__ void __launch_bounds__(kMidWarps * 32)
 k_mid_warp(MArgs a) {
   __shared__ int4 sK[kMidWarps][32];
@@ -1693,8 +1708,11 @@ k_mid_warp(MArgs a) {
   sE[w][lane] = du;
 #pragma unroll
   for (int k = 0; k < 6; ++k) sQ[w][k][lane] = 0;
-  // flat layout of the rows' entries
-  const int32_t len = lane < dv && !up && pu >= 2 ? pu : 0;
+  // flat layout of the rows' entries: each row up to v's own label (Adj+(u) is
+  // label-sorted; a binary search per lane, rows in parallel, halves the flat
+  // length against scanning whole rows)
+  int32_t len = 0;
+  if (lane < dv && !up && pu >= 2) len = kMidWarpExact ? row_lower_bound(a.adjj + psu, pu, (int32_t)r) : pu;
   int32_t incl = len;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {

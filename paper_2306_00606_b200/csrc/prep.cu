@@ -362,7 +362,41 @@ __device__ __forceinline__ void sort_one(int64_t b, int pv, int lane, const int3
   __syncwarp();
 }
 
-// Rows of 2..256 entries of nodes [r0, r1): a warp per group of 32 nodes sorts the group's rows.
+// A row of 2..16 entries sorted by ONE thread in registers (a 16-input bitonic
+// network, padding sorts last): most Adj+ rows are this short (low-degree
+// nodes have few higher-ranked neighbours), and a warp-wide sort per such row
+// left most lanes idle.
+__device__ __forceinline__ void sort_row_thread16(int32_t* __restrict__ row, int32_t* __restrict__ rowd, int p,
+                                                  const int32_t* __restrict__ deg_by_rank) {
+  uint32_t x[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) x[i] = i < p ? (uint32_t)row[i] : 0xffffffffu;
+#pragma unroll
+  for (int k = 2; k <= 16; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const uint32_t lo = min(x[i], x[l]), hi = max(x[i], x[l]);
+          const bool up = (i & k) == 0;
+          x[i] = up ? lo : hi;
+          x[l] = up ? hi : lo;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    if (i < p) {
+      row[i] = (int32_t)x[i];
+      rowd[i] = __ldg(deg_by_rank + x[i]);
+    }
+}
+
+// Rows of 2..256 entries of nodes [r0, r1): rows of <= 16 entries a thread each,
+// the longer ones a warp each (per group of 32 nodes).
 __global__ void k_sort_small(const int64_t* __restrict__ offsets, const int32_t* __restrict__ dplus, int64_t r0, int64_t r1,
                              const int32_t* __restrict__ deg_by_rank, int32_t* __restrict__ adjj,
                              int32_t* __restrict__ adjd, int32_t* __restrict__ scratch) {
@@ -372,7 +406,11 @@ __global__ void k_sort_small(const int64_t* __restrict__ offsets, const int32_t*
     const int64_t mine = r0 + g * 32 + lane;
     int p = 0;
     if (mine < r1) p = dplus[mine];
-    unsigned todo = __ballot_sync(0xffffffffu, p >= 2 && p <= 256);
+    if (p >= 2 && p <= 16) {
+      const int64_t b = offsets[mine];
+      sort_row_thread16(adjj + b, adjd + b, p, deg_by_rank);
+    }
+    unsigned todo = __ballot_sync(0xffffffffu, p > 16 && p <= 256);
     while (todo) {
       const int x = __ffs(todo) - 1;
       todo &= todo - 1;

@@ -267,6 +267,50 @@ __global__ void __launch_bounds__(kRowThreads) k_row_sums(
     }
     return;
   }
+  if (__all_sync(0xffffffffu, dg <= 32)) {
+    // all four rows fit one 32-lane step: lane e takes slot e of every row, the four
+    // rows' loads and gathers issued together (one row after another was four
+    // dependent load chains per warp)
+    int64_t bk[4];
+    int32_t dk[4], jk[4], djk[4], labk[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      bk[k] = __shfl_sync(0xffffffffu, bg, 8 * k);
+      dk[k] = __shfl_sync(0xffffffffu, dg, 8 * k);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) jk[k] = lane < dk[k] ? nbr[bk[k] + lane] : 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const bool in = lane < dk[k];
+      djk[k] = in ? __ldg(deg + jk[k]) : 0;
+      labk[k] = in && adjj ? __ldg(rank_of + jk[k]) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t v = v0 + k;
+      const bool in = lane < dk[k];
+      if (in) nd[bk[k] + lane] = djk[k];
+      const bool take = in && ranks_above(djk[k], jk[k], dk[k], (int32_t)v);
+      const unsigned mask = __ballot_sync(0xffffffffu, take);
+      if (take && adjj) {
+        const int64_t o = EFG_CLAMP(bk[k] + __popc(mask & ((1u << lane) - 1)), bk[k] + dk[k]);
+        adjj[o] = labk[k];
+        adjd[o] = djk[k];
+      }
+      int64_t sv = djk[k], qv = (int64_t)djk[k] * djk[k];
+      for (int o = 16; o; o >>= 1) {
+        sv += __shfl_xor_sync(0xffffffffu, sv, o);
+        qv += __shfl_xor_sync(0xffffffffu, qv, o);
+      }
+      if (lane == k && v < r1) {
+        s1[v] = sv;
+        s2[v] = qv;
+        dplus[v] = __popc(mask);
+      }
+    }
+    return;
+  }
   for (int k = 0; k < 4 && v0 + k < r1; ++k) {
     const int64_t v = v0 + k;
     if (nbig > 0 && offsets[v + 1] - offsets[v] > kRowBig) continue;  // a hub: one of the first nbig CTAs has it

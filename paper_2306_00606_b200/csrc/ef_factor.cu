@@ -1389,12 +1389,8 @@ constexpr int kMidChunk = 256;     // rows between entry flushes: 32-bit entry w
 // probe-loop unroll (entries per lane per step), measured per loop: bitmap scan with
 // the 8-byte word+prefix entries 4 for long rows, 2 / 1 for rows whose scan is at most
 // 64 / 32 entries (k_mid_big 12.25 -> 11.80 ms; peeking at labels 31 / 63 of longer
-// rows to shorten their step measured slower: 12.38), r02; k_mid_warp 2
-// (0.85 vs 0.95 ms at 4), bitmap 2 (12.6 vs 13.2 ms), hash 4 in big CTAs, 2 in small
-#ifndef EFG_MID_WARP_UNROLL
-#define EFG_MID_WARP_UNROLL 2
-#endif
-constexpr int kMidUnroll = EFG_MID_WARP_UNROLL;
+// rows to shorten their step measured slower: 12.38), r02; hash 4 in big CTAs, 2 in
+// small (1 for scans of at most 32 entries)
 #ifndef EFG_MID_UNROLL_BM
 #define EFG_MID_UNROLL_BM 4
 #endif

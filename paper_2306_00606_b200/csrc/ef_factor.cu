@@ -347,11 +347,13 @@ template <int G>
 __global__ void k_ctab_group(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
                              const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey,
                              const int32_t* __restrict__ hcnt, const int32_t* __restrict__ deg,
-                             const double* __restrict__ F, double* __restrict__ ctab, int64_t flen) {
+                             const double* __restrict__ F, double* __restrict__ ctab, int64_t flen,
+                             int max_d = 0x7fffffff) {
   const int sub = threadIdx.x & (G - 1);
   int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / G;
   if (q >= count) return;
   const int32_t i = rows[q];
+  if (dcnt[i] > max_d) return;  // k_ctab_block's
   int64_t b = offsets[i], e = b + dcnt[i];
   int32_t di = deg[i];
   for (int64_t o = b + sub; o < e; o += G) {
@@ -385,6 +387,11 @@ constexpr int kCtabStage = 1024;
 constexpr int kCtabThreads = 128;
 constexpr int kCtabOut = 4;
 constexpr int kExpK = 15, kExpTiles = 64, kExpGrid = 128, kExpMin = 12, kExpMinD = 128;
+#ifndef EFG_CTAB_WARP_D
+#define EFG_CTAB_WARP_D 128
+#endif
+constexpr int kCtabWarpD = EFG_CTAB_WARP_D;  // rows with fewer distinct degrees: a warp each (<= kExpMinD, <= 128)
+static_assert(kCtabWarpD <= 128 && kCtabWarpD <= kExpMinD, "k_ctab_warp stages at most 128 inputs, unexpanded");
 constexpr double kExpRatio = 0.135;
 constexpr float kExpGrowth = 1.25f;  // tile t: x in [base (g^t - 1), base (g^(t+1) - 1))
 
@@ -404,6 +411,58 @@ __device__ __forceinline__ void ctab_outputs(const int32_t* __restrict__ sx, con
   }
 }
 
+// Rows of degree > 64 with fewer than kCtabWarpD distinct neighbour degrees
+// (half of k_ctab_block's rows at R-MAT22, 4.5 % of its terms): a warp each.
+// The inputs (x, h) are staged in the warp's shared slice once, each lane
+// carries up to 4 outputs (y = its own + 32, + 64, + 96) and every staged pair
+// feeds their F gathers -- the same fma sequence per output as k_ctab_block's
+// direct path (inputs in ascending order), so the values are identical.
+constexpr int kCtabWarps = 8;
+__global__ void __launch_bounds__(kCtabWarps * 32)
+k_ctab_warp(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
+            const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey, const int32_t* __restrict__ hcnt,
+            const int32_t* __restrict__ deg, const double* __restrict__ F, double* __restrict__ ctab, int64_t flen,
+            int max_d) {
+  __shared__ int32_t sx[kCtabWarps][128];
+  __shared__ double sh[kCtabWarps][128];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (q >= count) return;
+  const int32_t i = rows[q];
+  const int D = dcnt[i];
+  if (D > max_d) return;  // k_ctab_block's
+  const int64_t b = offsets[i];
+  const int32_t di = deg[i];
+  for (int a = lane; a < D; a += 32) {
+    sx[w][a] = hkey[b + a];
+    sh[w][a] = (double)hcnt[b + a];
+  }
+  __syncwarp();
+  int64_t base[4];
+  int32_t yk[4];
+  double acc[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int o = lane + 32 * k;
+    yk[k] = o < D ? sx[w][o] : sx[w][0];  // past-the-end outputs shadow the first one
+    base[k] = (int64_t)yk[k] + di - 4;
+    acc[k] = 0.0;
+  }
+  const int K = (D + 31) >> 5;  // warp-uniform
+  for (int a = 0; a < D; ++a) {
+    const int32_t x = sx[w][a];
+    const double h = sh[w][a];
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (k < K) acc[k] = fma(h, __ldg(F + EFG_CLAMP(base[k] + x, flen)), acc[k]);
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int o = lane + 32 * k;
+    if (o < D) ctab[b + o] = acc[k] - __ldg(F + EFG_CLAMP(base[k] + yk[k], flen));
+  }
+}
+
 // tile of input x (fast single precision: a boundary off by one only moves a
 // member to a neighbouring tile, and every expanded tile's ratio is checked)
 __device__ __forceinline__ int exp_tile(int32_t x, float inv_base, float inv_lg) {
@@ -417,7 +476,7 @@ __global__ void __launch_bounds__(kCtabThreads, EFG_CTAB_MINB)
 k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __restrict__ offsets,
              const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey, const int32_t* __restrict__ hcnt,
              const int32_t* __restrict__ deg, const double* __restrict__ F, double* __restrict__ ctab,
-             int exp_min, int exp_min_d, int64_t flen) {
+             int exp_min, int exp_min_d, int64_t flen, int min_d = 0) {
   __shared__ int32_t sx[kCtabStage];
   __shared__ double sh[kCtabStage];
   __shared__ int32_t tbeg[kExpGrid], tend[kExpGrid];
@@ -431,6 +490,7 @@ k_ctab_block(const int32_t* __restrict__ rows, int64_t nrows, const int64_t* __r
   const int32_t i = rows[r];
   const int64_t b = offsets[i];
   const int D = dcnt[i];
+  if (D < min_d) return;  // a warp's row (k_ctab_group<32>)
   const int32_t di = deg[i];
   constexpr int T = kCtabThreads;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -2336,8 +2396,13 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
       const int64_t o = rows.row[k], ng = c[cslot(kCG, k)], nb = c[cslot(kCB, k)];
       EFG_LAUNCH(k_ctab_group<8>, ceil_div(ng * 8, B), B, 0, s, L.cg + o, ng, g.offsets, dcnt, hkey, hcnt, P.deg,
                  P.ftab, ctab, P.ftab_len);
+      // rows of degree > 64: fewer than kCtabWarpD distinct neighbour degrees (half of them,
+      // no far-field expansion) a warp each, the rest a CTA each
       EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab,
-                 ctab, kExpMin, kExpMinD, P.ftab_len);
+                 ctab, kExpMin, kExpMinD, P.ftab_len, kCtabWarpD);
+      if (kCtabWarpD > 0)
+        EFG_LAUNCH(k_ctab_warp, ceil_div(nb, kCtabWarps), kCtabWarps * 32, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey,
+                   hcnt, P.deg, P.ftab, ctab, P.ftab_len, kCtabWarpD - 1);
       // chains pushed from the rows whose tables are now complete
       const int64_t ps1 = c[cslot(kHS, k)], pb = c[cslot(kHB, k)], pl = c[cslot(kHL, k)];
       EFG_LAUNCH(k_push_warp256, ceil_div(ps1, kPushWarps), kPushWarps * 32, 0, s, L.hs + o, ps1, g.offsets, g.nbr,

@@ -47,6 +47,7 @@ struct FArgs {
   const double* F;
   const double* G;         // G[S] = F(S-6) - F(S-4): triangle correction per unit weight
   const int64_t* PT;       // P[S] = rint(G[S] 2^40): triangle sums are exact integers (any order, any path)
+  const uint64_t* PQ;      // Q = -P (the block listing's table)
   int64_t flen;            // F / G / PT table length (bounds-checked builds)
   const int32_t* pc;       // [2m] |Adj+(nbr[e])|
   const int32_t* adjj;     // oriented adjacency Adj+ as rank labels
@@ -908,7 +909,8 @@ k_push_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
 }
 
 // 32 < d <= 256: warp per row, H_i's keys (<= 256) in the warp's shared slice,
-// binary search per slot.
+// binary search per slot.  (Also taking the 256 < d <= 2048 rows with <= 256
+// distinct neighbour degrees measured neutral, r02.)
 constexpr int kPushWarps = 8, kPushWarpKeys = 256;
 __global__ void __launch_bounds__(kPushWarps * 32)
 k_push_warp256(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
@@ -1494,6 +1496,7 @@ struct MArgs {
   const int32_t* by_rank;
   const int32_t* deg_by_rank;
   const int64_t* PT;        // fixed-point G
+  const uint64_t* PQ;       // Q = -P >= 0 (G < 0 on every reachable S): the block listing's table
   int64_t flen;             // PT length (bounds-checked builds)
   unsigned long long* acc;  // [4 n] per node: (hi, lo, count, pad)
   int64_t n, n32;           // labels < n32: degree > 32
@@ -1503,9 +1506,13 @@ struct MArgs {
   int64_t label0;           // first label of the launch's label units
 };
 
-__global__ void k_gfix(const double* __restrict__ G, int64_t len, int64_t* __restrict__ PT) {
+__global__ void k_gfix(const double* __restrict__ G, int64_t len, int64_t* __restrict__ PT, uint64_t* __restrict__ PQ) {
   const int64_t S = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (S < len) PT[S] = (int64_t)rint(ldexp(G[S], kListScale));
+  if (S < len) {
+    const int64_t p = (int64_t)rint(ldexp(G[S], kListScale));
+    PT[S] = p;
+    PQ[S] = (uint64_t)(-p);
+  }
 }
 
 // one partial sum (|s| < 2^63) and its triangle count into a node's words
@@ -1562,7 +1569,7 @@ __device__ __forceinline__ void smap_insert(int4* keys, V* vals, uint32_t lg, in
 }
 
 // Scan of one row Adj+(u)[lane::32] in phases of kUnroll entries (labels +
-// degrees, then membership, then the G gathers), calling hit(y, label, P)
+// degrees, then membership, then the G gathers), calling hit(y, label, Q = -P)
 // for every w found in Adj+(v) (y = its position there).
 template <int U, bool BF = false, class Find, class Deg, class Hit>
 __device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu, int32_t lim, int32_t s0, int lane,
@@ -1570,10 +1577,10 @@ __device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu
   // Adj+(u) is sorted by label and only labels < lim = rank(v) can lie in
   // Adj+(v): the scan stops at the first entry >= lim (i.e. at v itself)
   const int32_t* __restrict__ row = a.adjj + psu;
-  const int64_t* __restrict__ pt = a.PT + s0;
+  const uint64_t* __restrict__ pt = a.PQ + s0;
   for (int32_t p0 = 0; p0 < pu; p0 += 32 * U) {
     int32_t j[U], d[U], y[U];
-    int64_t g[U];
+    uint64_t g[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const int32_t p = p0 + lane + 32 * k;
@@ -1652,38 +1659,41 @@ __device__ __forceinline__ void reds_add(uint32_t addr, uint32_t v) {
 }
 
 // The bitmap form of mid_scan (labels < lim <= 32 kBmWords): a running row
-// pointer and the row's G-table base stay in registers; one 8-byte shared
+// pointer and the row's Q-table base stay in registers; one 8-byte shared
 // load per entry gives membership and, with a popcount, the position in
-// Adj+(v); w's degree (shared) and the G gather are predicated on the hit.
+// Adj+(v).  Branch-free up to the hit: the key is clamped to lim (the bitmap
+// holds a zero word at lim >> 5 whose prefix is |part|, and lim is never a
+// member), so every lane's position is a valid index and w's degree is read
+// unpredicated; only the Q gather and the hit are predicated.  The row is
+// label-sorted, so the scan is past lim exactly when some lane's last entry is.
 template <int U, class Hit>
 __device__ __forceinline__ void mid_scan_bm(const int32_t* __restrict__ row, int32_t pu, int32_t lim,
-                                            const int64_t* __restrict__ PT, uint32_t s0, uint32_t bmb, uint32_t db,
+                                            const uint64_t* __restrict__ PQ, uint32_t s0, uint32_t bmb, uint32_t db,
                                             int lane, Hit hit, int64_t flen = 0) {
   const int32_t* __restrict__ rp = row + lane;
   for (int32_t q = lane; q - lane < pu; q += 32 * U, rp += 32 * U) {
     int32_t j[U], y[U];
-    int64_t g[U];
+    bool h[U];
+    uint64_t g[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) j[k] = q + 32 * k < pu ? __ldg(rp + 32 * k) : INT32_MAX;
-    bool past = false;
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      const bool in = j[k] < lim;
-      past |= !in;
-      const uint32_t key = in ? (uint32_t)j[k] : 0u;
+      const uint32_t key = (uint32_t)min(j[k], lim);
       const uint2 wp = lds64(bmb + 8u * (key >> 5));
-      const uint32_t bit = 1u << (key & 31);
-      y[k] = (in && (wp.x & bit)) ? (int32_t)(wp.y + __popc(wp.x & (bit - 1))) : -1;
+      const uint32_t bit = __funnelshift_l(0u, 1u, key);  // 1 << (key & 31): the wrapping shift, no mask
+      h[k] = (wp.x & bit) != 0u;
+      y[k] = (int32_t)(wp.y + __popc(wp.x & (bit - 1)));
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      const uint32_t d = (uint32_t)lds32(db + 4u * (uint32_t)max(y[k], 0));
-      g[k] = y[k] >= 0 ? __ldg(PT + EFG_CLAMP(s0 + d, flen)) : 0;
+      const uint32_t S = s0 + (uint32_t)lds32(db + 4u * (uint32_t)y[k]);  // 32-bit index: one wide multiply-add
+      g[k] = h[k] ? __ldg(PQ + EFG_CLAMP(S, flen)) : 0ull;
     }
 #pragma unroll
     for (int k = 0; k < U; ++k)
-      if (y[k] >= 0) hit(y[k], j[k], g[k]);
-    if (__any_sync(0xffffffffu, past)) break;
+      if (h[k]) hit(y[k], j[k], g[k]);
+    if (__any_sync(0xffffffffu, j[U - 1] >= lim)) break;
   }
 }
 
@@ -1841,11 +1851,11 @@ struct MidSmem {
       int4 lk[C::kNB];
       int16_t lv[4 * C::kNB];
     };
-    uint2 bmp[C::kBmWords > 0 ? C::kBmWords : 1];  // {bitmap word, popcount of the words before it}
+    uint2 bmp[C::kBmWords + 1];  // {bitmap word, popcount of the words before it}; + the zero word at lim >> 5
   };
   int64_t rps[C::kChunk];  // compacted rows of the current chunk: Adj+(u) start,
   int32_t ru[C::kChunk], rdu[C::kChunk], rpu[C::kChunk];  // u, du, |Adj+(u)|
-  int32_t node[C::kMaxP], edeg[C::kMaxP];
+  int32_t node[C::kMaxP], edeg[C::kMaxP + 1];  // edeg[np]: read (unused) by the bitmap scan's misses
   uint32_t elo[C::kMaxP], ehi[C::kMaxP], ec[C::kMaxP];
   int32_t nrows;
   int32_t wtot[C::kThreads / 32];
@@ -1894,6 +1904,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
     __syncthreads();
     if (use_bm) {
       for (int b = threadIdx.x; b < nbw; b += blockDim.x) sm.bmp[b] = make_uint2(0u, 0u);
+      if (threadIdx.x == 0) sm.bmp[nbw] = make_uint2(0u, (uint32_t)np);  // the word of key lim: no member, prefix |part|
     } else {
       for (int b = threadIdx.x; b < (1 << lgl); b += blockDim.x) sm.lk[b] = make_int4(-1, -1, -1, -1);
     }
@@ -1966,13 +1977,12 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
       for (int32_t x = w; x < nr; x += NW) {
         const int32_t u = sm.ru[x], du = sm.rdu[x], pu = sm.rpu[x];
         const int64_t psu = sm.rps[x];
-        int64_t rs = 0;
+        uint64_t rq = 0;  // the lane's sum of Q = -P over the row's hits
         uint32_t rc = 0;
         const auto degree = [&](int32_t y, int32_t) { return lds32(db + 4 * y); };
-        const auto hit = [&](int32_t y, int32_t, int64_t g) {
-          rs += g;
+        const auto hit = [&](int32_t y, int32_t, uint64_t q) {
+          rq += q;
           ++rc;
-          const uint64_t q = (uint64_t)(-g);
           reds_add(eb_lo + 4 * y, (uint32_t)(q & 0x3fffff));
           reds_add(eb_hi + 4 * y, (uint32_t)(q >> 22));
           reds_add(eb_c + 4 * y, 1u);
@@ -1983,11 +1993,11 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
         // instead of a 128-lane step
         const int32_t span = min(pu, lim);
         if (use_bm && kMidAdaptU && span <= 32)
-          mid_scan_bm<1>(a.adjj + psu, pu, lim, a.PT, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
+          mid_scan_bm<1>(a.adjj + psu, pu, lim, a.PQ, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
         else if (use_bm && kMidAdaptU && span <= 64)
-          mid_scan_bm<2>(a.adjj + psu, pu, lim, a.PT, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
+          mid_scan_bm<2>(a.adjj + psu, pu, lim, a.PQ, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
         else if (use_bm)
-          mid_scan_bm<kMidUnrollBm>(a.adjj + psu, pu, lim, a.PT, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
+          mid_scan_bm<kMidUnrollBm>(a.adjj + psu, pu, lim, a.PQ, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
         else if (kMidAdaptU && span <= 32)
           mid_scan<1, true>(a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); },
                             degree, hit);
@@ -1996,7 +2006,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
               a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); }, degree, hit);
         rc = warp_count(rc);
         if (rc) {
-          rs = warp_sum64(rs);
+          const int64_t rs = -warp_sum64((int64_t)rq);  // the row's sum of P (|lane sums| < 2^57)
           if (lane == 0) {
             red_node(a.acc, u, rs, rc);
             av.add_row(rs, rc);
@@ -2477,8 +2487,10 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
   a.Wtl = ctx.buf("f_Wtl").as<int64_t>(cnt > 0 ? cnt : 1);
   {
     int64_t* PT = ctx.buf("l_pt").as<int64_t>(P.ftab_len);
-    EFG_LAUNCH(k_gfix, ceil_div(P.ftab_len, B), B, 0, s, P.gtab, P.ftab_len, PT);
+    uint64_t* PQ = ctx.buf("l_pq").as<uint64_t>(P.ftab_len);
+    EFG_LAUNCH(k_gfix, ceil_div(P.ftab_len, B), B, 0, s, P.gtab, P.ftab_len, PT, PQ);
     a.PT = PT;
+    a.PQ = PQ;
   }
   // 2. triangles: listed once each for whole-graph passes, else per seed (the long kernels first)
   const int64_t nhubs = c[kHubs], ntasks = c[kNTasks];
@@ -2530,6 +2542,7 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     ma.by_rank = P.by_rank;
     ma.deg_by_rank = P.deg_by_rank;
     ma.PT = a.PT;
+    ma.PQ = a.PQ;
     ma.flen = P.ftab_len;
     ma.acc = acc;
     ma.n = n;

@@ -599,7 +599,11 @@ def main():
         return ef_cluster_centric_distributed(graph)
 
     def e2e_time(graph, steps):
-        e2e_run(graph)
+        # warm-up as the timed loop runs: the previous result is alive during the
+        # next call, so two sets of recycled page-locked output blocks circulate
+        keep = e2e_run(graph)
+        keep = (keep, e2e_run(graph))
+        del keep
         times = []
         for _ in range(steps):
             flush.fill_(1)

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -405,17 +406,27 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
     h2d(d_off, offsets, (n + 1) * sizeof(int64_t), stage_off);
     EFG_CUDA_CHECK(cudaEventRecord(c.chunk_ev[0], c.copy_stream));
     efg::Staging stg;
-    // Two chunks (measured at R-MAT22: 1: 51.8, 2: 50.6, 4: 52.7, 8: 58.7 ms e2e at
-    // equal sizes -- splitting kernels costs launch tails), the first one small:
-    // the engine starts once it lands and its rows (low ids: the heavy hubs in
-    // skewed graphs) keep the GPU busy while the rest copies.  First-chunk share
-    // measured: 50 %: 45.6, 25 %: 44.2, 15 %: 43.6, 10 %: 44.0, 5 %: 44.8 ms e2e; after the
-    // chain-table expansion (32.7 ms pass): 10 %: 37.7, 15 %: 37.3, 25 %: 37.0, 35 %: 37.4;
-    // three chunks (15/50, 25/60 %): 38.0, 38.4.
-    stg.nchunks = m2 >= (int64_t(1) << 22) ? 2 : 1;
-    const int first_pct = 25;
+    // Chunks growing from a small first one: the engine starts once it lands,
+    // and the per-row work of each chunk (orientation, sorts, histograms,
+    // tables, pushes: slower per slot than the copy) covers the next chunk's
+    // copy.  Measured at R-MAT22 (pass 23.3 ms, H2D 6.7 ms), e2e pinned ms:
+    // 1 chunk 29.9; 25 %: 28.3; 10/25/45: 26.9; 10/23/41/65: 27.0;
+    // 12/28/50/79: 26.8; 15/30/55/80: 26.6; 20/40/65: 26.1; 18/38/62: 25.9;
+    // 15/40/70: 26.0; 15/35/62: 25.85 (tools/ab_stage.sh, r02).
+    // chunk k's slots end at split[k] % of 2m (cumulative; the last chunk ends at 100 %)
+    int split[efg::kMaxChunks] = {15, 35, 62};
+    stg.nchunks = m2 >= (int64_t(1) << 22) ? 4 : 1;
+    if (const char* e = getenv("EFG_STAGE_SPLITS")) {  // tuning override (tools/ab_stage.sh): "10,25,45"
+      int k = 0;
+      for (const char* q = e; *q && k < efg::kMaxChunks - 1; ++k) {
+        split[k] = std::max(1, std::min(99, atoi(q)));
+        while (*q && *q != ',') ++q;
+        if (*q == ',') ++q;
+      }
+      if (m2 >= (int64_t(1) << 22)) stg.nchunks = k + 1;
+    }
     for (int k = 0; k <= stg.nchunks; ++k) {
-      const int64_t target = k == 0 ? 0 : k == stg.nchunks ? m2 : m2 * first_pct / 100;
+      const int64_t target = k == 0 ? 0 : k == stg.nchunks ? m2 : m2 * split[k - 1] / 100;
       stg.row[k] = k == stg.nchunks ? n : std::lower_bound(offsets, offsets + n + 1, target) - offsets;
       if (k > 0 && stg.row[k] < stg.row[k - 1]) stg.row[k] = stg.row[k - 1];
       stg.slot[k] = offsets[stg.row[k]];

@@ -27,6 +27,8 @@
 //   mass = dv(dv-1) + S1(v) - dv          (test_expected_force.py:139-147)
 // All sums run in a fixed order per seed (no atomics on values), so results
 // are bitwise reproducible and independent of sharding.
+#include <cstdlib>
+
 #include <cub/cub.cuh>
 
 #include "common.cuh"
@@ -1498,6 +1500,7 @@ struct MArgs {
   const int64_t* PT;        // fixed-point G
   const uint64_t* PQ;       // Q = -P >= 0 (G < 0 on every reachable S): the block listing's table
   int64_t flen;             // PT length (bounds-checked builds)
+  int32_t bm_lim;           // label bitmap for parts with lim <= this (else the hash; EFG_MID_BM_LIMIT, tests)
   unsigned long long* acc;  // [4 n] per node: (hi, lo, count, pad)
   int64_t n, n32;           // labels < n32: degree > 32
   int64_t nhubs, ntasks;    // labels < nhubs come as ntasks row-range tasks
@@ -1566,56 +1569,6 @@ __device__ __forceinline__ void smap_insert(int4* keys, V* vals, uint32_t lg, in
         vals[4 * b + k] = (V)val;
         return;
       }
-}
-
-// Scan of one row Adj+(u)[lane::32] in phases of kUnroll entries (labels +
-// degrees, then membership, then the G gathers), calling hit(y, label, Q = -P)
-// for every w found in Adj+(v) (y = its position there).
-template <int U, bool BF = false, class Find, class Deg, class Hit>
-__device__ __forceinline__ void mid_scan(const MArgs& a, int64_t psu, int32_t pu, int32_t lim, int32_t s0, int lane,
-                                         Find find, Deg degree, Hit hit) {
-  // Adj+(u) is sorted by label and only labels < lim = rank(v) can lie in
-  // Adj+(v): the scan stops at the first entry >= lim (i.e. at v itself)
-  const int32_t* __restrict__ row = a.adjj + psu;
-  const uint64_t* __restrict__ pt = a.PQ + s0;
-  for (int32_t p0 = 0; p0 < pu; p0 += 32 * U) {
-    int32_t j[U], d[U], y[U];
-    uint64_t g[U];
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int32_t p = p0 + lane + 32 * k;
-      j[k] = p < pu ? __ldg(row + p) : INT32_MAX;
-    }
-    bool past = false;
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const bool in = j[k] < lim;
-      past |= !in;
-      if (BF) {  // branch-free (cheap constant-time maps): every lane looks up a valid key, misses selected away
-        const int32_t yy = find(in ? j[k] : 0);
-        y[k] = in ? yy : -1;
-      } else {
-        y[k] = in ? find(j[k]) : -1;
-      }
-    }
-    // only hits need w's degree: looked up by its position in Adj+(v) (4 B streamed per probe instead of 8)
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      if (BF) {
-        const int32_t dd = degree(y[k] >= 0 ? y[k] : 0, j[k]);
-        d[k] = y[k] >= 0 ? dd : 0;
-      } else {
-        d[k] = y[k] >= 0 ? degree(y[k], j[k]) : 0;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k)
-      g[k] = y[k] >= 0 ? __ldg(pt + EFG_CLAMP((uint32_t)d[k], a.flen - s0)) : 0;  // 32-bit index off a row base
-#pragma unroll
-    for (int k = 0; k < U; ++k)
-      if (y[k] >= 0) hit(y[k], j[k], g[k]);
-    if (__any_sync(0xffffffffu, past)) break;
-  }
 }
 
 // Warp sums on the native reduction unit (REDUX): a 32-bit count directly,
@@ -1697,22 +1650,57 @@ __device__ __forceinline__ void mid_scan_bm(const int32_t* __restrict__ row, int
   }
 }
 
-// position of key in the shared map (keys at kb: NB = 2^lg buckets of 4; int16
-// positions at vb), or -1
-__device__ __forceinline__ int32_t mfind(uint32_t kb, uint32_t vb, uint32_t lg, int32_t key) {
-  uint32_t b = ((uint32_t)key * 2654435761u) >> (32 - lg);
-  int4 q = lds128(kb + 16 * b);
-  int k = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
-  if (k < 0 && q.w != -1) {  // first bucket full (rare at load <= 1/4): continue the probe sequence
-    const uint32_t mask = (1u << lg) - 1;
-    while (true) {
-      b = (b + 1) & mask;
-      q = lds128(kb + 16 * b);
-      k = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
-      if (k >= 0 || q.w == -1) break;
-    }
+// The hash form of the scan (Adj+(v) parts whose labels reach past the
+// bitmap): a bucketed map label -> packed entry (position | degree << 10) at
+// NB = 2^lg buckets of 4 keys (kb) and 4 values (pvb), load <= 1/4.  One
+// 16-byte load answers the common case; a bucket that is full and misses
+// continues the linear probe (rare).  Labels >= lim are never members, so no
+// clamp; a miss reads the value of slot 0 (unused) and only the Q gather and
+// the hit are predicated, as in mid_scan_bm.
+constexpr int kPosBits = 10;  // entry positions < kMidMaxP = 1024
+__device__ __forceinline__ int32_t mslot_slow(uint32_t kb, uint32_t lg, uint32_t b, int32_t key) {
+  const uint32_t mask = (1u << lg) - 1;
+  while (true) {
+    b = (b + 1) & mask;
+    const int4 q = lds128(kb + 16 * b);
+    const int k = q.x == key ? 0 : q.y == key ? 1 : q.z == key ? 2 : q.w == key ? 3 : -1;
+    if (k >= 0) return (int32_t)(4 * b + k);
+    if (q.w == -1) return -1;
   }
-  return k >= 0 ? lds_s16(vb + 2 * (4 * b + k)) : -1;
+}
+template <int U, class Hit>
+__device__ __forceinline__ void mid_scan_hash(const int32_t* __restrict__ row, int32_t pu, int32_t lim,
+                                              const uint64_t* __restrict__ PQ, uint32_t s0, uint32_t kb, uint32_t pvb,
+                                              uint32_t lg, int lane, Hit hit, int64_t flen = 0) {
+  const int32_t* __restrict__ rp = row + lane;
+  for (int32_t q = lane; q - lane < pu; q += 32 * U, rp += 32 * U) {
+    int32_t j[U], fs[U];
+    uint64_t g[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) j[k] = q + 32 * k < pu ? __ldg(rp + 32 * k) : INT32_MAX;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int32_t key = j[k];
+      const uint32_t b = ((uint32_t)key * 2654435761u) >> (32 - lg);
+      const int4 e = lds128(kb + 16 * b);
+      // at most one key of the bucket matches: the slot as a sum of selects (no branches)
+      const bool m0 = e.x == key, m1 = e.y == key, m2 = e.z == key, m3 = e.w == key;
+      const int32_t sl = (int32_t)(4 * b) + (m1 ? 1 : 0) + (m2 ? 2 : 0) + (m3 ? 3 : 0);
+      fs[k] = (m0 | m1 | m2 | m3) ? sl : -1;
+      if (fs[k] < 0 && e.w != -1) fs[k] = mslot_slow(kb, lg, b, key);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const uint32_t pv = (uint32_t)lds32(pvb + 4u * (uint32_t)max(fs[k], 0));
+      fs[k] = fs[k] >= 0 ? (int32_t)(pv & ((1u << kPosBits) - 1)) : -1;
+      const uint32_t S = s0 + (pv >> kPosBits);
+      g[k] = fs[k] >= 0 ? __ldg(PQ + EFG_CLAMP(S, flen)) : 0ull;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k)
+      if (fs[k] >= 0) hit(fs[k], j[k], g[k]);
+    if (__any_sync(0xffffffffu, j[U - 1] >= lim)) break;
+  }
 }
 
 // first position of a label-sorted Adj+ row (length pu) holding a label >= lim
@@ -1849,7 +1837,7 @@ struct MidSmem {
   union {
     struct {
       int4 lk[C::kNB];
-      int16_t lv[4 * C::kNB];
+      uint32_t lv[4 * C::kNB];  // packed entry: position | degree << kPosBits
     };
     uint2 bmp[C::kBmWords + 1];  // {bitmap word, popcount of the words before it}; + the zero word at lim >> 5
   };
@@ -1899,7 +1887,8 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
     const int32_t np = min(pv - q0, kMidMaxP);
     const int32_t lim = q0 + np < pv ? __ldg(a.adjj + pb + q0 + np) : labv;
     const uint32_t lgl = min(32u - __clz(max(np, 2) - 1), (uint32_t)kMidLgNB);  // NB = min(2^lgl >= np, kMidNB)
-    const bool use_bm = C::kBmWords > 0 && lim <= 32 * C::kBmWords;              // block-uniform
+    (void)EFG_DCHECK(np <= (1 << kPosBits));
+    const bool use_bm = C::kBmWords > 0 && lim <= 32 * C::kBmWords && lim <= a.bm_lim;  // block-uniform
     const int nbw = use_bm ? (lim + 31) >> 5 : 0;
     __syncthreads();
     if (use_bm) {
@@ -1912,9 +1901,10 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
     for (int t = threadIdx.x; t < np; t += blockDim.x) {
       const int32_t l = __ldg(a.adjj + pb + q0 + t);
       if (use_bm) atomicOr(&sm.bmp[l >> 5].x, 1u << (l & 31));
-      else smap_insert(sm.lk, sm.lv, lgl, l, t);
+      const int32_t dl = __ldg(a.deg_by_rank + l);
+      if (!use_bm) smap_insert(sm.lk, sm.lv, lgl, l, t | (dl << kPosBits));
       sm.node[t] = __ldg(a.by_rank + l);
-      sm.edeg[t] = __ldg(a.deg_by_rank + l);
+      sm.edeg[t] = dl;
       sm.elo[t] = 0;
       sm.ehi[t] = 0;
       sm.ec[t] = 0;
@@ -1979,7 +1969,6 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
         const int64_t psu = sm.rps[x];
         uint64_t rq = 0;  // the lane's sum of Q = -P over the row's hits
         uint32_t rc = 0;
-        const auto degree = [&](int32_t y, int32_t) { return lds32(db + 4 * y); };
         const auto hit = [&](int32_t y, int32_t, uint64_t q) {
           rq += q;
           ++rc;
@@ -1999,11 +1988,10 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
         else if (use_bm)
           mid_scan_bm<kMidUnrollBm>(a.adjj + psu, pu, lim, a.PQ, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
         else if (kMidAdaptU && span <= 32)
-          mid_scan<1, true>(a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); },
-                            degree, hit);
+          mid_scan_hash<1>(a.adjj + psu, pu, lim, a.PQ, (uint32_t)(dv + du), kb, vb, lgl, lane, hit, a.flen);
         else
-          mid_scan<C::kUnrollHash, true>(
-              a, psu, pu, lim, dv + du, lane, [&](int32_t key) { return mfind(kb, vb, lgl, key); }, degree, hit);
+          mid_scan_hash<C::kUnrollHash>(a.adjj + psu, pu, lim, a.PQ, (uint32_t)(dv + du), kb, vb, lgl, lane, hit,
+                                        a.flen);
         rc = warp_count(rc);
         if (rc) {
           const int64_t rs = -warp_sum64((int64_t)rq);  // the row's sum of P (|lane sums| < 2^57)
@@ -2544,6 +2532,8 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
     ma.PT = a.PT;
     ma.PQ = a.PQ;
     ma.flen = P.ftab_len;
+    ma.bm_lim = INT32_MAX;
+    if (const char* e = getenv("EFG_MID_BM_LIMIT")) ma.bm_lim = atoi(e);  // tests: the hash path on every part
     ma.acc = acc;
     ma.n = n;
     ma.n32 = c[kTr1] + c[kTr2] + c[kTr3] + c[kHubs];  // whole-graph pass: nodes of degree > 32

@@ -119,6 +119,21 @@ def test_dense_core_listing_parts(dense_core):
     assert ef_close(res_f.ef[seeds], ef)
 
 
+@pytest.mark.parametrize("graph", ["rmat18", "dense_core"])
+def test_listing_hash_map_matches_bitmap(graph, request, monkeypatch):
+    # Adj+(v) parts whose labels reach past the bitmap (lim > 65536: graphs with
+    # that many nodes of degree > 256) take the hash form of the listing scan;
+    # EFG_MID_BM_LIMIT=0 forces it on every part: the fixed-point sums are
+    # exact, so the results are bitwise those of the bitmap scan
+    g = request.getfixturevalue(graph)
+    base = _run(g, 0, "factorized", None, want_tw=True)
+    monkeypatch.setenv("EFG_MID_BM_LIMIT", "0")
+    hashed = _run(g, 0, "factorized", None, want_tw=True)
+    assert np.array_equal(base.stats["T"], hashed.stats["T"])
+    assert np.array_equal(base.stats["W"], hashed.stats["W"])
+    assert np.array_equal(base.ef, hashed.ef) and np.array_equal(base.cluster_total, hashed.cluster_total)
+
+
 def test_dense_core_shards_bitwise(dense_core):
     # whole-graph passes list triangles, shards run the per-seed path: both sum
     # the same exact fixed-point values, so the results are bitwise identical

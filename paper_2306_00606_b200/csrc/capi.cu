@@ -414,16 +414,22 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
     // 12/28/50/79: 26.8; 15/30/55/80: 26.6; 20/40/65: 26.1; 18/38/62: 25.9;
     // 15/40/70: 26.0; 15/35/62: 25.85 (tools/ab_stage.sh, r02).
     // chunk k's slots end at split[k] % of 2m (cumulative; the last chunk ends at 100 %)
+    // Smaller inputs (ER-1M, Chung-Lu 2^20: ~70 MB, 1.3 ms of copy) pay more in
+    // per-chunk launches than they overlap: two chunks, the first 40 % (ER-1M e2e
+    // ms: 1 chunk 3.28, 25 %: 3.20, 40 %: 3.06-3.11, 15/35/62: 3.59; Chung-Lu:
+    // 5.91, 6.00, 6.11, 6.52).
     int split[efg::kMaxChunks] = {15, 35, 62};
-    stg.nchunks = m2 >= (int64_t(1) << 22) ? 4 : 1;
-    if (const char* e = getenv("EFG_STAGE_SPLITS")) {  // tuning override (tools/ab_stage.sh): "10,25,45"
+    stg.nchunks = m2 >= (int64_t(1) << 25) ? 4 : m2 >= (int64_t(1) << 22) ? 2 : 1;
+    if (stg.nchunks == 2) split[0] = 40;
+    if (const char* e = getenv("EFG_STAGE_SPLITS")) {  // tuning override (tools/ab_stage.sh): "10,25,45" / "none"
       int k = 0;
+      if (!strcmp(e, "none")) e = "";
       for (const char* q = e; *q && k < efg::kMaxChunks - 1; ++k) {
         split[k] = std::max(1, std::min(99, atoi(q)));
         while (*q && *q != ',') ++q;
         if (*q == ',') ++q;
       }
-      if (m2 >= (int64_t(1) << 22)) stg.nchunks = k + 1;
+      stg.nchunks = k + 1;
     }
     for (int k = 0; k <= stg.nchunks; ++k) {
       const int64_t target = k == 0 ? 0 : k == stg.nchunks ? m2 : m2 * split[k - 1] / 100;

@@ -3,7 +3,7 @@
 mkdir -p gpurun_out
 for rep in 1 2; do
   for cfg in "$@"; do
-    EFG_STAGE_SPLITS=$cfg python bench.py --steps 3 --warmup 3 --no-cpu-baseline \
+    EFG_STAGE_SPLITS=$cfg python bench.py --config ${CONFIG:-rmat22} --steps 3 --warmup 3 --no-cpu-baseline \
       --e2e-steps 10 > gpurun_out/ab_stage.log 2>&1 || tail -5 gpurun_out/ab_stage.log
     python - "$cfg" <<'P'
 import json, sys

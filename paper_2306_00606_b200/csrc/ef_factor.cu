@@ -1448,7 +1448,10 @@ constexpr int kMidWarps = 8;
 constexpr int kMidThreads = 256;
 constexpr int kMidNB = 512;         // shared map of Adj+(v): <= 1024 keys at load <= 1/2
 constexpr int kMidLgNB = 9;
-constexpr int kMidMaxP = 1024;      // longer Adj+(v) are processed in parts of this size
+#ifndef EFG_MID_MAXP
+#define EFG_MID_MAXP 1024
+#endif
+constexpr int kMidMaxP = EFG_MID_MAXP;  // longer Adj+(v) are processed in parts of this size
 constexpr int kMidChunk = 256;     // rows between entry flushes: 32-bit entry words cannot overflow
 // probe-loop unroll (entries per lane per step), measured per loop: bitmap scan with
 // the 8-byte word+prefix entries 4 for long rows, 2 / 1 for rows whose scan is at most

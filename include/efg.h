@@ -179,6 +179,10 @@ EFG_API int efg_ef_bins(efg_ctx *ctx, const double *ef, int64_t n, int64_t k, do
 EFG_API int efg_profile_enable(efg_ctx *ctx, int32_t on);
 EFG_API int efg_profile_reset(efg_ctx *ctx);
 EFG_API int efg_profile_report(efg_ctx *ctx, char *buf, int64_t cap);
+/* The last profiled call's records in issue order as JSON
+ * [["name", start_ms, ms], ...], start relative to the call's first record
+ * (host->device copies of efg_expected_force appear as "h2d"). */
+EFG_API int efg_profile_timeline(efg_ctx *ctx, char *buf, int64_t cap);
 
 /* Host-side row formatter of write_ef_csv (expected_force.py:123-130): for
  * i in [0, n) appends "<orig_ids[i]>,<ef[i] as %.9g>,<cluster_total[i]>\n"

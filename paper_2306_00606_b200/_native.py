@@ -36,7 +36,7 @@ EXPORTED = (
     "efg_ef_finish",
     "efg_topk",
     "efg_topk_device", "efg_rank_ascending", "efg_ef_bins", "efg_host_alloc", "efg_host_free", "efg_profile_enable", "efg_profile_reset",
-    "efg_profile_report", "efg_rmat_build", "efg_format_ef_csv",
+    "efg_profile_report", "efg_profile_timeline", "efg_rmat_build", "efg_format_ef_csv",
 )
 
 
@@ -118,6 +118,7 @@ def lib():
             "efg_profile_enable": ([p, i32], ctypes.c_int),
             "efg_profile_reset": ([p], ctypes.c_int),
             "efg_profile_report": ([p, ctypes.c_char_p, i64], ctypes.c_int),
+            "efg_profile_timeline": ([p, ctypes.c_char_p, i64], ctypes.c_int),
             "efg_rmat_build": ([p, i32, i64, p, p, p, P(i32), P(i64), P(i64)], ctypes.c_int),
             "efg_format_ef_csv": ([p, p, p, i64, i32, p, i64, P(i64)], ctypes.c_int),
         }
@@ -169,6 +170,14 @@ class Context:
         buf = ctypes.create_string_buffer(1 << 16)
         check(lib().efg_profile_report(self.handle, buf, len(buf)))
         return {k: {"ms": v[0], "launches": int(v[1])} for k, v in json.loads(buf.value.decode()).items()}
+
+    def profile_timeline(self) -> list:
+        """[(name, start_ms, ms)] of the last profiled call, in issue order."""
+        import json
+
+        buf = ctypes.create_string_buffer(1 << 20)
+        check(lib().efg_profile_timeline(self.handle, buf, len(buf)))
+        return [tuple(x) for x in json.loads(buf.value.decode())]
 
 
 _contexts: dict[int, Context] = {}

@@ -32,12 +32,15 @@ cudaEvent_t Profiler::take() {
 }
 
 void Profiler::resolve() {
+  timeline.clear();
   for (auto& r : pending) {
-    float ms = 0.f;
+    float ms = 0.f, t0 = 0.f;
     EFG_CUDA_CHECK(cudaEventElapsedTime(&ms, r.a, r.b));
+    EFG_CUDA_CHECK(cudaEventElapsedTime(&t0, pending.front().a, r.a));
     auto& t = totals[r.name];
     t.first += ms;
     t.second += 1;
+    timeline.push_back({r.name, t0, ms});
   }
   pending.clear();
   used = 0;
@@ -401,7 +404,8 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
       if (staged)
         c.stager.add(c.copy_stream, dst, src, bytes);
       else
-        EFG_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c.copy_stream));
+        EFG_REGION("h2d", c.copy_stream,
+                   EFG_CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c.copy_stream)));
     };
     h2d(d_off, offsets, (n + 1) * sizeof(int64_t), stage_off);
     EFG_CUDA_CHECK(cudaEventRecord(c.chunk_ev[0], c.copy_stream));
@@ -444,7 +448,9 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
       stg.ready[k] = c.chunk_ev[1 + k];
     }
     EFG_CUDA_CHECK(cudaEventRecord(ev[1], c.copy_stream));  // all inputs resident
-    c.stager.start((int)std::max(1u, std::thread::hardware_concurrency() / 2));
+    int workers = (int)std::max(1u, std::thread::hardware_concurrency() / 2);
+    if (const char* e = getenv("EFG_STAGE_WORKERS")) workers = std::max(1, atoi(e));  // tuning (tools/ab_env.sh)
+    c.stager.start(workers);
     EFG_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.chunk_ev[0], 0));
     double* d_ef = c.buf("o_ef").as<double>(n);
     int64_t* d_tot = c.buf("o_tot").as<int64_t>(n);
@@ -455,7 +461,7 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
     c.total_sent = false;
     run_engine(c, g, stg, efg::SeedRange{0, n}, eng, d_ef, d_tot, d_fl, d_T, d_W, st);
     EFG_CUDA_CHECK(cudaEventRecord(ev[5], c.stream));
-    EFG_CUDA_CHECK(cudaMemcpyAsync(ef, d_ef, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    EFG_REGION("d2h", c.stream, EFG_CUDA_CHECK(cudaMemcpyAsync(ef, d_ef, n * sizeof(double), cudaMemcpyDeviceToHost, c.stream)));
     if (c.total_sent)  // the engine already queued it on the copy stream
       EFG_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.aux_ev[1], 0));
     else
@@ -680,6 +686,22 @@ int efg_profile_report(efg_ctx* ctx, char* buf, int64_t cap) {
     }
     js += "}";
     EFG_REQUIRE((int64_t)js.size() < cap, "report buffer too small");
+    std::memcpy(buf, js.c_str(), js.size() + 1);
+  });
+}
+
+int efg_profile_timeline(efg_ctx* ctx, char* buf, int64_t cap) {
+  if (!buf || cap < 3) return fail(efg::EFG_INVALID, "bad timeline buffer");
+  return guarded(ctx, [&](Context& c) {
+    std::string js = "[";
+    char item[256];
+    for (size_t k = 0; k < c.prof.timeline.size(); ++k) {
+      const auto& sp = c.prof.timeline[k];
+      snprintf(item, sizeof item, "%s[\"%s\",%.4f,%.4f]", k ? "," : "", sp.name.c_str(), sp.start, sp.ms);
+      js += item;
+    }
+    js += "]";
+    EFG_REQUIRE((int64_t)js.size() < cap, "timeline buffer too small");
     std::memcpy(buf, js.c_str(), js.size() + 1);
   });
 }

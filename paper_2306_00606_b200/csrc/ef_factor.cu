@@ -2206,9 +2206,37 @@ constexpr int kNCounts = kNSlots + (kCB + 1) * kMaxChunks;
 __host__ __device__ constexpr int cslot(int c, int k) { return kNSlots + c * kMaxChunks + k; }
 constexpr int64_t kHistWarpMax = 32, kHistBlockMax = kHistThreads * kHistItems, kCtabGroupMax = 64;
 
-// Node-class lists.  Histogram and chain-table classes are selected per row
-// chunk (chunk k's part of list X starts at X + row[k]), so their kernels can
-// run on a chunk as soon as its neighbours are resident.
+// per-chunk runs of the row-class lists: chunk k of class c = ids in [row[k], row[k+1])
+struct ChunkLists {
+  const int32_t* list[kCB + 1];
+  int nlists, nchunks;
+  int64_t row[kMaxChunks + 1];
+};
+__device__ __forceinline__ int64_t ids_below(const int32_t* __restrict__ l, int64_t len, int64_t x) {
+  int64_t lo = 0, hi = len;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (l[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+__global__ void k_chunk_counts(ChunkLists cl, int64_t* __restrict__ cdev) {
+  const int c = threadIdx.x / kMaxChunks, k = threadIdx.x % kMaxChunks;
+  if (c >= cl.nlists || k >= cl.nchunks) return;
+  const int64_t len = cdev[c];  // the class's total (slot c)
+  cdev[cslot(c, k)] = ids_below(cl.list[c], len, cl.row[k + 1]) - ids_below(cl.list[c], len, cl.row[k]);
+}
+// first entry of chunk k's run in class list cls (host, from the read-back counts)
+static inline int64_t lstart(const int64_t* c, int cls, int k) {
+  int64_t s = 0;
+  for (int j = 0; j < k; ++j) s += c[cslot(cls, j)];
+  return s;
+}
+
+// Node-class lists.  Histogram and chain-table classes are selected once over
+// all rows; chunk k's run of list X starts at X + lstart(c, X, k), so their
+// kernels can run on a chunk as soon as its neighbours are resident.
 // row_lists: the per-chunk histogram / chain-table classes; tri_lists (with
 // seeds): the triangle classes and the hub list.
 static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, SeedRange r, int64_t* cdev, bool seeds,
@@ -2227,18 +2255,27 @@ static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, See
     L.cg = list("f_l_cg", n);
     L.cb = list("f_l_cb", n);
   }
-  for (int k = 0; k < stg.nchunks; ++k) {
-    const SeedRange ch{stg.row[k], stg.row[k + 1]};
-    const int64_t o = stg.row[k];
-    select_seeds(ctx, ch, DegRange{off, -1, 8}, L.hw8 + o, cdev + cslot(kHW8, k));
-    select_seeds(ctx, ch, DegRange{off, 8, kHistWarpMax}, L.hw + o, cdev + cslot(kHW, k));
-    select_seeds(ctx, ch, DegRange{off, kHistWarpMax, 256}, L.hs + o, cdev + cslot(kHS, k));
-    select_seeds(ctx, ch, DegRange{off, 256, kHistBlockMax}, L.hb + o, cdev + cslot(kHB, k));
-    select_seeds(ctx, ch, DegRange{off, kHistBlockMax, INT64_MAX}, L.hl + o, cdev + cslot(kHL, k));
-    if (!seeds) continue;
-    select_seeds(ctx, ch, DegRange{off, kHistWarpMax, kCtabGroupMax}, L.cg + o, cdev + cslot(kCG, k));
-    select_seeds(ctx, ch, DegRange{off, kCtabGroupMax, INT64_MAX}, L.cb + o, cdev + cslot(kCB, k));
+  // one selection per class over all the chunks' rows (ids ascending); chunk
+  // k's part is the run of ids in [row[k], row[k+1]) (k_chunk_counts), at
+  // lstart(c, cls, k) -- 7 selections instead of 7 per chunk (each a few
+  // launches: 28 of them were 2 ms on the staged path before any row work)
+  const SeedRange all{stg.row[0], stg.row[stg.nchunks]};
+  select_seeds(ctx, all, DegRange{off, -1, 8}, L.hw8, cdev + kHW8);
+  select_seeds(ctx, all, DegRange{off, 8, kHistWarpMax}, L.hw, cdev + kHW);
+  select_seeds(ctx, all, DegRange{off, kHistWarpMax, 256}, L.hs, cdev + kHS);
+  select_seeds(ctx, all, DegRange{off, 256, kHistBlockMax}, L.hb, cdev + kHB);
+  select_seeds(ctx, all, DegRange{off, kHistBlockMax, INT64_MAX}, L.hl, cdev + kHL);
+  if (seeds) {
+    select_seeds(ctx, all, DegRange{off, kHistWarpMax, kCtabGroupMax}, L.cg, cdev + kCG);
+    select_seeds(ctx, all, DegRange{off, kCtabGroupMax, INT64_MAX}, L.cb, cdev + kCB);
   }
+  ChunkLists cl{};
+  const int32_t* lists[kCB + 1] = {L.hw8, L.hw, L.hs, L.hb, L.hl, L.cg, L.cb};
+  for (int c = 0; c <= kCB; ++c) cl.list[c] = lists[c];
+  cl.nlists = seeds ? kCB + 1 : kHL + 1;
+  cl.nchunks = stg.nchunks;
+  for (int k = 0; k <= stg.nchunks; ++k) cl.row[k] = stg.row[k];
+  EFG_LAUNCH(k_chunk_counts, 1, 64, 0, ctx.stream, cl, cdev);
   }
   if (!seeds || !tri_lists) return L;
   L.trs = list("f_l_trs", cnt);
@@ -2260,23 +2297,25 @@ static void build_histograms(Context& ctx, const Prepared& P, const Lists& L, co
   cudaStream_t s = ctx.stream;
   const int B = 256;
   const int64_t* off = P.g.offsets;
-  const int64_t o = stg.row[k];
   const int64_t nw = c[cslot(kHW, k)], ns = c[cslot(kHS, k)], nb = c[cslot(kHB, k)], nl = c[cslot(kHL, k)];
   if (small_rows) {
     const int64_t nw8 = c[cslot(kHW8, k)];
-    EFG_LAUNCH(k_hist_warp, ceil_div(nw8 * 32, B), B, 0, s, L.hw8 + o, nw8, off, P.nd, hkey, hcnt, dcnt);
-    EFG_LAUNCH(k_hist_warp, ceil_div(nw * 32, B), B, 0, s, L.hw + o, nw, off, P.nd, hkey, hcnt, dcnt);
+    EFG_LAUNCH(k_hist_warp, ceil_div(nw8 * 32, B), B, 0, s, L.hw8 + lstart(c, kHW8, k), nw8, off, P.nd, hkey, hcnt,
+               dcnt);
+    EFG_LAUNCH(k_hist_warp, ceil_div(nw * 32, B), B, 0, s, L.hw + lstart(c, kHW, k), nw, off, P.nd, hkey, hcnt, dcnt);
   }
   int bits = 1;
   while (bits < 31 && (int64_t(1) << bits) <= (int64_t)P.dmax + 1) ++bits;
-  EFG_LAUNCH(k_hist_warp8, ceil_div(ns * 32, kHistW8Warps * 32), kHistW8Warps * 32, 0, s, L.hs + o, ns, off, P.nd,
+  EFG_LAUNCH(k_hist_warp8, ceil_div(ns * 32, kHistW8Warps * 32), kHistW8Warps * 32, 0, s, L.hs + lstart(c, kHS, k), ns,
+             off, P.nd,
              hkey, hcnt, dcnt);
-  EFG_LAUNCH((k_hist_block<kHistThreads, kHistItems>), nb, kHistThreads, 0, s, L.hb + o, nb, off, P.nd, hkey, hcnt,
+  EFG_LAUNCH((k_hist_block<kHistThreads, kHistItems>), nb, kHistThreads, 0, s, L.hb + lstart(c, kHB, k), nb, off, P.nd,
+             hkey, hcnt,
              dcnt, bits);
   if (nl) {
     const int smw = kHistWin * (int)sizeof(int32_t);
     EFG_CUDA_CHECK(cudaFuncSetAttribute(k_hist_count, cudaFuncAttributeMaxDynamicSharedMemorySize, smw));
-    EFG_LAUNCH(k_hist_count, nl, kHistBigThreads, smw, s, L.hl + o, nl, off, P.nd, hkey, hcnt, dcnt);
+    EFG_LAUNCH(k_hist_count, nl, kHistBigThreads, smw, s, L.hl + lstart(c, kHL, k), nl, off, P.nd, hkey, hcnt, dcnt);
   }
 }
 
@@ -2390,28 +2429,28 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
       // (d <= 8: four rows per warp)
       const int64_t nsm8 = c[cslot(kHW8, k)], nsm = c[cslot(kHW, k)];
       EFG_LAUNCH(k_small_rows8, ceil_div(ceil_div(nsm8, 4), kSmallWarps), kSmallWarps * 32, 0, s,
-                 L.hw8 + rows.row[k], nsm8, g.offsets, g.nbr, P.nd, P.ftab, P.s1, ca, P.ftab_len);
-      EFG_LAUNCH(k_small_rows, ceil_div(nsm, kSmallWarps), kSmallWarps * 32, 0, s, L.hw + rows.row[k], nsm,
+                 L.hw8 + lstart(c, kHW8, k), nsm8, g.offsets, g.nbr, P.nd, P.ftab, P.s1, ca, P.ftab_len);
+      EFG_LAUNCH(k_small_rows, ceil_div(nsm, kSmallWarps), kSmallWarps * 32, 0, s, L.hw + lstart(c, kHW, k), nsm,
                  g.offsets, g.nbr, P.nd, P.deg, P.ftab, P.s1, ca, P.ftab_len);
       // chain tables C_i(y): rows with 32 < d <= 64 by 8-lane groups, the rest by CTAs
-      const int64_t o = rows.row[k], ng = c[cslot(kCG, k)], nb = c[cslot(kCB, k)];
-      EFG_LAUNCH(k_ctab_group<8>, ceil_div(ng * 8, B), B, 0, s, L.cg + o, ng, g.offsets, dcnt, hkey, hcnt, P.deg,
+      const int64_t ng = c[cslot(kCG, k)], nb = c[cslot(kCB, k)];
+      EFG_LAUNCH(k_ctab_group<8>, ceil_div(ng * 8, B), B, 0, s, L.cg + lstart(c, kCG, k), ng, g.offsets, dcnt, hkey, hcnt, P.deg,
                  P.ftab, ctab, P.ftab_len);
       // rows of degree > 64: fewer than kCtabWarpD distinct neighbour degrees (half of them,
       // no far-field expansion) a warp each, the rest a CTA each
-      EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab,
+      EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + lstart(c, kCB, k), nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab,
                  ctab, kExpMin, kExpMinD, P.ftab_len, kCtabWarpD);
       if (kCtabWarpD > 0)
-        EFG_LAUNCH(k_ctab_warp, ceil_div(nb, kCtabWarps), kCtabWarps * 32, 0, s, L.cb + o, nb, g.offsets, dcnt, hkey,
+        EFG_LAUNCH(k_ctab_warp, ceil_div(nb, kCtabWarps), kCtabWarps * 32, 0, s, L.cb + lstart(c, kCB, k), nb, g.offsets, dcnt, hkey,
                    hcnt, P.deg, P.ftab, ctab, P.ftab_len, kCtabWarpD - 1);
       // chains pushed from the rows whose tables are now complete
       const int64_t ps1 = c[cslot(kHS, k)], pb = c[cslot(kHB, k)], pl = c[cslot(kHL, k)];
-      EFG_LAUNCH(k_push_warp256, ceil_div(ps1, kPushWarps), kPushWarps * 32, 0, s, L.hs + o, ps1, g.offsets, g.nbr,
+      EFG_LAUNCH(k_push_warp256, ceil_div(ps1, kPushWarps), kPushWarps * 32, 0, s, L.hs + lstart(c, kHS, k), ps1, g.offsets, g.nbr,
                  P.nd, dcnt, hkey, hcnt, ctab, P.s1, ca);
-      EFG_LAUNCH(k_push_block, pb, kPushThreads, 0, s, L.hb + o, pb, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,
+      EFG_LAUNCH(k_push_block, pb, kPushThreads, 0, s, L.hb + lstart(c, kHB, k), pb, g.offsets, g.nbr, P.nd, dcnt, hkey, hcnt, ctab,
                  P.s1, ca);
       // rows of degree > 2048 in kPushSlices slices each (a hub row is one CTA's long serial loop otherwise)
-      EFG_LAUNCH(k_push_block, dim3((unsigned)pl, kPushSlices), kPushThreads, 0, s, L.hl + o, pl, g.offsets, g.nbr,
+      EFG_LAUNCH(k_push_block, dim3((unsigned)pl, kPushSlices), kPushThreads, 0, s, L.hl + lstart(c, kHL, k), pl, g.offsets, g.nbr,
                  P.nd, dcnt, hkey, hcnt, ctab, P.s1, ca);
     }
     if (dmode == kDistRepl || dmode == kDistRows) {  // the part's S1 / S2 into the words (the finish needs them)

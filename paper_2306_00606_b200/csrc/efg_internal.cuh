@@ -37,6 +37,11 @@ struct Profiler {
   size_t used = 0;
   std::vector<Rec> pending;
   std::map<std::string, std::pair<double, int64_t>> totals;  // name -> (ms, launches)
+  struct Span {
+    std::string name;
+    float start, ms;  // start relative to the call's first recorded event
+  };
+  std::vector<Span> timeline;  // every record of the last resolved call (efg_profile_timeline)
   cudaEvent_t take();
   void resolve();  // after a stream sync
   ~Profiler();

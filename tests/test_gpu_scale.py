@@ -242,3 +242,26 @@ def test_star_beyond_listing_bound():
     leaves = np.flatnonzero(deg == 1)
     assert np.all(np.abs(r.ef[leaves] - np.log(k - 1.0)) <= 1e-9 * np.log(k - 1.0) + 1e-12)
     assert np.array_equal(r.cluster_total, deg * (deg - 1) + np.add.reduceat(deg[g.neighbors], g.offsets[:-1]) - deg)
+
+
+@pytest.mark.parametrize("splits", ["none", "40", "15,35,62", "5,10,20,40,60,80,90"])
+def test_staged_chunks_bitwise(rmat18, splits, monkeypatch):
+    # host inputs reach the device in row chunks and the engine takes up each
+    # chunk's rows as it lands (class lists selected once, per-chunk runs from
+    # k_chunk_counts): any split gives the device-resident result bit for bit,
+    # from page-locked and from pageable host arrays
+    import torch
+    from paper_2306_00606_b200 import device as D
+    from paper_2306_00606_b200.graph import Graph
+
+    dg = D.DeviceGraph.from_host(rmat18)
+    n = rmat18.n
+    full = [torch.empty(n, dtype=t, device="cuda") for t in (torch.float64, torch.int64, torch.uint8)]
+    D.ef_range(dg, 0, n, *full)
+    want = [x.cpu().numpy() for x in full]
+    monkeypatch.setenv("EFG_STAGE_SPLITS", splits)
+    pageable = Graph(n, rmat18.m, np.array(rmat18.offsets, copy=True), np.array(rmat18.neighbors, copy=True), None)
+    for g in (rmat18, pageable):
+        r = efg.ef_cluster_centric(g)
+        assert np.array_equal(r.ef, want[0]) and np.array_equal(r.cluster_total, want[1])
+        assert np.array_equal(r.flags, want[2])

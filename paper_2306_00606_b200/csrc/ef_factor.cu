@@ -2205,6 +2205,110 @@ enum Slot {
 constexpr int kNCounts = kNSlots + (kCB + 1) * kMaxChunks;
 __host__ __device__ constexpr int cslot(int c, int k) { return kNSlots + c * kMaxChunks + k; }
 constexpr int64_t kHistWarpMax = 32, kHistBlockMax = kHistThreads * kHistItems, kCtabGroupMax = 64;
+#ifndef EFG_CLASS_KERNELS
+#define EFG_CLASS_KERNELS 1
+#endif
+constexpr bool kClassKernels = EFG_CLASS_KERNELS;
+
+// Row-class lists in one pass over the degrees (instead of one CUB selection
+// per class): tiles of kClsTile rows, per-tile class counts, a scan of the
+// tile counts per class, then each tile scatters its rows in id order (the
+// same ascending lists as a selection).  Classes: histogram class 0..4 (d <=
+// 8, <= 32, <= 256, <= kHistBlockMax, above) and chain-table class 5 / 6
+// (32 < d <= 64, d > 64); 12-bit fields of packed per-thread counts.
+constexpr int kClsThreads = 256, kClsPer = 8, kClsTile = kClsThreads * kClsPer;
+struct ClassArgs {
+  const int32_t* deg;
+  int64_t r0, r1;
+  int32_t ntiles, nclasses;  // 5 (histograms only) or 7
+  int32_t* list[7];
+  int64_t* tcount;  // [7][ntiles]
+  int64_t* tbase;   // [7][ntiles]
+};
+// per-thread packed counts of its kClsPer rows: hist classes (5 x 12 bits) and chain-table classes (2 x 12 bits)
+__device__ __forceinline__ void cls_counts(const ClassArgs& a, int64_t v0, uint64_t& hc, uint32_t& cc) {
+  hc = 0;
+  cc = 0;
+#pragma unroll
+  for (int i = 0; i < kClsPer; ++i) {
+    const int64_t v = v0 + i;
+    if (v >= a.r1) break;
+    const int32_t d = __ldg(a.deg + v);
+    const int h = d <= 8 ? 0 : d <= 32 ? 1 : d <= 256 ? 2 : d <= (int32_t)(kHistThreads * kHistItems) ? 3 : 4;
+    hc += 1ull << (12 * h);
+    if (a.nclasses > 5 && d > 32) cc += 1u << (d > 64 ? 12 : 0);
+  }
+}
+__global__ void __launch_bounds__(kClsThreads) k_class_count(ClassArgs a) {
+  using BR64 = cub::BlockReduce<uint64_t, kClsThreads>;
+  using BR32 = cub::BlockReduce<uint32_t, kClsThreads>;
+  __shared__ typename BR64::TempStorage t64;
+  __shared__ typename BR32::TempStorage t32;
+  const int tile = blockIdx.x;
+  uint64_t hc;
+  uint32_t cc;
+  cls_counts(a, a.r0 + (int64_t)tile * kClsTile + threadIdx.x * kClsPer, hc, cc);
+  hc = BR64(t64).Sum(hc);
+  cc = BR32(t32).Sum(cc);
+  if (threadIdx.x == 0) {
+    for (int c = 0; c < 5; ++c) a.tcount[(int64_t)c * a.ntiles + tile] = (int64_t)((hc >> (12 * c)) & 0xfff);
+    for (int c = 5; c < a.nclasses; ++c) a.tcount[(int64_t)c * a.ntiles + tile] = (int64_t)((cc >> (12 * (c - 5))) & 0xfff);
+  }
+}
+// block c: exclusive scan of class c's tile counts; its total into cdev[c]
+__global__ void __launch_bounds__(1024) k_class_scan(ClassArgs a, int64_t* __restrict__ cdev) {
+  using BS = cub::BlockScan<int64_t, 1024>;
+  __shared__ typename BS::TempStorage tmp;
+  __shared__ int64_t carry;
+  const int c = blockIdx.x;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int32_t t0 = 0; t0 < a.ntiles; t0 += 1024) {
+    const int32_t t = t0 + threadIdx.x;
+    const int64_t x = t < a.ntiles ? a.tcount[(int64_t)c * a.ntiles + t] : 0;
+    int64_t ex, tot;
+    BS(tmp).ExclusiveSum(x, ex, tot);
+    const int64_t base = carry;
+    if (t < a.ntiles) a.tbase[(int64_t)c * a.ntiles + t] = base + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry = base + tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) cdev[c] = carry;
+}
+__global__ void __launch_bounds__(kClsThreads) k_class_scatter(ClassArgs a) {
+  using BS64 = cub::BlockScan<uint64_t, kClsThreads>;
+  using BS32 = cub::BlockScan<uint32_t, kClsThreads>;
+  __shared__ typename BS64::TempStorage t64;
+  __shared__ typename BS32::TempStorage t32;
+  const int tile = blockIdx.x;
+  const int64_t v0 = a.r0 + (int64_t)tile * kClsTile + threadIdx.x * kClsPer;
+  uint64_t hc;
+  uint32_t cc;
+  cls_counts(a, v0, hc, cc);
+  BS64(t64).ExclusiveSum(hc, hc);
+  BS32(t32).ExclusiveSum(cc, cc);
+  int64_t pos[7];
+#pragma unroll
+  for (int c = 0; c < 5; ++c) pos[c] = a.tbase[(int64_t)c * a.ntiles + tile] + (int64_t)((hc >> (12 * c)) & 0xfff);
+#pragma unroll
+  for (int c = 5; c < 7; ++c)
+    pos[c] = c < a.nclasses ? a.tbase[(int64_t)c * a.ntiles + tile] + (int64_t)((cc >> (12 * (c - 5))) & 0xfff) : 0;
+#pragma unroll
+  for (int i = 0; i < kClsPer; ++i) {
+    const int64_t v = v0 + i;
+    if (v >= a.r1) break;
+    const int32_t d = __ldg(a.deg + v);
+    const int h = d <= 8 ? 0 : d <= 32 ? 1 : d <= 256 ? 2 : d <= (int32_t)(kHistThreads * kHistItems) ? 3 : 4;
+#pragma unroll
+    for (int c = 0; c < 5; ++c)
+      if (c == h) a.list[c][pos[c]++] = (int32_t)v;
+    if (a.nclasses > 5 && d > 32) {
+      if (d > 64) a.list[6][pos[6]++] = (int32_t)v;
+      else a.list[5][pos[5]++] = (int32_t)v;
+    }
+  }
+}
 
 // per-chunk runs of the row-class lists: chunk k of class c = ids in [row[k], row[k+1])
 struct ChunkLists {
@@ -2260,14 +2364,33 @@ static Lists make_lists(Context& ctx, const Prepared& P, const Staging& stg, See
   // lstart(c, cls, k) -- 7 selections instead of 7 per chunk (each a few
   // launches: 28 of them were 2 ms on the staged path before any row work)
   const SeedRange all{stg.row[0], stg.row[stg.nchunks]};
-  select_seeds(ctx, all, DegRange{off, -1, 8}, L.hw8, cdev + kHW8);
-  select_seeds(ctx, all, DegRange{off, 8, kHistWarpMax}, L.hw, cdev + kHW);
-  select_seeds(ctx, all, DegRange{off, kHistWarpMax, 256}, L.hs, cdev + kHS);
-  select_seeds(ctx, all, DegRange{off, 256, kHistBlockMax}, L.hb, cdev + kHB);
-  select_seeds(ctx, all, DegRange{off, kHistBlockMax, INT64_MAX}, L.hl, cdev + kHL);
-  if (seeds) {
-    select_seeds(ctx, all, DegRange{off, kHistWarpMax, kCtabGroupMax}, L.cg, cdev + kCG);
-    select_seeds(ctx, all, DegRange{off, kCtabGroupMax, INT64_MAX}, L.cb, cdev + kCB);
+  static_assert(kHistWarpMax == 32 && kCtabGroupMax == 64, "k_class_* hard-code the class bounds");
+  if (kClassKernels) {
+    ClassArgs ca{};
+    ca.deg = P.deg;
+    ca.r0 = all.lo;
+    ca.r1 = all.hi;
+    ca.ntiles = (int32_t)ceil_div(all.hi - all.lo, (int64_t)kClsTile);
+    ca.nclasses = seeds ? 7 : 5;
+    int32_t* lists7[7] = {L.hw8, L.hw, L.hs, L.hb, L.hl, L.cg, L.cb};
+    for (int c = 0; c < 7; ++c) ca.list[c] = lists7[c];
+    ca.tcount = ctx.buf("f_cls_tiles").as<int64_t>(2 * 7 * (int64_t)std::max(ca.ntiles, 1));
+    ca.tbase = ca.tcount + 7 * (int64_t)std::max(ca.ntiles, 1);
+    if (ca.ntiles > 0) {
+      EFG_LAUNCH(k_class_count, ca.ntiles, kClsThreads, 0, ctx.stream, ca);
+      EFG_LAUNCH(k_class_scan, ca.nclasses, 1024, 0, ctx.stream, ca, cdev);
+      EFG_LAUNCH(k_class_scatter, ca.ntiles, kClsThreads, 0, ctx.stream, ca);
+    }
+  } else {
+    select_seeds(ctx, all, DegRange{off, -1, 8}, L.hw8, cdev + kHW8);
+    select_seeds(ctx, all, DegRange{off, 8, kHistWarpMax}, L.hw, cdev + kHW);
+    select_seeds(ctx, all, DegRange{off, kHistWarpMax, 256}, L.hs, cdev + kHS);
+    select_seeds(ctx, all, DegRange{off, 256, kHistBlockMax}, L.hb, cdev + kHB);
+    select_seeds(ctx, all, DegRange{off, kHistBlockMax, INT64_MAX}, L.hl, cdev + kHL);
+    if (seeds) {
+      select_seeds(ctx, all, DegRange{off, kHistWarpMax, kCtabGroupMax}, L.cg, cdev + kCG);
+      select_seeds(ctx, all, DegRange{off, kCtabGroupMax, INT64_MAX}, L.cb, cdev + kCB);
+    }
   }
   ChunkLists cl{};
   const int32_t* lists[kCB + 1] = {L.hw8, L.hw, L.hs, L.hb, L.hl, L.cg, L.cb};

@@ -1448,11 +1448,21 @@ constexpr int kMidWarps = 8;
 constexpr int kMidThreads = 256;
 constexpr int kMidNB = 512;         // shared map of Adj+(v): <= 1024 keys at load <= 1/2
 constexpr int kMidLgNB = 9;
+// Adj+(v) parts of 768 entries with chunks of 512 rows fill the same shared
+// memory as 1024 / 256 (5 CTAs per SM): half the chunk barriers and entry
+// flushes for a few more parts (R-MAT22: |Adj+(v)| <= 813); measured
+// k_mid_big 11.06 (1024 / 256) -> 10.62 ms (768 / 512); 640 / 512: 11.26
 #ifndef EFG_MID_MAXP
-#define EFG_MID_MAXP 1024
+#define EFG_MID_MAXP 768
 #endif
 constexpr int kMidMaxP = EFG_MID_MAXP;  // longer Adj+(v) are processed in parts of this size
-constexpr int kMidChunk = 256;     // rows between entry flushes: 32-bit entry words cannot overflow
+#ifndef EFG_MID_CHUNK
+#define EFG_MID_CHUNK 512
+#endif
+// rows between entry flushes: 32-bit entry words cannot overflow (per entry and chunk at most
+// kMidChunk hits of Q < 2^45: low pieces < 512 * 2^22 = 2^31, high pieces < 512 * 2^23 = 2^32)
+constexpr int kMidChunk = EFG_MID_CHUNK;
+static_assert(kMidChunk <= 512, "entry words would overflow");
 // probe-loop unroll (entries per lane per step), measured per loop: bitmap scan with
 // the 8-byte word+prefix entries 4 for long rows, 2 / 1 for rows whose scan is at most
 // 64 / 32 entries (k_mid_big 12.25 -> 11.80 ms; peeking at labels 31 / 63 of longer
@@ -1884,7 +1894,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
   const int32_t labv = __ldg(a.rank_of + v);
   if (pv == 0) return;  // no triangle has v in the middle
   Acc2 av;
-  // Adj+(v) in parts of kMidMaxP entries (one part unless |Adj+(v)| > 1024);
+  // Adj+(v) in parts of kMidMaxP entries (one part unless |Adj+(v)| > kMidMaxP);
   // a part's rows stop at its last label
   for (int32_t q0 = 0; q0 < pv; q0 += kMidMaxP) {
     const int32_t np = min(pv - q0, kMidMaxP);

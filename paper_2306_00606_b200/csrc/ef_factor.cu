@@ -1444,16 +1444,22 @@ __global__ void k_hub_bitmaps(const int32_t* __restrict__ hubs, int64_t nhubs, c
 // which commute, so the result does not depend on scheduling.  Global words
 // per node: (sum of s >> 32, sum of s & (2^32-1), count), never overflowing
 // (a row has < 2^16 hits, a node < 2^31 partial sums).
+#ifndef EFG_MID_BIG_THREADS
+#define EFG_MID_BIG_THREADS 320
+#endif
 constexpr int kMidWarps = 8;
 constexpr int kMidThreads = 256;
 constexpr int kMidNB = 512;         // shared map of Adj+(v): <= 1024 keys at load <= 1/2
 constexpr int kMidLgNB = 9;
-// Adj+(v) parts of 768 entries with chunks of 512 rows fill the same shared
-// memory as 1024 / 256 (5 CTAs per SM): half the chunk barriers and entry
-// flushes for a few more parts (R-MAT22: |Adj+(v)| <= 813); measured
-// k_mid_big 11.06 (1024 / 256) -> 10.62 ms (768 / 512); 640 / 512: 11.26
+// Big middles: CTAs of 10 warps, 4 per SM (48 registers: 40 warps, as 5 x 8),
+// each with Adj+(v) parts of 1024 entries and chunks of 512 rows (48 KB of
+// shared memory).  Measured k_mid_big, R-MAT22 (r02): 8 warps x 5 CTAs with
+// parts / chunks of 1024 / 256: 11.06 ms; 768 / 512 (same shared memory):
+// 10.62; 640 / 512: 11.26; 10 warps x 4 CTAs, 768 / 512: 10.37, 1024 / 512:
+// 10.27; 12 warps x 3 CTAs: 10.88.  Fewer, larger chunks halve the barrier
+// waits and entry flushes; fewer CTAs per SM build fewer Adj+(v) bitmaps.
 #ifndef EFG_MID_MAXP
-#define EFG_MID_MAXP 768
+#define EFG_MID_MAXP 1024
 #endif
 constexpr int kMidMaxP = EFG_MID_MAXP;  // longer Adj+(v) are processed in parts of this size
 #ifndef EFG_MID_CHUNK
@@ -1472,7 +1478,7 @@ static_assert(kMidChunk <= 512, "entry words would overflow");
 #define EFG_MID_UNROLL_BM 4
 #endif
 #ifndef EFG_MID_BIG_MINB
-#define EFG_MID_BIG_MINB 5
+#define EFG_MID_BIG_MINB 4
 #endif
 constexpr int kMidUnrollBm = EFG_MID_UNROLL_BM;
 #ifndef EFG_MID_ADAPT_U
@@ -1487,7 +1493,8 @@ constexpr int kMidSmallDeg = 256;  // middle vertices of degree <= this run in s
 // CTA shapes of k_mid_block: big (hub tasks and degree > kMidSmallDeg) and
 // small (32 < degree <= kMidSmallDeg, where |Adj+(v)| and the rows are few).
 struct MidBig {
-  static constexpr int kThreads = kMidThreads, kNB = kMidNB, kLgNB = kMidLgNB, kMaxP = kMidMaxP, kChunk = kMidChunk;
+  static constexpr int kThreads = EFG_MID_BIG_THREADS, kNB = kMidNB, kLgNB = kMidLgNB, kMaxP = kMidMaxP,
+                       kChunk = kMidChunk;
   static constexpr int kBmWords = 2048;  // label bitmap for rank(v) <= 65536 (same shared bytes as the hash)
   static constexpr int kUnrollHash = 4;
 };
@@ -2037,8 +2044,9 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
   }
 }
 
-// Launch shapes: 5 CTAs per SM for the big instantiation (<= 51 registers:
-// measured 14.6 ms against 15.6 at 63 registers / 4 CTAs), 12 for the small.
+// Launch shapes: 4 CTAs of 320 threads per SM for the big instantiation (<= 51
+// registers; round 1 with 256-thread CTAs: 5 per SM 14.6 ms against 15.6 at 63
+// registers / 4), 12 for the small.
 template <bool PART>
 __global__ void __launch_bounds__(MidBig::kThreads, EFG_MID_BIG_MINB) k_mid_big(MArgs a, HubTasks tk) {
   mid_block_body<PART, MidBig>(a, tk);

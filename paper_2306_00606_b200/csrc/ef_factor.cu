@@ -1276,7 +1276,10 @@ struct HubMap {
 // Hub work is cut into tasks of kHubRows consecutive rows, so the largest
 // hubs spread over many SMs; each task rebuilds the filter (dv bits, well
 // below its probe count) and writes a partial merged per hub in task order.
-constexpr int64_t kHubRows = 8192;
+#ifndef EFG_HUB_ROWS
+#define EFG_HUB_ROWS 16384  // k_mid_big 10.40 / 10.28 / 10.26 ms at 4096 / 8192 / 16384 (r02)
+#endif
+constexpr int64_t kHubRows = EFG_HUB_ROWS;
 
 struct HubTasks {
   const int32_t* seed;  // [ntasks]
@@ -1498,8 +1501,17 @@ struct MidBig {
   static constexpr int kBmWords = 2048;  // label bitmap for rank(v) <= 65536 (same shared bytes as the hash)
   static constexpr int kUnrollHash = 4;
 };
+// small middles (33..256): CTAs of 3 warps (14 per SM, shared-memory bound):
+// a middle has ~30 rows, so fewer warps wait less at its barriers; measured
+// k_mid_small 2.32 ms with 4 warps x 12, 2.24 with 3 x 14, 2.74 with 6 x 8
+#ifndef EFG_MID_SMALL_THREADS
+#define EFG_MID_SMALL_THREADS 96
+#endif
+#ifndef EFG_MID_SMALL_MINB
+#define EFG_MID_SMALL_MINB 16
+#endif
 struct MidSmall {
-  static constexpr int kThreads = 128, kNB = 128, kLgNB = 7, kMaxP = kMidSmallDeg, kChunk = kMidSmallDeg;
+  static constexpr int kThreads = EFG_MID_SMALL_THREADS, kNB = 128, kLgNB = 7, kMaxP = kMidSmallDeg, kChunk = kMidSmallDeg;
   static constexpr int kBmWords = 0;
   static constexpr int kUnrollHash = 2;
 };
@@ -2052,7 +2064,7 @@ __global__ void __launch_bounds__(MidBig::kThreads, EFG_MID_BIG_MINB) k_mid_big(
   mid_block_body<PART, MidBig>(a, tk);
 }
 template <bool PART>
-__global__ void __launch_bounds__(MidSmall::kThreads, 12) k_mid_small(MArgs a, HubTasks tk) {
+__global__ void __launch_bounds__(MidSmall::kThreads, EFG_MID_SMALL_MINB) k_mid_small(MArgs a, HubTasks tk) {
   mid_block_body<PART, MidSmall>(a, tk);
 }
 

@@ -1510,8 +1510,12 @@ struct MidBig {
 #ifndef EFG_MID_SMALL_MINB
 #define EFG_MID_SMALL_MINB 16
 #endif
+#ifndef EFG_MID_SMALL_CHUNK
+#define EFG_MID_SMALL_CHUNK 256
+#endif
 struct MidSmall {
-  static constexpr int kThreads = EFG_MID_SMALL_THREADS, kNB = 128, kLgNB = 7, kMaxP = kMidSmallDeg, kChunk = kMidSmallDeg;
+  static constexpr int kThreads = EFG_MID_SMALL_THREADS, kNB = 128, kLgNB = 7, kMaxP = kMidSmallDeg,
+                       kChunk = EFG_MID_SMALL_CHUNK;
   static constexpr int kBmWords = 0;
   static constexpr int kUnrollHash = 2;
 };

@@ -841,7 +841,13 @@ k_small_rows8(const int32_t* __restrict__ rows, int64_t count, const int64_t* __
 // located through a direct-mapped shared table (key -> position; only keys
 // present are ever read, so it needs no clearing), larger ones by binary
 // search over H_i's keys (shared memory, global beyond kPushKeys).
-constexpr int kPushThreads = 128, kPushKeys = 4096, kPushDirect = 4096, kPushSlices = 16;
+#ifndef EFG_PUSH_THREADS
+#define EFG_PUSH_THREADS 128
+#endif
+#ifndef EFG_PUSH_SLICES
+#define EFG_PUSH_SLICES 8  // k_push_block ms (r02): 4: 1.04, 6: 1.03, 8: 1.07, 12: 1.14, 16: 1.17, 32: 1.43; e2e best at 8
+#endif
+constexpr int kPushThreads = EFG_PUSH_THREADS, kPushKeys = 4096, kPushDirect = 4096, kPushSlices = EFG_PUSH_SLICES;
 #ifndef EFG_PUSH_UNROLL
 #define EFG_PUSH_UNROLL 4
 #endif

@@ -171,7 +171,10 @@ k_hist_warp8(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
   if (lane == 0) dcnt[i] = total;
 }
 
-constexpr int kHistThreads = 256, kHistItems = 8;
+#ifndef EFG_HIST_THREADS
+#define EFG_HIST_THREADS 128  // k_hist_block (rows of 257..2048 slots) ms (r02): 128: 0.470, 256: 0.489, 512: 0.766
+#endif
+constexpr int kHistThreads = EFG_HIST_THREADS, kHistItems = 2048 / EFG_HIST_THREADS;  // rows of <= 2048 slots
 // 256 < d <= THREADS*ITEMS (2048): CTA per row, radix sort in shared memory
 // over the bits degrees actually use (keys < 2^bits; padding = 2^bits - 1
 // sorts last).
@@ -238,7 +241,10 @@ k_hist_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
 // degrees of other hubs -- few -- so the first pass also collects them
 // (<= kHistOvf) and counts them by pairwise comparison instead of further
 // window passes over the whole row.
-constexpr int kHistWin = 16384, kHistBigThreads = 512, kHistOvf = 2048;
+#ifndef EFG_HIST_BIG_THREADS
+#define EFG_HIST_BIG_THREADS 512
+#endif
+constexpr int kHistWin = 16384, kHistBigThreads = EFG_HIST_BIG_THREADS, kHistOvf = 2048;
 __global__ void __launch_bounds__(kHistBigThreads)
 k_hist_count(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
              const int32_t* __restrict__ nd, int32_t* __restrict__ hkey, int32_t* __restrict__ hcnt,
@@ -420,7 +426,10 @@ __device__ __forceinline__ void ctab_outputs(const int32_t* __restrict__ sx, con
 // carries up to 4 outputs (y = its own + 32, + 64, + 96) and every staged pair
 // feeds their F gathers -- the same fma sequence per output as k_ctab_block's
 // direct path (inputs in ascending order), so the values are identical.
-constexpr int kCtabWarps = 8;
+#ifndef EFG_CTAB_WARPS
+#define EFG_CTAB_WARPS 4  // 4 / 8 / 16 warps per CTA: 0.512 / 0.538 / 0.71 ms (r02)
+#endif
+constexpr int kCtabWarps = EFG_CTAB_WARPS;
 __global__ void __launch_bounds__(kCtabWarps * 32)
 k_ctab_warp(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
             const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey, const int32_t* __restrict__ hcnt,
@@ -708,7 +717,10 @@ __device__ __forceinline__ void chain_push(const ChainAcc& ca, int32_t v, int32_
 // k computes C_i(key_k) over the D keys (shuffled in), and each slot takes the
 // value of its degree's run.  Same table values as k_hist_warp + k_ctab_group
 // (same summation order).
-constexpr int kSmallWarps = 8;
+#ifndef EFG_SMALL_WARPS
+#define EFG_SMALL_WARPS 4
+#endif
+constexpr int kSmallWarps = EFG_SMALL_WARPS;
 __global__ void __launch_bounds__(kSmallWarps * 32)
 k_small_rows(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
                              const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd,
@@ -919,7 +931,10 @@ k_push_block(const int32_t* __restrict__ rows, int64_t count, const int64_t* __r
 // 32 < d <= 256: warp per row, H_i's keys (<= 256) in the warp's shared slice,
 // binary search per slot.  (Also taking the 256 < d <= 2048 rows with <= 256
 // distinct neighbour degrees measured neutral, r02.)
-constexpr int kPushWarps = 8, kPushWarpKeys = 256;
+#ifndef EFG_PUSH_WARPS
+#define EFG_PUSH_WARPS 4
+#endif
+constexpr int kPushWarps = EFG_PUSH_WARPS, kPushWarpKeys = 256;
 __global__ void __launch_bounds__(kPushWarps * 32)
 k_push_warp256(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
                const int32_t* __restrict__ nbr, const int32_t* __restrict__ nd, const int32_t* __restrict__ dcnt,

@@ -44,7 +44,10 @@ __device__ __forceinline__ bool ranks_above(int32_t dj, int32_t j, int32_t di, i
 // [offsets[v], offsets[v] + dplus[v]) -- slot space, so no scan is needed and
 // the pass runs per row chunk while the rest of the graph is still copied.
 constexpr int kRowUnroll = 4;
-constexpr int kRowThreads = 256;
+#ifndef EFG_ROW_THREADS
+#define EFG_ROW_THREADS 256
+#endif
+constexpr int kRowThreads = EFG_ROW_THREADS;
 // Rows longer than kRowBig (hubs) would be one warp's serial chain of
 // dependent loads (the top R-MAT22 hub: 965 steps, ~1 ms); with the
 // orientation they go to the first kRowBigBlocks CTAs of the same launch,

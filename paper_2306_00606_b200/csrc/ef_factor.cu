@@ -121,7 +121,10 @@ __global__ void k_hist_warp(const int32_t* __restrict__ rows, int64_t count, con
 // 32 < d <= 256: warp per row, the neighbour degrees sorted in registers
 // (32x8 bitonic), run heads by comparison with the left neighbour, their
 // positions compacted by a warp scan; counts = distance to the next head.
-constexpr int kHistW8Warps = 8;
+#ifndef EFG_HIST_W8_WARPS
+#define EFG_HIST_W8_WARPS 8
+#endif
+constexpr int kHistW8Warps = EFG_HIST_W8_WARPS;
 __global__ void __launch_bounds__(kHistW8Warps * 32)
 k_hist_warp8(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
              const int32_t* __restrict__ nd, int32_t* __restrict__ hkey, int32_t* __restrict__ hcnt,
@@ -1471,7 +1474,10 @@ __global__ void k_hub_bitmaps(const int32_t* __restrict__ hubs, int64_t nhubs, c
 #ifndef EFG_MID_BIG_THREADS
 #define EFG_MID_BIG_THREADS 320
 #endif
-constexpr int kMidWarps = 8;
+#ifndef EFG_MID_WARPS
+#define EFG_MID_WARPS 4  // k_mid_warp ms (r02): 4: 0.746, 8: 0.795, 16: 0.853
+#endif
+constexpr int kMidWarps = EFG_MID_WARPS;  // k_mid_warp: warps (middles) per CTA
 constexpr int kMidThreads = 256;
 constexpr int kMidNB = 512;         // shared map of Adj+(v): <= 1024 keys at load <= 1/2
 constexpr int kMidLgNB = 9;

@@ -176,6 +176,23 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
+    def wait_live(self, timeout=3.0):
+        """Block until nvidia-smi has reported once (its start-up takes ~0.1-0.3 s)."""
+        t0 = time.perf_counter()
+        while self.proc and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.01)
+        self.mark = len(self.lines)
+
+    def ensure_sample(self, step, timeout=3.0):
+        """A timed region shorter than the 200 ms sampling period may see no sample: keep
+        running the same step (untimed, the numbers are already taken) until one arrives."""
+        import torch
+
+        t0 = time.perf_counter()
+        while self.proc and len(self.lines) <= getattr(self, "mark", 0) and time.perf_counter() - t0 < timeout:
+            step()
+            torch.cuda.synchronize()
+
     def __exit__(self, *exc):
         if self.proc:
             self.proc.terminate()
@@ -187,7 +204,7 @@ class ClockSampler:
     def summary(self):
         sm, smax, reasons = [], [], set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in self.lines:
+        for ln in self.lines[getattr(self, "mark", 0):] or self.lines:  # the samples of the timed steps
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -547,6 +564,7 @@ def main():
     stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     with ClockSampler(local_dev) as clocks:
+        clocks.wait_live()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
@@ -558,6 +576,7 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        clocks.ensure_sample(step)
     ms = max_over_ranks(float(sum(a.elapsed_time(b) for a, b in ev)))
     ms_per_step = ms / args.steps
     value = n / (ms_per_step / 1e3)

@@ -1301,7 +1301,7 @@ struct HubMap {
 // hubs spread over many SMs; each task rebuilds the filter (dv bits, well
 // below its probe count) and writes a partial merged per hub in task order.
 #ifndef EFG_HUB_ROWS
-#define EFG_HUB_ROWS 16384  // k_mid_big 10.40 / 10.28 / 10.26 ms at 4096 / 8192 / 16384 (r02)
+#define EFG_HUB_ROWS 8192  // k_mid_big R-MAT22 10.40 / 10.28 / 10.26 ms at 4096 / 8192 / 16384; Chung-Lu 0.90 at 8192, 1.31 at 16384 (r02)
 #endif
 constexpr int64_t kHubRows = EFG_HUB_ROWS;
 

@@ -9,7 +9,7 @@ for lib in "$@"; do
 done
 for rep in 1 2; do
   for lib in "$@"; do
-    EFG_LIB=$(realpath $lib) python bench.py --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3 > gpurun_out/abk.log 2>&1 || tail -5 gpurun_out/abk.log
+    EFG_LIB=$(realpath $lib) python bench.py --config ${CONFIG:-rmat22} --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 3 > gpurun_out/abk.log 2>&1 || tail -5 gpurun_out/abk.log
     python - "$lib" "$KERNELS" <<'P'
 import json, sys
 d = json.loads([x for x in open('gpurun_out/abk.log') if x.startswith('{')][-1])

@@ -48,12 +48,21 @@ constexpr int kRowUnroll = 4;
 #define EFG_ROW_THREADS 256
 #endif
 constexpr int kRowThreads = EFG_ROW_THREADS;
+#ifndef EFG_SORT_LARGE_PER_SM
+#define EFG_SORT_LARGE_PER_SM 8
+#endif
+#ifndef EFG_SORT_SMALL_PER_SM
+#define EFG_SORT_SMALL_PER_SM 32  // k_sort_small ms (r02): 8: 0.46, 16: 0.41, 32: 0.38-0.39
+#endif
 // Rows longer than kRowBig (hubs) would be one warp's serial chain of
 // dependent loads (the top R-MAT22 hub: 965 steps, ~1 ms); with the
 // orientation they go to the first kRowBigBlocks CTAs of the same launch,
 // which walk the ranks in descending degree order, a CTA per row.
 constexpr int32_t kRowBig = 2048;
-constexpr int kRowBigBlocks = 148;
+#ifndef EFG_ROW_BIG_BLOCKS
+#define EFG_ROW_BIG_BLOCKS 296  // hub-row CTAs of k_row_sums (r02: 74: 1.33 ms, 148: 0.96, 296: 0.89, 592-888: 0.885)
+#endif
+constexpr int kRowBigBlocks = EFG_ROW_BIG_BLOCKS;
 
 __device__ __forceinline__ void row_sums_big(const int64_t* __restrict__ offsets, const int32_t* __restrict__ nbr,
                                              int32_t* __restrict__ nd, const int32_t* __restrict__ deg,
@@ -573,10 +582,11 @@ void prepare_tail(Context& ctx, Prepared& P, bool need_orientation, bool need_sl
     // the side stream while the short rows and the slot table fill the GPU
     EFG_CUDA_CHECK(cudaEventRecord(ctx.side_ev[0], s));
     EFG_CUDA_CHECK(cudaStreamWaitEvent(ctx.side_stream, ctx.side_ev[0], 0));
-    EFG_LAUNCH(k_sort_large, 4 * ctx.num_sms, B, 0, ctx.side_stream, g.offsets, P.dplus, n, P.by_rank,
+    EFG_LAUNCH(k_sort_large, EFG_SORT_LARGE_PER_SM * ctx.num_sms, B, 0, ctx.side_stream, g.offsets, P.dplus, n, P.by_rank,
                P.deg_by_rank, P.adjj, P.adjd, scratch, r0, r1);
     EFG_CUDA_CHECK(cudaEventRecord(ctx.side_ev[1], ctx.side_stream));
-    EFG_LAUNCH(k_sort_small, std::min<int64_t>(ceil_div(groups * 32, B), 16 * ctx.num_sms), B, 0, s, g.offsets,
+    EFG_LAUNCH(k_sort_small, std::min<int64_t>(ceil_div(groups * 32, B), EFG_SORT_SMALL_PER_SM * ctx.num_sms), B, 0, s,
+               g.offsets,
                P.dplus, r0, r1, P.deg_by_rank, P.adjj, P.adjd, scratch);
   }
   if (need_slot_table) {

@@ -1515,6 +1515,15 @@ constexpr int kMidUnrollBm = EFG_MID_UNROLL_BM;
 #define EFG_MID_ADAPT_U 1
 #endif
 constexpr bool kMidAdaptU = EFG_MID_ADAPT_U;
+#ifndef EFG_MID_U1_SPAN
+#define EFG_MID_U1_SPAN 32
+#endif
+#ifndef EFG_MID_U2_SPAN
+#define EFG_MID_U2_SPAN 64
+#endif
+#ifndef EFG_MID_H1_SPAN
+#define EFG_MID_H1_SPAN 32
+#endif
 
 
 
@@ -1537,6 +1546,9 @@ struct MidBig {
 #ifndef EFG_MID_SMALL_MINB
 #define EFG_MID_SMALL_MINB 16
 #endif
+#ifndef EFG_MID_SMALL_UNROLL
+#define EFG_MID_SMALL_UNROLL 2
+#endif
 #ifndef EFG_MID_SMALL_CHUNK
 #define EFG_MID_SMALL_CHUNK 256
 #endif
@@ -1544,7 +1556,7 @@ struct MidSmall {
   static constexpr int kThreads = EFG_MID_SMALL_THREADS, kNB = 128, kLgNB = 7, kMaxP = kMidSmallDeg,
                        kChunk = EFG_MID_SMALL_CHUNK;
   static constexpr int kBmWords = 0;
-  static constexpr int kUnrollHash = 2;
+  static constexpr int kUnrollHash = EFG_MID_SMALL_UNROLL;
 };
 constexpr int kListScale = 40;      // P = rint(G * 2^40)
 constexpr int64_t kListMaxDeg = 1000000;  // |G(3 dmax)| < 32
@@ -2044,13 +2056,13 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
         // (distinct labels below lim), so short scans take one step of 32 / 64 lanes
         // instead of a 128-lane step
         const int32_t span = min(pu, lim);
-        if (use_bm && kMidAdaptU && span <= 32)
+        if (use_bm && kMidAdaptU && span <= EFG_MID_U1_SPAN)
           mid_scan_bm<1>(a.adjj + psu, pu, lim, a.PQ, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
-        else if (use_bm && kMidAdaptU && span <= 64)
+        else if (use_bm && kMidAdaptU && span <= EFG_MID_U2_SPAN)
           mid_scan_bm<2>(a.adjj + psu, pu, lim, a.PQ, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
         else if (use_bm)
           mid_scan_bm<kMidUnrollBm>(a.adjj + psu, pu, lim, a.PQ, (uint32_t)(dv + du), bmb, db, lane, hit, a.flen);
-        else if (kMidAdaptU && span <= 32)
+        else if (kMidAdaptU && span <= EFG_MID_H1_SPAN)
           mid_scan_hash<1>(a.adjj + psu, pu, lim, a.PQ, (uint32_t)(dv + du), kb, vb, lgl, lane, hit, a.flen);
         else
           mid_scan_hash<C::kUnrollHash>(a.adjj + psu, pu, lim, a.PQ, (uint32_t)(dv + du), kb, vb, lgl, lane, hit,

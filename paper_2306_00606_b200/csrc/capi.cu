@@ -392,14 +392,17 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
     // pageable caller memory (a reference Graph's numpy arrays) goes through
     // the pinned staging ring (stage.cu); page-locked memory is copied directly
     const bool stage_off = efg::is_pageable(offsets), stage_nbr = efg::is_pageable(neighbors);
+    int workers = (int)std::max(1u, std::thread::hardware_concurrency() / 2);
+    if (const char* e = getenv("EFG_STAGE_WORKERS")) workers = std::max(1, atoi(e));  // tuning (tools/ab_env.sh)
     struct JoinGuard {  // never leave staging workers running past this call
       efg::HostStager& s;
       ~JoinGuard() {
+        s.close();
         for (auto& w : s.workers) w.join();
         s.workers.clear();
       }
     } join_guard{c.stager};
-    c.stager.begin();
+    c.stager.begin(stage_off || stage_nbr ? workers : 0);
     auto h2d = [&](void* dst, const void* src, size_t bytes, bool staged) {
       if (staged)
         c.stager.add(c.copy_stream, dst, src, bytes);
@@ -448,9 +451,7 @@ int efg_expected_force(efg_ctx* ctx, const int64_t* offsets, const int32_t* neig
       stg.ready[k] = c.chunk_ev[1 + k];
     }
     EFG_CUDA_CHECK(cudaEventRecord(ev[1], c.copy_stream));  // all inputs resident
-    int workers = (int)std::max(1u, std::thread::hardware_concurrency() / 2);
-    if (const char* e = getenv("EFG_STAGE_WORKERS")) workers = std::max(1, atoi(e));  // tuning (tools/ab_env.sh)
-    c.stager.start(workers);
+    c.stager.close();  // every piece is on the stream
     EFG_CUDA_CHECK(cudaStreamWaitEvent(c.stream, c.chunk_ev[0], 0));
     double* d_ef = c.buf("o_ef").as<double>(n);
     int64_t* d_tot = c.buf("o_tot").as<int64_t>(n);

@@ -48,12 +48,19 @@ struct Profiler {
 };
 
 // Pageable host -> device copies through a ring of pinned buffers filled by
-// host worker threads (stage.cu).  add() enqueues a range's pieces on a
-// stream (gate callback + copy + event each); start() launches the workers;
-// finish() joins them (call once every gate has been enqueued).
+// host worker threads (stage.cu).  begin(threads) starts the workers; add()
+// enqueues a range's pieces on a stream (gate callback + copy + event each)
+// and hands them to the workers as it goes; close() says no more pieces come;
+// finish() joins the workers.
 struct HostStager {
-  static constexpr size_t kPiece = size_t(8) << 20;
-  static constexpr int kRing = 16;
+#ifndef EFG_STAGE_PIECE_MB
+#define EFG_STAGE_PIECE_MB 8
+#endif
+#ifndef EFG_STAGE_RING
+#define EFG_STAGE_RING 16
+#endif
+  static constexpr size_t kPiece = size_t(EFG_STAGE_PIECE_MB) << 20;
+  static constexpr int kRing = EFG_STAGE_RING;
   struct Piece {
     const char* src;
     char* dst;
@@ -64,22 +71,26 @@ struct HostStager {
     int64_t idx;
   };
   std::vector<char*> bufs;        // kRing pinned buffers of kPiece bytes
-  std::vector<cudaEvent_t> ev;    // per piece: its device copy done
-  std::vector<Piece> pieces;
+  std::vector<cudaEvent_t> ev;    // per piece: its device copy done (guarded by mu)
+  std::vector<Piece> pieces;      // guarded by mu
   std::deque<Gate> gates;         // stable addresses (callback arguments)
   std::deque<uint8_t> ready;      // guarded by mu
+  size_t piece = kPiece;          // this call's piece size (<= kPiece; EFG_STAGE_PIECE_KB, tests)
+  int64_t enqueued = 0;           // pieces whose gate / copy / event are on the stream (guarded by mu)
+  bool closed = false;            // guarded by mu
   std::mutex mu;
   std::condition_variable cv;
   std::vector<std::thread> workers;
   bool failed = false;
-  void begin();
+  void begin(int threads);
   void add(cudaStream_t s, void* dst, const void* src, size_t bytes);
-  void start(int threads);
+  void close();
   void finish();
   ~HostStager();
 
  private:
   void ensure(size_t npieces);
+  void work(int t, int T);
 };
 bool is_pageable(const void* p);
 

@@ -6,18 +6,18 @@
 // copy stream moves each piece to the device as soon as it is staged, so the
 // PCIe copy, the host copies and the engine's per-chunk work overlap.
 //
-// Stream order: every piece is enqueued up front (before the engine waits on
-// the chunk events) as
+// Stream order: every piece is enqueued as
 //     [host gate: piece staged] -> cudaMemcpyAsync(dst, ring[b]) -> event[p]
 // on the copy stream.  The gate is a cudaLaunchHostFunc callback that blocks
-// until a worker thread has filled the piece's ring buffer.  Worker t stages
-// pieces t, t+T, ... in increasing order; before reusing ring buffer b it
-// waits for event[p - R] (the device copy of the piece that used b last).
-// That copy depends only on gates <= p - R, all owned by pieces a worker
-// reaches before p, so the waits cannot form a cycle.
+// until a worker thread has filled the piece's ring buffer.  The workers run
+// while the pieces are enqueued (a long input's gates, copies and events can
+// fill the stream's queue, and then the enqueue waits for gates that only the
+// workers open); worker t stages pieces t, t+T, ... in increasing order, each
+// once it is on the stream (see work()).
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <thread>
 
@@ -45,15 +45,22 @@ bool is_pageable(const void* p) {
   return at.type == cudaMemoryTypeUnregistered;
 }
 
-void HostStager::begin() {
-  pieces.clear();
+void HostStager::begin(int threads) {
+  for (auto& w : workers) w.join();  // (none: the previous call's finish() joined them)
+  workers.clear();
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    pieces.clear();
+    ready.clear();
+    enqueued = 0;
+    closed = false;
+    failed = false;
+  }
   gates.clear();
-  std::lock_guard<std::mutex> lock(mu);
-  ready.clear();
-  failed = false;
-}
-
-void HostStager::ensure(size_t npieces) {
+  piece = kPiece;
+  if (const char* e = getenv("EFG_STAGE_PIECE_KB"))  // smaller pieces (tests: many more stream operations)
+    piece = std::max<size_t>(4096, std::min<size_t>(kPiece, (size_t)atoll(e) << 10));
+  if (threads <= 0) return;  // nothing pageable in this call
   if (bufs.empty()) {
     for (int b = 0; b < kRing; ++b) {
       void* p = nullptr;
@@ -61,9 +68,22 @@ void HostStager::ensure(size_t npieces) {
       bufs.push_back(static_cast<char*>(p));
     }
   }
-  while (ev.size() < npieces) {
+  // Workers run from the start: the stream's queue of gates, copies and events
+  // may fill while add() enqueues (the enqueue then blocks until the stream
+  // drains), and only staged pieces open the gates that drain it.
+  const int T = std::max(1, std::min<int>(threads, kRing / 2));
+  for (int t = 0; t < T; ++t) workers.emplace_back([this, t, T] { work(t, T); });
+}
+
+void HostStager::ensure(size_t npieces) {
+  while (true) {
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (ev.size() >= npieces) return;
+    }
     cudaEvent_t e;
     EFG_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    std::lock_guard<std::mutex> lock(mu);
     ev.push_back(e);
   }
 }
@@ -71,40 +91,70 @@ void HostStager::ensure(size_t npieces) {
 void HostStager::add(cudaStream_t s, void* dst, const void* src, size_t bytes) {
   const char* from = static_cast<const char*>(src);
   char* to = static_cast<char*>(dst);
-  for (size_t off = 0; off < bytes; off += kPiece) pieces.push_back({from + off, to + off, std::min(kPiece, bytes - off)});
-  ensure(pieces.size());
-  // enqueue only the new pieces (earlier add() calls queued theirs)
-  const size_t first = gates.size();
+  size_t first, last;
   {
-    std::lock_guard<std::mutex> lock(mu);  // gate callbacks of earlier pieces may be reading `ready`
-    while (ready.size() < pieces.size()) ready.push_back(0);
+    std::lock_guard<std::mutex> lock(mu);
+    first = pieces.size();
+    for (size_t off = 0; off < bytes; off += piece)
+      pieces.push_back({from + off, to + off, std::min(piece, bytes - off)});
+    last = pieces.size();
+    while (ready.size() < last) ready.push_back(0);
   }
-  for (size_t p = first; p < pieces.size(); ++p) gates.push_back({this, (int64_t)p});
-  for (size_t p = first; p < pieces.size(); ++p) {
+  ensure(last);
+  for (size_t p = first; p < last; ++p) gates.push_back({this, (int64_t)p});
+  for (size_t p = first; p < last; ++p) {
+    cudaEvent_t e;
+    size_t nbytes;
+    char* d;
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      e = ev[p];
+      nbytes = pieces[p].bytes;
+      d = pieces[p].dst;
+    }
     EFG_CUDA_CHECK(cudaLaunchHostFunc(s, gate_fn, &gates[p]));
-    EFG_CUDA_CHECK(cudaMemcpyAsync(pieces[p].dst, bufs[p % kRing], pieces[p].bytes, cudaMemcpyHostToDevice, s));
-    EFG_CUDA_CHECK(cudaEventRecord(ev[p], s));
+    EFG_CUDA_CHECK(cudaMemcpyAsync(d, bufs[p % kRing], nbytes, cudaMemcpyHostToDevice, s));
+    EFG_CUDA_CHECK(cudaEventRecord(e, s));
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      enqueued = (int64_t)p + 1;  // its ring buffer's previous copy event is recorded: a worker may stage it
+    }
+    cv.notify_all();
   }
 }
 
-void HostStager::start(int threads) {
-  const int64_t np = (int64_t)pieces.size();
-  if (np == 0) return;
-  const int T = std::max(1, std::min<int>(threads, kRing / 2));
-  for (int t = 0; t < T; ++t) {
-    workers.emplace_back([this, t, T, np] {
-      for (int64_t p = t; p < np; p += T) {
-        bool ok = true;
-        if (p >= kRing && cudaEventSynchronize(ev[p - kRing]) != cudaSuccess) ok = false;
-        if (ok) std::memcpy(bufs[p % kRing], pieces[p].src, pieces[p].bytes);
-        {
-          std::lock_guard<std::mutex> lock(mu);
-          if (!ok) failed = true;
-          ready[p] = 1;  // even on failure: a gate must never block forever
-        }
-        cv.notify_all();
-      }
-    });
+void HostStager::close() {
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    closed = true;
+  }
+  cv.notify_all();
+}
+
+// Worker t stages pieces t, t+T, ... in increasing order, each once it is on
+// the stream; before reusing ring buffer b it waits for event[p - kRing] (the
+// device copy of the piece that used b last).  That copy depends only on gates
+// <= p - kRing, all owned by pieces a worker reaches before p: no cycle.
+void HostStager::work(int t, int T) {
+  for (int64_t p = t;; p += T) {
+    Piece pc;
+    cudaEvent_t prev = nullptr;
+    {
+      std::unique_lock<std::mutex> lock(mu);
+      cv.wait(lock, [&] { return p < enqueued || closed; });
+      if (p >= enqueued) return;  // closed and no such piece
+      pc = pieces[p];
+      if (p >= kRing) prev = ev[p - kRing];
+    }
+    bool ok = true;
+    if (prev && cudaEventSynchronize(prev) != cudaSuccess) ok = false;
+    if (ok) std::memcpy(bufs[p % kRing], pc.src, pc.bytes);
+    {
+      std::lock_guard<std::mutex> lock(mu);
+      if (!ok) failed = true;
+      ready[p] = 1;  // even on failure: a gate must never block forever
+    }
+    cv.notify_all();
   }
 }
 
@@ -115,6 +165,7 @@ void HostStager::finish() {
 }
 
 HostStager::~HostStager() {
+  close();
   for (auto& w : workers) w.join();
   for (auto p : bufs) cudaFreeHost(p);
   for (auto e : ev) cudaEventDestroy(e);

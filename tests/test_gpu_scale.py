@@ -244,8 +244,9 @@ def test_star_beyond_listing_bound():
     assert np.array_equal(r.cluster_total, deg * (deg - 1) + np.add.reduceat(deg[g.neighbors], g.offsets[:-1]) - deg)
 
 
-@pytest.mark.parametrize("splits", ["none", "40", "15,35,62", "5,10,20,40,60,80,90"])
-def test_staged_chunks_bitwise(rmat18, splits, monkeypatch):
+@pytest.mark.parametrize("splits,piece_kb", [("none", None), ("40", None), ("15,35,62", None),
+                                             ("5,10,20,40,60,80,90", None), ("15,35,62", 64)])
+def test_staged_chunks_bitwise(rmat18, splits, piece_kb, monkeypatch):
     # host inputs reach the device in row chunks and the engine takes up each
     # chunk's rows as it lands (class lists selected once, per-chunk runs from
     # k_chunk_counts): any split gives the device-resident result bit for bit,
@@ -260,6 +261,9 @@ def test_staged_chunks_bitwise(rmat18, splits, monkeypatch):
     D.ef_range(dg, 0, n, *full)
     want = [x.cpu().numpy() for x in full]
     monkeypatch.setenv("EFG_STAGE_SPLITS", splits)
+    if piece_kb:  # pageable staging in 64 KB pieces: ~300 gate / copy / event triples, more than a
+        # stream queue holds before the workers open the first gates (enqueue and staging overlap)
+        monkeypatch.setenv("EFG_STAGE_PIECE_KB", str(piece_kb))
     pageable = Graph(n, rmat18.m, np.array(rmat18.offsets, copy=True), np.array(rmat18.neighbors, copy=True), None)
     for g in (rmat18, pageable):
         r = efg.ef_cluster_centric(g)

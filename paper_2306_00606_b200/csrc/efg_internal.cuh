@@ -76,6 +76,13 @@ struct HostStager {
   std::deque<Gate> gates;         // stable addresses (callback arguments)
   std::deque<uint8_t> ready;      // guarded by mu
   size_t piece = kPiece;          // this call's piece size (<= kPiece; EFG_STAGE_PIECE_KB, tests)
+  // device-side gates: the copy stream waits on a flag in mapped page-locked
+  // memory (cuStreamWaitValue32) that the worker sets after staging the piece
+  static constexpr int64_t kFlags = int64_t(1) << 20;
+  uint32_t* flags_h = nullptr;    // [kFlags] host view
+  void* flags_d = nullptr;        // device view
+  void* wait_fn = nullptr;        // cuStreamWaitValue32 (driver entry point), or null: host-function gates
+  int64_t flags_used = 0;         // flags set by the previous call (reset at begin)
   int64_t enqueued = 0;           // pieces whose gate / copy / event are on the stream (guarded by mu)
   bool closed = false;            // guarded by mu
   std::mutex mu;

@@ -14,9 +14,11 @@
 // fill the stream's queue, and then the enqueue waits for gates that only the
 // workers open); worker t stages pieces t, t+T, ... in increasing order, each
 // once it is on the stream (see work()).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <thread>
@@ -24,6 +26,11 @@
 #include "efg_internal.cuh"
 
 namespace efg {
+
+#ifndef EFG_STAGE_WAITVALUE
+#define EFG_STAGE_WAITVALUE 1
+#endif
+constexpr bool kStageWaitValue = EFG_STAGE_WAITVALUE;
 
 namespace {
 void CUDART_CB gate_fn(void* arg) {
@@ -57,10 +64,32 @@ void HostStager::begin(int threads) {
     failed = false;
   }
   gates.clear();
+  if (flags_h && flags_used) std::memset(flags_h, 0, (size_t)flags_used * sizeof(uint32_t));  // last call's waits are done
+  flags_used = 0;
   piece = kPiece;
   if (const char* e = getenv("EFG_STAGE_PIECE_KB"))  // smaller pieces (tests: many more stream operations)
     piece = std::max<size_t>(4096, std::min<size_t>(kPiece, (size_t)atoll(e) << 10));
   if (threads <= 0) return;  // nothing pageable in this call
+  if (kStageWaitValue && !flags_h) {
+    cudaDriverEntryPointQueryResult q{};
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn) {
+      void* h = nullptr;
+      if (cudaHostAlloc(&h, kFlags * sizeof(uint32_t), cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess) {
+        std::memset(h, 0, kFlags * sizeof(uint32_t));
+        void* d = nullptr;
+        if (cudaHostGetDevicePointer(&d, h, 0) == cudaSuccess) {
+          flags_h = static_cast<uint32_t*>(h);
+          flags_d = d;
+          wait_fn = fn;
+        } else {
+          cudaFreeHost(h);
+        }
+      }
+    }
+    cudaGetLastError();  // a failed probe leaves the host-function gates in place
+  }
   if (bufs.empty()) {
     for (int b = 0; b < kRing; ++b) {
       void* p = nullptr;
@@ -112,7 +141,15 @@ void HostStager::add(cudaStream_t s, void* dst, const void* src, size_t bytes) {
       nbytes = pieces[p].bytes;
       d = pieces[p].dst;
     }
-    EFG_CUDA_CHECK(cudaLaunchHostFunc(s, gate_fn, &gates[p]));
+    if (wait_fn && (int64_t)p < kFlags) {
+      using WaitFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+      const CUresult r = reinterpret_cast<WaitFn>(wait_fn)(
+          (CUstream)s, (CUdeviceptr)(static_cast<char*>(flags_d) + p * sizeof(uint32_t)), 1u, CU_STREAM_WAIT_VALUE_GEQ);
+      if (r != CUDA_SUCCESS) throw Error(EFG_CUDA, "cuStreamWaitValue32 failed");
+      flags_used = (int64_t)p + 1;
+    } else {
+      EFG_CUDA_CHECK(cudaLaunchHostFunc(s, gate_fn, &gates[p]));
+    }
     EFG_CUDA_CHECK(cudaMemcpyAsync(d, bufs[p % kRing], nbytes, cudaMemcpyHostToDevice, s));
     EFG_CUDA_CHECK(cudaEventRecord(e, s));
     {
@@ -154,6 +191,10 @@ void HostStager::work(int t, int T) {
       if (!ok) failed = true;
       ready[p] = 1;  // even on failure: a gate must never block forever
     }
+    if (flags_h && p < kFlags) {  // the device-side gate: the staged bytes are visible before the flag
+      std::atomic_thread_fence(std::memory_order_seq_cst);
+      __atomic_store_n(flags_h + p, 1u, __ATOMIC_RELEASE);
+    }
     cv.notify_all();
   }
 }
@@ -167,6 +208,7 @@ void HostStager::finish() {
 HostStager::~HostStager() {
   close();
   for (auto& w : workers) w.join();
+  if (flags_h) cudaFreeHost(flags_h);
   for (auto p : bufs) cudaFreeHost(p);
   for (auto e : ev) cudaEventDestroy(e);
 }

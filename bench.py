@@ -163,10 +163,14 @@ class ClockSampler:
         self.lines = []
 
     def __enter__(self):
+        if os.environ.get("EFG_BENCH_CLOCKS") == "off":  # diagnostics only
+            return self
+        fields = os.environ.get("EFG_BENCH_CLOCK_FIELDS", self.FIELDS)
+        period = os.environ.get("EFG_BENCH_CLOCK_MS", "200")
         try:
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={fields}", "--format=csv,noheader,nounits",
+                 "-lms", period], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             threading.Thread(target=self._read, daemon=True).start()
         except OSError:
             self.proc = None
@@ -563,6 +567,10 @@ def main():
     # ---- timed region: K steps, L2 flushed between steps, CUDA events on the stream
     stream = torch.cuda.current_stream()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    import gc
+
+    gc.collect()
+    gc.disable()  # no collector pause inside a timed step (the step's host syncs would stretch it)
     with ClockSampler(local_dev) as clocks:
         clocks.wait_live()
         if world > 1:
@@ -577,7 +585,9 @@ def main():
         if world > 1:
             dist.barrier()
         clocks.ensure_sample(step)
-    ms = max_over_ranks(float(sum(a.elapsed_time(b) for a, b in ev)))
+    gc.enable()
+    step_ms = [a.elapsed_time(b) for a, b in ev]  # this rank's per-step device times (diagnostic)
+    ms = max_over_ranks(float(sum(step_ms)))
     ms_per_step = ms / args.steps
     value = n / (ms_per_step / 1e3)
 
@@ -724,7 +734,8 @@ def main():
     line = {
         "metric": METRICS[args.config],
         "value": value, "unit": "seeds/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "ms_per_step": ms_per_step, "step_ms": [round(x, 3) for x in step_ms], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
         "dtype": "f64+int64", "data": "synthetic",
         "config": {"workload": CONFIGS[args.config], "n": n, "m": m, "engine": args.engine,
                    "parallelism": (f"whole-graph pass in {world} parts: rows per part, Adj+ row exchange "

@@ -1932,8 +1932,6 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
   const uint32_t kb = (uint32_t)__cvta_generic_to_shared(sm.lk), vb = (uint32_t)__cvta_generic_to_shared(sm.lv);
   const uint32_t eb_lo = (uint32_t)__cvta_generic_to_shared(sm.elo), eb_hi = (uint32_t)__cvta_generic_to_shared(sm.ehi),
                  eb_c = (uint32_t)__cvta_generic_to_shared(sm.ec), db = (uint32_t)__cvta_generic_to_shared(sm.edeg);
-  __shared__ int64_t red_h[kMidThreads / 32], red_l[kMidThreads / 32];
-  __shared__ uint32_t red_c[kMidThreads / 32];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   constexpr int NW = kMidThreads / 32;
   int32_t v, x0, x1;
@@ -2088,14 +2086,12 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
       }
     }
   }
-  const int64_t vh = block_sum<kMidThreads>(av.hi, red_h);
-  const int64_t vl = block_sum<kMidThreads>(av.lo, red_l);
-  const uint32_t vc = block_sum<kMidThreads>(av.c, red_c);
-  if (threadIdx.x == 0 && vc) {
+  // v's own share: each warp's lane 0 holds its rows' part (integer words, any order): no block reduction
+  if (lane == 0 && av.c) {
     unsigned long long* q = a.acc + 4 * (int64_t)v;
-    atomicAdd(q, (unsigned long long)vh);
-    atomicAdd(q + 1, (unsigned long long)vl);
-    atomicAdd(q + 2, (unsigned long long)vc);
+    atomicAdd(q, (unsigned long long)av.hi);
+    atomicAdd(q + 1, (unsigned long long)av.lo);
+    atomicAdd(q + 2, (unsigned long long)av.c);
   }
 }
 

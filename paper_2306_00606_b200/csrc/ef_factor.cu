@@ -1971,6 +1971,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
       for (int b = threadIdx.x; b < (1 << lgl); b += blockDim.x) sm.lk[b] = make_int4(-1, -1, -1, -1);
     }
     __syncthreads();
+    if (threadIdx.x == 0) sm.nrows = 0;  // the part's first chunk count (read after the next barrier)
     for (int t = threadIdx.x; t < np; t += blockDim.x) {
       const int32_t l = __ldg(a.adjj + pb + q0 + t);
       if (use_bm) atomicOr(&sm.bmp[l >> 5].x, 1u << (l & 31));
@@ -2014,8 +2015,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
     const uint32_t bmb = (uint32_t)__cvta_generic_to_shared(sm.bmp);
     for (int32_t c0 = x0; c0 < x1; c0 += kMidChunk) {
       // compact the chunk's rows (lower-ranked u with |Adj+(u)| >= 2) into shared memory
-      __syncthreads();
-      if (threadIdx.x == 0) sm.nrows = 0;
+      // (the count was zeroed before the part's setup barriers / in the previous chunk's flush)
       __syncthreads();
       for (int32_t x = c0 + threadIdx.x; x < min(x1, c0 + kMidChunk); x += blockDim.x) {
         const int64_t e = ob + x;
@@ -2076,6 +2076,7 @@ __device__ __forceinline__ void mid_block_body(const MArgs& a, const HubTasks& t
       }
       __syncthreads();
       for (int t = threadIdx.x; t < np; t += blockDim.x) {
+        if (t == 0) sm.nrows = 0;  // the next chunk's count (read again after its first barrier)
         if (sm.ec[t]) {
           const uint64_t q = ((uint64_t)sm.ehi[t] << 22) + sm.elo[t];
           red_node(a.acc, sm.node[t], -(int64_t)q, sm.ec[t]);

@@ -402,8 +402,8 @@ constexpr int kExpK = 15, kExpTiles = 64, kExpGrid = 128, kExpMin = 12, kExpMinD
 #ifndef EFG_CTAB_WARP_D
 #define EFG_CTAB_WARP_D 128
 #endif
-constexpr int kCtabWarpD = EFG_CTAB_WARP_D;  // rows with fewer distinct degrees: a warp each (<= kExpMinD, <= 128)
-static_assert(kCtabWarpD <= 128 && kCtabWarpD <= kExpMinD, "k_ctab_warp stages at most 128 inputs, unexpanded");
+constexpr int kCtabWarpD = EFG_CTAB_WARP_D;  // rows with fewer distinct degrees: a warp each, direct
+static_assert(kCtabWarpD % 32 == 0 && kCtabWarpD <= 512, "k_ctab_warp: 32 x OUT staged inputs (rows past kExpMinD go direct there)");
 constexpr double kExpRatio = 0.135;
 constexpr float kExpGrowth = 1.25f;  // tile t: x in [base (g^t - 1), base (g^(t+1) - 1))
 
@@ -433,13 +433,14 @@ __device__ __forceinline__ void ctab_outputs(const int32_t* __restrict__ sx, con
 #define EFG_CTAB_WARPS 4  // 4 / 8 / 16 warps per CTA: 0.512 / 0.538 / 0.71 ms (r02)
 #endif
 constexpr int kCtabWarps = EFG_CTAB_WARPS;
+template <int OUT>
 __global__ void __launch_bounds__(kCtabWarps * 32)
 k_ctab_warp(const int32_t* __restrict__ rows, int64_t count, const int64_t* __restrict__ offsets,
             const int32_t* __restrict__ dcnt, const int32_t* __restrict__ hkey, const int32_t* __restrict__ hcnt,
             const int32_t* __restrict__ deg, const double* __restrict__ F, double* __restrict__ ctab, int64_t flen,
             int max_d) {
-  __shared__ int32_t sx[kCtabWarps][128];
-  __shared__ double sh[kCtabWarps][128];
+  __shared__ int32_t sx[kCtabWarps][32 * OUT];
+  __shared__ double sh[kCtabWarps][32 * OUT];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t q = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (q >= count) return;
@@ -453,11 +454,11 @@ k_ctab_warp(const int32_t* __restrict__ rows, int64_t count, const int64_t* __re
     sh[w][a] = (double)hcnt[b + a];
   }
   __syncwarp();
-  int64_t base[4];
-  int32_t yk[4];
-  double acc[4];
+  int64_t base[OUT];
+  int32_t yk[OUT];
+  double acc[OUT];
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < OUT; ++k) {
     const int o = lane + 32 * k;
     yk[k] = o < D ? sx[w][o] : sx[w][0];  // past-the-end outputs shadow the first one
     base[k] = (int64_t)yk[k] + di - 4;
@@ -468,11 +469,11 @@ k_ctab_warp(const int32_t* __restrict__ rows, int64_t count, const int64_t* __re
     const int32_t x = sx[w][a];
     const double h = sh[w][a];
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < OUT; ++k)
       if (k < K) acc[k] = fma(h, __ldg(F + EFG_CLAMP(base[k] + x, flen)), acc[k]);
   }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < OUT; ++k) {
     const int o = lane + 32 * k;
     if (o < D) ctab[b + o] = acc[k] - __ldg(F + EFG_CLAMP(base[k] + yk[k], flen));
   }
@@ -2634,7 +2635,7 @@ PrepInfo ef_factorized(Context& ctx, const CSRView& g, const Staging& stg, SeedR
       EFG_LAUNCH(k_ctab_block, nb, kCtabThreads, 0, s, L.cb + lstart(c, kCB, k), nb, g.offsets, dcnt, hkey, hcnt, P.deg, P.ftab,
                  ctab, kExpMin, kExpMinD, P.ftab_len, kCtabWarpD);
       if (kCtabWarpD > 0)
-        EFG_LAUNCH(k_ctab_warp, ceil_div(nb, kCtabWarps), kCtabWarps * 32, 0, s, L.cb + lstart(c, kCB, k), nb, g.offsets, dcnt, hkey,
+        EFG_LAUNCH(k_ctab_warp<kCtabWarpD / 32>, ceil_div(nb, kCtabWarps), kCtabWarps * 32, 0, s, L.cb + lstart(c, kCB, k), nb, g.offsets, dcnt, hkey,
                    hcnt, P.deg, P.ftab, ctab, P.ftab_len, kCtabWarpD - 1);
       // chains pushed from the rows whose tables are now complete
       const int64_t ps1 = c[cslot(kHS, k)], pb = c[cslot(kHB, k)], pl = c[cslot(kHL, k)];

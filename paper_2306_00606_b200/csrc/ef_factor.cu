@@ -396,16 +396,22 @@ __global__ void k_ctab_group(const int32_t* __restrict__ rows, int64_t count, co
 // one gather per member; R-MAT22: 92 % of the terms); the rest are summed
 // term by term.  Fixed per-output summation order (deterministic).
 constexpr int kCtabStage = 1024;
-constexpr int kCtabThreads = 128;
+#ifndef EFG_CTAB_THREADS
+#define EFG_CTAB_THREADS 128
+#endif
+constexpr int kCtabThreads = EFG_CTAB_THREADS;
 constexpr int kCtabOut = 4;
-constexpr int kExpK = 15, kExpTiles = 64, kExpGrid = 128, kExpMin = 12, kExpMinD = 128;
+constexpr int kExpK = 15, kExpTiles = 64, kExpGrid = kCtabThreads, kExpMin = 12, kExpMinD = 128;
 #ifndef EFG_CTAB_WARP_D
 #define EFG_CTAB_WARP_D 128
 #endif
 constexpr int kCtabWarpD = EFG_CTAB_WARP_D;  // rows with fewer distinct degrees: a warp each, direct
 static_assert(kCtabWarpD % 32 == 0 && kCtabWarpD <= 512, "k_ctab_warp: 32 x OUT staged inputs (rows past kExpMinD go direct there)");
 constexpr double kExpRatio = 0.135;
-constexpr float kExpGrowth = 1.25f;  // tile t: x in [base (g^t - 1), base (g^(t+1) - 1))
+#ifndef EFG_EXP_GROWTH
+#define EFG_EXP_GROWTH 1.25f
+#endif
+constexpr float kExpGrowth = EFG_EXP_GROWTH;  // tile t: x in [base (g^t - 1), base (g^(t+1) - 1))
 
 template <int K>
 __device__ __forceinline__ void ctab_outputs(const int32_t* __restrict__ sx, const double* __restrict__ sh, int nq,

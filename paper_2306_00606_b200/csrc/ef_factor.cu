@@ -1739,7 +1739,9 @@ __device__ __forceinline__ void mid_scan_bm(const int32_t* __restrict__ row, int
 // continues the linear probe (rare).  Labels >= lim are never members, so no
 // clamp; a miss reads the value of slot 0 (unused) and only the Q gather and
 // the hit are predicated, as in mid_scan_bm.
-constexpr int kPosBits = 10;  // entry positions < kMidMaxP = 1024
+constexpr int kPosBits = 10;  // entry positions < kMidMaxP <= 1024
+static_assert(kMidMaxP <= (1 << kPosBits) && kMidSmallDeg <= (1 << kPosBits), "packed hash entries hold positions in kPosBits");
+static_assert(kListMaxDeg < (int64_t(1) << (32 - kPosBits)), "packed hash entries hold degrees <= kListMaxDeg above the position");
 __device__ __forceinline__ int32_t mslot_slow(uint32_t kb, uint32_t lg, uint32_t b, int32_t key) {
   const uint32_t mask = (1u << lg) - 1;
   while (true) {

@@ -1311,6 +1311,9 @@ struct HubMap {
 #define EFG_HUB_ROWS 8192  // k_mid_big R-MAT22 10.40 / 10.28 / 10.26 ms at 4096 / 8192 / 16384; Chung-Lu 0.90 at 8192, 1.31 at 16384 (r02)
 #endif
 constexpr int64_t kHubRows = EFG_HUB_ROWS;
+#ifndef EFG_MID_SMALL_DEG
+#define EFG_MID_SMALL_DEG 256  // listing middles of degree <= this in small CTAs (k_list_counts' split)
+#endif
 
 struct HubTasks {
   const int32_t* seed;  // [ntasks]
@@ -1378,8 +1381,9 @@ __device__ __forceinline__ int64_t ranks_above_deg(const int32_t* __restrict__ d
 __global__ void k_list_counts(const int32_t* __restrict__ deg_by_rank, int64_t n, int64_t* __restrict__ c,
                               int slot_s, int slot_1, int slot_2, int slot_3, int slot_hub, int slot_tasks) {
   __shared__ int64_t red[8];
-  const int64_t g32 = ranks_above_deg(deg_by_rank, n, 32), g256 = ranks_above_deg(deg_by_rank, n, 256),
+  const int64_t g32 = ranks_above_deg(deg_by_rank, n, 32), g256 = ranks_above_deg(deg_by_rank, n, EFG_MID_SMALL_DEG),
                 g1024 = ranks_above_deg(deg_by_rank, n, 1024), ghub = ranks_above_deg(deg_by_rank, n, kHashMaxDeg);
+  static_assert(EFG_MID_SMALL_DEG < 1024, "the listing's small / big split below the tr3 bound");
   int64_t t = 0;
   for (int64_t r = threadIdx.x; r < ghub; r += blockDim.x) t += ceil_div(deg_by_rank[r], kHubRows);
   t = block_sum<256>(t, red);
@@ -1534,7 +1538,7 @@ constexpr bool kMidAdaptU = EFG_MID_ADAPT_U;
 
 
 
-constexpr int kMidSmallDeg = 256;  // middle vertices of degree <= this run in small CTAs
+constexpr int kMidSmallDeg = EFG_MID_SMALL_DEG;  // middle vertices of degree <= this run in small CTAs
 
 // CTA shapes of k_mid_block: big (hub tasks and degree > kMidSmallDeg) and
 // small (32 < degree <= kMidSmallDeg, where |Adj+(v)| and the rows are few).
@@ -1560,7 +1564,7 @@ struct MidBig {
 #define EFG_MID_SMALL_CHUNK 256
 #endif
 struct MidSmall {
-  static constexpr int kThreads = EFG_MID_SMALL_THREADS, kNB = 128, kLgNB = 7, kMaxP = kMidSmallDeg,
+  static constexpr int kThreads = EFG_MID_SMALL_THREADS, kNB = 128, kLgNB = 7, kMaxP = kMidSmallDeg < 256 ? kMidSmallDeg : 256,
                        kChunk = EFG_MID_SMALL_CHUNK;
   static constexpr int kBmWords = 0;
   static constexpr int kUnrollHash = EFG_MID_SMALL_UNROLL;

@@ -177,3 +177,24 @@ def test_algorithm1_engine_matches_reference_golden(golden):
         _, _, _, T, W = O.ef_seeds(case.get("offsets"), case.get("neighbors"), threads=4)
         assert np.array_equal(r.stats["T"], T), name
         assert ef_close(r.stats["W"], W, rtol=1e-12, atol=1e-9), name
+
+
+def test_profile_timeline_of_an_end_to_end_call():
+    # efg_profile_timeline: every launch and copy of the last profiled call, in
+    # issue order, with start offsets from the call's first record
+    from paper_2306_00606_b200 import _native
+
+    g, _ = efg.generate_rmat(efg.RmatParams(scale=12, avg_degree=16, seed=3))
+    ref = efg.ef_cluster_centric(g)
+    ctx = _native.context(0)
+    ctx.profile_reset()
+    ctx.profile(True)
+    try:
+        r = efg.ef_cluster_centric(g)
+    finally:
+        ctx.profile(False)
+    tl = ctx.profile_timeline()
+    names = [t[0] for t in tl]
+    assert names[0] == "h2d" and "d2h" in names and any(nm.startswith("k_mid") for nm in names)
+    assert all(ms >= 0.0 and start >= 0.0 for _, start, ms in tl)
+    assert np.array_equal(r.ef, ref.ef)  # profiling does not change the result
